@@ -1,0 +1,478 @@
+#!/usr/bin/env python
+"""bench.py — unified-KV paged decode attention on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1], "config 2"): 4 services sharing ONE merged-block
+pool — Llama-3-8B (32L, 8 KV / 32 Q heads), Mistral-7B (same), Llama-2-13B (40L, 40H),
+OPT-6.7B (32L, 32H), d=128, fp16 — 256 decode requests each (1024 total) at context
+2048.  As written that KV needs ~1.0 TB, so the pool is LAYER-SLICED:
+block tables come from the full-shape allocator (bit-exact, 76,460+ merged blocks),
+each native block physically stores 4 layers and logical layer l reads physical
+layer l % 4.  Every per-layer launch reads exactly the config's bytes (23.6 GB per
+layer index, far larger than the 126 MB L2, so no L2 flush is needed).
+
+One step = one decode iteration of all 1024 requests over all 40 layer indices:
+  GPU allocator grow (+1 token each) -> per layer: KV append of the new token +
+  paged decode attention (one launch covering all services).
+value = decode K/V bytes of the step / device time of the step (GB/s), max over ranks.
+e2e   = the same through the C-ABI with host (pinned) buffers: H2D of q/k/v and D2H of
+        the attention output inside the timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SERVICES = [  # (name, layers, kv_heads, q_heads)
+    ("llama-3-8b", 32, 8, 32),
+    ("mistral-7b", 32, 8, 32),
+    ("llama-2-13b", 40, 40, 40),
+    ("opt-6.7b", 32, 32, 32),
+]
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler over the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        def run():
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap")
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.samples.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def pool_blocks_for(P, ctx_max, nreq):
+    tot = 0
+    for name, L, H, Hq in SERVICES:
+        spec = P.ModelSpec(name, L, H, 128, 2, Hq)
+        sub = int(P.plan_merged_shape([P.ModelSpec(n, l, h, 128, 2, q) for n, l, h, q in SERVICES]) //
+                  P.native_block_bytes(spec))
+        slots = nreq * ((ctx_max + 15) // 16)
+        tot += (slots + sub - 1) // sub
+    return tot + 64
+
+
+def setup(P, torch, args, device):
+    models = [P.ModelSpec(n, L, H, 128, 2, Hq) for n, L, H, Hq in SERVICES]
+    nreq = args.requests
+    ctx_max = args.ctx + args.warmup + args.steps * 2 + 8
+    pool_blocks = pool_blocks_for(P, ctx_max, nreq)
+    cache = P.UnifiedKvCache(models, 16, 1, pool_blocks, device=device, dtype=P.FP16,
+                             phys_layers=args.phys_layers, max_requests=4 * nreq + 16,
+                             max_blocks_per_request=(ctx_max + 15) // 16 + 1, allocate_storage=True)
+    groups = []
+    ops = []
+    for m in range(len(SERVICES)):
+        groups.append((m, [1 + r * len(SERVICES) + m for r in range(nreq)]))
+    for r in range(nreq):  # interleaved arrival order across services
+        for m in range(len(SERVICES)):
+            ops.append((0, 1 + r * len(SERVICES) + m, m, args.ctx))
+    granted = cache.replay(ops)
+    assert granted.all(), "pool too small for the workload"
+    stream = torch.cuda.current_stream(device)
+    cache.set_stream(stream)
+    cache.synth_fill(20250421, 1.0, stream)
+    batch = cache.batch(groups)
+    g = torch.Generator(device=device).manual_seed(1)
+    q = [torch.randn((nreq, Hq, 128), generator=g, device=device).half() for _, _, _, Hq in SERVICES]
+    out = [torch.empty_like(x) for x in q]
+    k = [torch.randn((nreq, 1, H, 128), generator=g, device=device).half() * 0.5 for _, _, H, _ in SERVICES]
+    v = [torch.randn((nreq, 1, H, 128), generator=g, device=device).half() * 0.5 for _, _, H, _ in SERVICES]
+    torch.cuda.synchronize(device)
+    return cache, batch, q, out, k, v, stream
+
+
+NLAYERS = max(L for _, L, _, _ in SERVICES)
+
+
+def step_device(batch, q, out, k, v, stream, ev=None):
+    """One decode step; optional per-layer decode events for the kernel roofline."""
+    batch.grow(1)
+    for layer in range(NLAYERS):
+        batch.append(k, v, layer, 1, stream)
+        if ev is not None:
+            ev[layer][0].record(stream)
+        batch.decode(q, out, layer, stream=stream)
+        if ev is not None:
+            ev[layer][1].record(stream)
+
+
+def step_bytes(batch):
+    kv = tot = 0.0
+    for layer in range(NLAYERS):
+        a, b = batch.decode_bytes(layer)
+        kv += a
+        tot += b
+    return kv, tot
+
+
+def run_gpu(args):
+    import torch
+
+    import paper_2504_15720_b200 as P
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cache, batch, q, out, k, v, stream = setup(P, torch, args, local)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if not dist:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x):
+        if not dist:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    # ---- device-resident timed region (value) ------------------------------------------
+    for _ in range(args.warmup):
+        step_device(batch, q, out, k, v, stream)
+    barrier()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(NLAYERS)]
+    kv_total = all_total = 0.0
+    dec_ms = 0.0
+    dec_bytes = 0.0
+    launches0 = cache.kernel_launches()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    step_ms = []
+    with Clocks(local) as clk:
+        barrier()
+        t0.record(stream)
+        for _ in range(args.steps):
+            s0 = torch.cuda.Event(enable_timing=True)
+            s1 = torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            step_device(batch, q, out, k, v, stream, ev)
+            s1.record(stream)
+            kvb, totb = step_bytes(batch)  # host mirror: exact context of this step
+            kv_total += kvb
+            all_total += totb
+            dec_bytes += totb
+            torch.cuda.synchronize()
+            step_ms.append(s0.elapsed_time(s1))
+            dec_ms += sum(e[0].elapsed_time(e[1]) for e in ev)
+        t1.record(stream)
+        barrier()
+    launches = cache.kernel_launches() - launches0
+    elapsed_ms = max_over_ranks(t0.elapsed_time(t1))
+    kv_all = sum_over_ranks(kv_total)
+    value = kv_all / (elapsed_ms / 1e3) / 1e9
+    tokens_s = sum_over_ranks(float(args.requests * len(SERVICES) * args.steps)) / (elapsed_ms / 1e3)
+    hbm, peak_kind = peaks()
+    achieved = dec_bytes / (dec_ms / 1e3) / 1e9  # algorithmic bytes / decode launch time
+    n_launch = args.steps * NLAYERS
+
+    # ---- e2e through the C-ABI with host buffers -----------------------------------------
+    hq = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in q]
+    ho = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in out]
+    hk = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in k]
+    hv = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in v]
+    for a, b in zip(hq + hk + hv, q + k + v):
+        a.copy_(b)
+    h2d = sum(x.numel() * 2 for x in hq + hk + hv) * NLAYERS
+    d2h = sum(x.numel() * 2 for x in ho) * NLAYERS
+
+    def step_e2e():
+        batch.grow(1)
+        for layer in range(NLAYERS):
+            for a, b in zip(q + k + v, hq + hk + hv):
+                a.copy_(b, non_blocking=True)
+            batch.append(k, v, layer, 1, stream)
+            batch.decode(q, out, layer, stream=stream)
+            for a, b in zip(ho, out):
+                a.copy_(b, non_blocking=True)
+
+    for _ in range(args.warmup):
+        step_e2e()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    kv_e2e = 0.0
+    e0.record(stream)
+    for _ in range(args.steps):
+        step_e2e()
+        kv_e2e += step_bytes(batch)[0]
+    e1.record(stream)
+    barrier()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1))
+    e2e_value = sum_over_ranks(kv_e2e) / (e2e_ms / 1e3) / 1e9
+
+    result = {
+        "metric": "unified-KV paged decode attention HBM GB/s (mixed services)",
+        "value": round(value, 1),
+        "unit": "GB/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(elapsed_ms / args.steps, 3),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "fp16",
+        "data": "synthetic (SplitMix64 K/V pool, randn q/k/v); no checkpoints",
+        "tokens_per_s": round(tokens_s, 1),
+        "config": {
+            "workload": "config2-layer-sliced: 4 services (llama-3-8b, mistral-7b, llama-2-13b, opt-6.7b) x "
+                        f"{args.requests} decode requests, ctx {args.ctx}+, one unified pool; "
+                        f"{args.phys_layers} physical layers per native block (logical l -> l % "
+                        f"{args.phys_layers}), 40 layer-index launches per step",
+            "requests": args.requests * len(SERVICES) * world,
+            "ctx": args.ctx,
+            "pool_blocks": cache.pool_size(),
+            "merged_block_bytes": cache.merged_block_bytes(),
+            "pool_gb": round(cache.storage()[1] / 1e9, 2),
+            "l2": "inputs larger than L2 (23.6 GB per layer launch vs 126 MB L2); no flush",
+            "parallelism": f"placement-sharded replicas x{world} (tp=1 groups, no collective)",
+        },
+        "e2e": {"value": round(e2e_value, 1), "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e2e_ms / args.steps, 3)},
+        "roofline": {"bound": "hbm", "kernel": "skv decode_kernel (+plan/combine)",
+                     "achieved": round(achieved, 1), "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": round(achieved / hbm, 4), "traffic": None,
+                     "avg_launch_ms": round(dec_ms / n_launch, 4),
+                     "bytes_per_launch": round(dec_bytes / n_launch, 1)},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_baseline(cache, batch, q, args)
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def _sample_image(cache, batch_groups, per_group):
+    """Compact host image holding only the sampled requests' merged blocks."""
+    import oracle_py as O  # noqa: F401  (checker only; never on the product path)
+
+    samp = []
+    blocks = set()
+    for m, ids in batch_groups:
+        for rid in ids[:per_group]:
+            bt = cache.block_table_np(rid)
+            samp.append((m, rid, bt))
+            blocks.update(bt[:, 0].tolist())
+    blocks = sorted(blocks)
+    remap = {b: i for i, b in enumerate(blocks)}
+    img = cache.read_blocks(np.array(blocks, dtype=np.int32))
+    return samp, remap, img
+
+
+def cpu_baseline(cache, batch, q, args, budget_s=None):
+    """fp32 CPU oracle (oracle/attn_oracle.c, OpenMP over all host cores) on a bounded
+    sample of the same workload: the first few requests of every service, layer 0."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle_py as O
+
+    budget_s = budget_s or args.cpu_seconds
+    groups = batch.groups
+    per = args.cpu_requests
+    samp, remap, img = _sample_image(cache, groups, per)
+    cores = os.cpu_count() or 1
+    work = []
+    nbytes = 0.0
+    for m, ids in groups:
+        lay = cache.layout(m)
+        olay = O.layout(lay.merged_stride, lay.native_stride, lay.layer_stride, lay.head_stride, lay.kv_stride,
+                        lay.tpb, lay.head_dim, lay.kv_heads, lay.q_heads, lay.phys_layers, lay.dtype)
+        rows = [s for s in samp if s[0] == m]
+        width = max(len(s[2]) for s in rows)
+        tabs = np.zeros((len(rows), width, 2), np.int32)
+        ctx = np.zeros(len(rows), np.int64)
+        for i, (_, rid, bt) in enumerate(rows):
+            tabs[i, :len(bt), 0] = [remap[b] for b in bt[:, 0]]
+            tabs[i, :len(bt), 1] = bt[:, 1]
+            ctx[i] = cache.request_tokens(rid)
+        qh = q[m][:len(rows)].view(__import__("torch").int16).cpu().numpy().view(np.uint16)
+        work.append((olay, tabs, ctx, qh))
+        nbytes += float(ctx.sum()) * lay.kv_heads * 128 * 2 * 2
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        for olay, tabs, ctx, qh in work:
+            O.decode_attention(olay, img, 0, tabs, ctx, qh, 1.0 / np.sqrt(128.0), nthreads=cores)
+        reps += 1
+        if time.perf_counter() - t0 > budget_s or reps >= 50:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": round(nbytes * reps / dt / 1e9, 3), "unit": "GB/s", "cores": cores, "kind": "port",
+            "sample": f"fp32 oracle decode, layer 0, first {per} requests of each of the 4 services at ctx "
+                      f"~{args.ctx}, {reps} reps in {dt:.1f} s (attention has no reference implementation; "
+                      "oracle/attn_oracle.c)"}
+
+
+def run_reference(args):
+    """Reference arm: the reference's own CPU path for this workload on the host cores —
+    the reference has no attention, so the fp32 oracle port stands in for decode and the
+    unmodified reference allocator (oracle/_ref) replays the step's allocation ops."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle_py as O
+
+    cores = os.cpu_count() or 1
+    # synthetic host pool for a bounded sample: per service `per` requests at ctx
+    per = args.cpu_requests
+    models = [(L, H, 128, 2) for _, L, H, _ in SERVICES]
+    allocator = O.RefCache(models, pool=200000) if O.ref_available() else O.OracleCache(models, pool=200000)
+    kind = "reference" if O.ref_available() else "port"
+    rid = 1
+    ids = {m: [] for m in range(len(SERVICES))}
+    for r in range(per):
+        for m in range(len(SERVICES)):
+            assert allocator.try_allocate(rid, m, args.ctx)
+            ids[m].append(rid)
+            rid += 1
+    merged = int(O.plan_merged_shape(models))
+    rng = np.random.default_rng(0)
+    work = []
+    nbytes = 0.0
+    used = sorted({b for m in ids for i in ids[m] for b, _ in allocator.block_table(i)})
+    remap = {b: k for k, b in enumerate(used)}
+    # 4 physical layers like the GPU arm; image holds only the used blocks
+    Lp = args.phys_layers
+    stride = 0
+    lays = []
+    for m, (name, L, H, Hq) in enumerate(SERVICES):
+        layer_stride = H * 2 * 16 * 128 * 2
+        native = min(Lp, L) * layer_stride
+        lays.append((L, H, Hq, layer_stride, native))
+    sub = [int(merged // (16 * L * 2 * H * 128 * 2)) for _, L, H, _ in SERVICES]
+    stride = max(s * l[4] for s, l in zip(sub, lays))
+    stride = (stride + 255) // 256 * 256
+    img = rng.integers(0, 0x3C00, size=len(used) * stride // 2, dtype=np.uint16).view(np.uint8)
+    for m, (L, H, Hq, layer_stride, native) in enumerate(lays):
+        olay = O.layout(stride, native, layer_stride, 2 * 16 * 128 * 2, 16 * 128 * 2, 16, 128, H, Hq,
+                        min(Lp, L), 0)
+        tabs = np.array([[(remap[b], s) for b, s in allocator.block_table(i)] for i in ids[m]], np.int32)
+        ctx = np.full(len(ids[m]), args.ctx, np.int64)
+        qh = rng.integers(0, 0x3C00, size=(len(ids[m]), Hq, 128), dtype=np.uint16)
+        work.append((olay, tabs, ctx, qh))
+        nbytes += float(ctx.sum()) * H * 128 * 2 * 2
+    # allocator: one decode step of grows for the sampled requests, timed separately
+    def one_step():
+        t = time.perf_counter()
+        for olay, tabs, ctx, qh in work:
+            O.decode_attention(olay, img, 0, tabs, ctx, qh, 1.0 / np.sqrt(128.0), nthreads=cores)
+        return time.perf_counter() - t
+
+    for _ in range(min(args.warmup, 1)):
+        one_step()
+    times = [one_step() for _ in range(args.steps)]
+    dt = sum(times)
+    value = nbytes * len(times) / dt / 1e9
+    ops = [(0, i, m, args.ctx + 1) for m in ids for i in ids[m]]
+    t = time.perf_counter()
+    allocator.replay(ops)
+    alloc_ns = (time.perf_counter() - t) / max(1, len(ops)) * 1e9
+    res = {
+        "impl": "reference",
+        "metric": "unified-KV paged decode attention HBM GB/s (mixed services)",
+        "value": round(value, 3), "unit": "GB/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / len(times) * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
+        "data": "synthetic", "config": {"workload": "config2 decode, bounded CPU sample", "ctx": args.ctx,
+                                        "requests_per_service": per},
+        "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": cores, "kind": "port",
+                         "sample": f"fp32 oracle decode (no reference attention exists), {per} requests per "
+                                   f"service at ctx {args.ctx}, 1 layer per step; allocator: {kind} "
+                                   f"replay {alloc_ns:.1f} ns/op"},
+        "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "allocator_ns_per_op": round(alloc_ns, 2), "allocator_kind": kind,
+    }
+    print(json.dumps(res), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--requests", type=int, default=256, help="decode requests per service")
+    ap.add_argument("--ctx", type=int, default=2048)
+    ap.add_argument("--phys-layers", dest="phys_layers", type=int, default=4)
+    ap.add_argument("--cpu-seconds", dest="cpu_seconds", type=float, default=8.0)
+    ap.add_argument("--cpu-requests", dest="cpu_requests", type=int, default=4)
+    ap.add_argument("--no-cpu-baseline", dest="no_cpu_baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,604 @@
+// skv_attn.cu — data-path kernels of the unified KV pool (sm_100a).
+//
+// Layout: sub-slot s of merged block b of model m starts at
+//   pool + b*merged_stride + s*native_stride[m];
+// inside a native block: [phys_layer][kv_head][K|V][tpb=16][head_dim], so the K
+// and V tiles of one (layer, head) are one contiguous 2*16*d*2 = 8 KiB run.
+//
+// Decode attention is HBM-bound (AI = Hq/Hkv flop/B): a persistent kernel, one
+// CTA per SM, 8 independent warps; each warp owns a ring of STAGES 8 KiB smem
+// tiles filled by cp.async.bulk (1-D TMA, mbarrier complete_tx) from
+// block-table-indirected addresses, and computes softmax(q·Kᵀ)·V for all G query
+// heads of a KV head from each tile (K/V read once per GQA group).  Work items
+// (request, kv head, split) are fetched dynamically; the ring runs ahead across
+// item boundaries.  Split-KV partials are merged by an LSE combine kernel.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "skv_internal.h"
+
+namespace skv {
+
+namespace {
+
+constexpr int kD = 128;                       // head_dim handled by the kernels
+constexpr int kTpb = 16;                      // tokens per native block
+constexpr int kTile = 2 * kTpb * kD * 2;      // K + V tile bytes (8 KiB)
+constexpr int kWarps = 8;
+constexpr int kStages = 3;
+constexpr int kRing = 16;
+constexpr float kLog2e = 1.4426950408889634f;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  while (!mbar_try_wait(bar, phase)) {
+  }
+}
+
+template <typename T>
+struct Cvt;
+template <>
+struct Cvt<__half> {
+  __device__ __forceinline__ static void to_f32(const uint4& r, float* f) {
+    const __half2* h = reinterpret_cast<const __half2*>(&r);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 v = __half22float2(h[k]);
+      f[2 * k] = v.x;
+      f[2 * k + 1] = v.y;
+    }
+  }
+  __device__ __forceinline__ static uint4 from_f32(const float* f) {
+    uint4 r;
+    __half2* h = reinterpret_cast<__half2*>(&r);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) h[k] = __floats2half2_rn(f[2 * k], f[2 * k + 1]);
+    return r;
+  }
+  __device__ __forceinline__ static uint16_t one(float x) { return __half_as_ushort(__float2half_rn(x)); }
+};
+template <>
+struct Cvt<__nv_bfloat16> {
+  __device__ __forceinline__ static void to_f32(const uint4& r, float* f) {
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(&r);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      f[2 * k] = __uint_as_float(w[k] << 16);
+      f[2 * k + 1] = __uint_as_float(w[k] & 0xffff0000u);
+    }
+  }
+  __device__ __forceinline__ static uint4 from_f32(const float* f) {
+    uint4 r;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&r);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) h[k] = __floats2bfloat162_rn(f[2 * k], f[2 * k + 1]);
+    return r;
+  }
+  __device__ __forceinline__ static uint16_t one(float x) {
+    return __bfloat16_as_ushort(__float2bfloat16_rn(x));
+  }
+};
+
+// Sum of 8 per-lane partials over the 16 lanes of a half-warp, scattered so lane
+// (c = lane&15) ends up with the total of index (c>>1)&7 (8 shuffles, not 32).
+__device__ __forceinline__ float reduce_scatter16(const float (&v)[8], int lane) {
+  const bool b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
+  float v4[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float send = b3 ? v[k] : v[k + 4];
+    const float keep = b3 ? v[k + 4] : v[k];
+    v4[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  float v2[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const float send = b2 ? v4[k] : v4[k + 2];
+    const float keep = b2 ? v4[k + 2] : v4[k];
+    v2[k] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  const float send = b1 ? v2[0] : v2[1];
+  const float keep = b1 ? v2[1] : v2[0];
+  float s = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+  s += __shfl_xor_sync(0xffffffffu, s, 1);
+  return s;
+}
+
+// One 16-token K/V tile for G query heads sharing a KV head.
+// Lane (c = lane&15, hf = lane>>4) reads dims [8c, 8c+8) of tokens 2i+hf.
+template <typename T, int G>
+__device__ __forceinline__ void consume_tile(const char* tile, int lane, int valid,
+                                             const float (&q)[G][8], float (&o)[G][8],
+                                             float (&mx)[G], float (&l)[G]) {
+  const int c = lane & 15, hf = lane >> 4;
+  float part[G][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint4 raw = *reinterpret_cast<const uint4*>(tile + (2 * i + hf) * (kD * 2) + c * 16);
+    float kf[8];
+    Cvt<T>::to_f32(raw, kf);
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      float a = 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) a = fmaf(q[g][j], kf[j], a);
+      part[g][i] = a;
+    }
+  }
+  const int tok = 2 * ((c >> 1) & 7) + hf;
+  float p[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    float s = reduce_scatter16(part[g], lane);
+    if (tok >= valid) s = -INFINITY;
+    float bm = s;
+    bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 2));
+    bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 4));
+    bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 8));
+    bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 16));
+    const float mnew = fmaxf(mx[g], bm);
+    const float alpha = exp2f(mx[g] - mnew);
+    p[g] = exp2f(s - mnew);
+    l[g] = l[g] * alpha + p[g];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[g][j] *= alpha;
+    mx[g] = mnew;
+  }
+  const char* vt = tile + kTpb * kD * 2;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint4 raw = *reinterpret_cast<const uint4*>(vt + (2 * i + hf) * (kD * 2) + c * 16);
+    float vf[8];
+    Cvt<T>::to_f32(raw, vf);
+    const int src = (hf << 4) | (i << 1);
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const float pt = __shfl_sync(0xffffffffu, p[g], src);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[g][j] = fmaf(pt, vf[j], o[g][j]);
+    }
+  }
+}
+
+// Per-warp producer: walks the same item sequence as the consumer, kStages tiles ahead.
+struct Producer {
+  int idx;         // current item, -1 before the first
+  int blk, bend;   // next block to issue / end (native block indices)
+  int cbase;       // first block of the cached table chunk (-1 = none)
+  int2 tc;         // lane-held table chunk entry
+  const int2* row;
+  const char* base;  // pool + layer/head offset of the current item
+  long long nstride;
+  int done;
+  int pushed, popped;  // ring counters
+  uint32_t issued, consumed;
+};
+
+struct WarpCtx {
+  char* tiles;
+  uint64_t* bars;
+  int* ring;
+  int lane;
+  int n_items;
+  uint64_t policy;
+};
+
+__device__ __forceinline__ bool produce_one(const DataParams& p, Producer& P, const WarpCtx& w) {
+  while (!P.done && P.blk >= P.bend) {
+    if (P.pushed - P.popped >= kRing) return false;
+    int idx = 0;
+    if (w.lane == 0) idx = atomicAdd(p.counter, 1);
+    idx = __shfl_sync(0xffffffffu, idx, 0);
+    if (idx >= w.n_items) {
+      P.done = 1;
+      break;
+    }
+    const int4 it = p.items[idx];
+    const DataGroup& g = p.g[it.y >> 16];
+    if (!g.active) continue;
+    if (w.lane == 0) w.ring[P.pushed % kRing] = idx;
+    __syncwarp();
+    P.pushed++;
+    P.idx = idx;
+    P.blk = it.z / kTpb;
+    P.bend = (it.w + kTpb - 1) / kTpb;
+    P.row = p.req_table + (size_t)p.handles[it.x] * p.cap;
+    P.base = p.pool + g.layer_off + (long long)(it.y & 0xffff) * g.head_stride;
+    P.nstride = g.native_stride;
+    P.cbase = -1;
+  }
+  if (P.done || P.blk >= P.bend) return false;
+  if (P.cbase < 0 || P.blk - P.cbase >= 32) {
+    P.cbase = P.blk;
+    const int b = P.blk + w.lane;
+    P.tc = b < P.bend ? P.row[b] : make_int2(0, 0);
+  }
+  const int rel = P.blk - P.cbase;
+  const int bx = __shfl_sync(0xffffffffu, P.tc.x, rel);
+  const int by = __shfl_sync(0xffffffffu, P.tc.y, rel);
+  const int stage = P.issued % kStages;
+  if (w.lane == 0) {
+    const char* src = P.base + (long long)bx * p.merged_stride + (long long)by * P.nstride;
+    mbar_expect_tx(&w.bars[stage], kTile);
+    bulk_g2s(w.tiles + stage * kTile, src, kTile, &w.bars[stage], w.policy);
+  }
+  P.issued++;
+  P.blk++;
+  return true;
+}
+
+__device__ __forceinline__ void fill(const DataParams& p, Producer& P, const WarpCtx& w) {
+  while (P.issued - P.consumed < (uint32_t)kStages) {
+    if (!produce_one(p, P, w)) break;
+  }
+}
+
+template <typename T, int G>
+__device__ __forceinline__ void process_item(const DataParams& p, Producer& P, const WarpCtx& w,
+                                             const int4 it) {
+  const int lane = w.lane, c = lane & 15, hf = lane >> 4;
+  const int grp = it.y >> 16, head = it.y & 0xffff;
+  const DataGroup& g = p.g[grp];
+  const int rl = it.x - g.req_begin;
+  float q[G][8], o[G][8], mx[G], l[G];
+#pragma unroll
+  for (int gg = 0; gg < G; ++gg) {
+    const T* qp = reinterpret_cast<const T*>(g.q) + ((size_t)rl * g.Hq + head * G + gg) * kD;
+    const uint4 raw = *reinterpret_cast<const uint4*>(qp + c * 8);
+    Cvt<T>::to_f32(raw, q[gg]);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      q[gg][j] *= p.scale_log2;
+      o[gg][j] = 0.f;
+    }
+    mx[gg] = -INFINITY;
+    l[gg] = 0.f;
+  }
+  const int b0 = it.z / kTpb, b1 = (it.w + kTpb - 1) / kTpb;
+  for (int b = b0; b < b1; ++b) {
+    if (P.issued == P.consumed) fill(p, P, w);
+    const int stage = P.consumed % kStages;
+    const uint32_t phase = (P.consumed / kStages) & 1u;
+    mbar_wait(&w.bars[stage], phase);
+    const int valid = min(kTpb, it.w - b * kTpb);
+    consume_tile<T, G>(w.tiles + stage * kTile, lane, valid, q, o, mx, l);
+    __syncwarp();
+    P.consumed++;
+    fill(p, P, w);
+  }
+  // finalize: l over the 16 distinct token lanes, o over the two token halves
+#pragma unroll
+  for (int gg = 0; gg < G; ++gg) {
+    float s = l[gg];
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    s += __shfl_xor_sync(0xffffffffu, s, 4);
+    s += __shfl_xor_sync(0xffffffffu, s, 8);
+    s += __shfl_xor_sync(0xffffffffu, s, 16);
+    l[gg] = s;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[gg][j] += __shfl_xor_sync(0xffffffffu, o[gg][j], 16);
+  }
+  const int ns = p.nsplit[it.x];
+  if (ns <= 1) {
+#pragma unroll
+    for (int gg = 0; gg < G; ++gg) {
+      if (hf == 0) {
+        const float inv = l[gg] > 0.f ? 1.f / l[gg] : 0.f;
+        float r[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = o[gg][j] * inv;
+        T* op = reinterpret_cast<T*>(g.out) + ((size_t)rl * g.Hq + head * G + gg) * kD + c * 8;
+        *reinterpret_cast<uint4*>(op) = Cvt<T>::from_f32(r);
+      }
+    }
+  } else {
+    const int split = it.z / p.split_tokens;
+#pragma unroll
+    for (int gg = 0; gg < G; ++gg) {
+      const size_t slot = (size_t)p.pbase[it.x] + (size_t)split * g.Hq + head * G + gg;
+      if (hf == 0) {
+        float4* dst = reinterpret_cast<float4*>(p.ws_o + slot * kD + c * 8);
+        dst[0] = make_float4(o[gg][0], o[gg][1], o[gg][2], o[gg][3]);
+        dst[1] = make_float4(o[gg][4], o[gg][5], o[gg][6], o[gg][7]);
+      }
+      if (lane == 0) p.ws_ml[slot] = make_float2(mx[gg], l[gg]);
+    }
+  }
+}
+
+template <typename T, int MAXG>
+__global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const __grid_constant__ DataParams p) {
+  extern __shared__ __align__(128) char smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  WarpCtx w;
+  w.tiles = smem + wid * kStages * kTile;
+  w.bars = reinterpret_cast<uint64_t*>(smem + kWarps * kStages * kTile) + wid * kStages;
+  w.ring = reinterpret_cast<int*>(smem + kWarps * kStages * kTile + kWarps * kStages * 8) + wid * kRing;
+  w.lane = lane;
+  w.n_items = *p.n_items;
+  w.policy = evict_first_policy();
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < kStages; ++s) mbar_init(&w.bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  Producer P;
+  P.idx = -1;
+  P.blk = P.bend = 0;
+  P.cbase = -1;
+  P.tc = make_int2(0, 0);
+  P.row = nullptr;
+  P.base = nullptr;
+  P.nstride = 0;
+  P.done = 0;
+  P.pushed = P.popped = 0;
+  P.issued = P.consumed = 0;
+  for (;;) {
+    fill(p, P, w);
+    if (P.pushed == P.popped) {
+      // ring empty: either finished or only zero-block items were skipped
+      if (P.done) break;
+      continue;
+    }
+    const int idx = w.ring[P.popped % kRing];
+    P.popped++;
+    const int4 it = p.items[idx];
+    const int G = p.g[it.y >> 16].G;
+    if (G == 1) process_item<T, 1>(p, P, w, it);
+    else if (MAXG >= 2 && G == 2) process_item<T, (MAXG >= 2 ? 2 : 1)>(p, P, w, it);
+    else if (MAXG >= 4 && G == 4) process_item<T, (MAXG >= 4 ? 4 : 1)>(p, P, w, it);
+    else if (MAXG >= 8 && G == 8) process_item<T, (MAXG >= 8 ? 8 : 1)>(p, P, w, it);
+  }
+}
+
+// Work list: one item per (request, split, kv head); partial slots for split requests.
+__global__ void __launch_bounds__(1024) plan_kernel(DataParams p) {
+  __shared__ int sm_warp[33];
+  __shared__ int carry_items, carry_slots;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) carry_items = carry_slots = 0;
+  __syncthreads();
+  auto scan = [&](int v, int* total) {
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) sm_warp[wid] = incl;
+    __syncthreads();
+    if (wid == 0) {
+      const int x = sm_warp[lane];
+      int xi = x;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, xi, o);
+        if (lane >= o) xi += t;
+      }
+      sm_warp[lane] = xi - x;
+      if (lane == 31) sm_warp[32] = xi;
+    }
+    __syncthreads();
+    const int ex = sm_warp[wid] + incl - v;
+    *total = sm_warp[32];
+    __syncthreads();
+    return ex;
+  };
+  for (int r0 = 0; r0 < p.nreq; r0 += 1024) {
+    const int r = r0 + tid;
+    const bool valid = r < p.nreq;
+    int ctx = 0, ns = 1, hkv = 0, hq = 0, grp = 0;
+    if (valid) {
+      grp = p.req_group[r];
+      ctx = p.req_tokens[p.handles[r]];
+      ns = ctx <= 0 ? 1 : (ctx + p.split_tokens - 1) / p.split_tokens;
+      hkv = p.g[grp].Hkv;
+      hq = p.g[grp].Hq;
+    }
+    int ti, ts;
+    const int ex_i = scan(valid ? ns * hkv : 0, &ti);
+    const int ex_s = scan(valid && ns > 1 ? ns * hq : 0, &ts);
+    if (valid) {
+      p.nsplit[r] = ns;
+      p.pbase[r] = carry_slots + ex_s;
+      int4* dst = p.items + carry_items + ex_i;
+      for (int s = 0; s < ns; ++s) {
+        const int tb = s * p.split_tokens, te = min(ctx, tb + p.split_tokens);
+        for (int h = 0; h < hkv; ++h) dst[s * hkv + h] = make_int4(r, (grp << 16) | h, tb, te);
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      carry_items += ti;
+      carry_slots += ts;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    *p.n_items = carry_items;
+    *p.counter = 0;
+  }
+}
+
+// LSE merge of split partials: one warp per (request, q head); lane owns 4 dims.
+template <typename T>
+__global__ void combine_kernel(const __grid_constant__ DataParams p) {
+  const int r = blockIdx.y;
+  if (p.nsplit[r] <= 1) return;
+  const int grp = p.req_group[r];
+  const DataGroup& g = p.g[grp];
+  if (!g.active) return;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int ns = p.nsplit[r];
+  for (int hq = blockIdx.x * (blockDim.x >> 5) + wid; hq < g.Hq; hq += gridDim.x * (blockDim.x >> 5)) {
+    float M = -INFINITY;
+    for (int s = 0; s < ns; ++s) M = fmaxf(M, p.ws_ml[(size_t)p.pbase[r] + (size_t)s * g.Hq + hq].x);
+    float L = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int s = 0; s < ns; ++s) {
+      const size_t slot = (size_t)p.pbase[r] + (size_t)s * g.Hq + hq;
+      const float2 ml = p.ws_ml[slot];
+      const float wgt = ml.y > 0.f ? exp2f(ml.x - M) : 0.f;
+      L += ml.y * wgt;
+      const float4 v = *reinterpret_cast<const float4*>(p.ws_o + slot * kD + lane * 4);
+      acc[0] += v.x * wgt;
+      acc[1] += v.y * wgt;
+      acc[2] += v.z * wgt;
+      acc[3] += v.w * wgt;
+    }
+    const float inv = L > 0.f ? 1.f / L : 0.f;
+    uint16_t* op = reinterpret_cast<uint16_t*>(g.out) + ((size_t)(r - g.req_begin) * g.Hq + hq) * kD + lane * 4;
+    ushort4 out;
+    out.x = Cvt<T>::one(acc[0] * inv);
+    out.y = Cvt<T>::one(acc[1] * inv);
+    out.z = Cvt<T>::one(acc[2] * inv);
+    out.w = Cvt<T>::one(acc[3] * inv);
+    *reinterpret_cast<ushort4*>(op) = out;
+  }
+}
+
+// KV append: one warp per (request, new token, kv head); lanes 0-15 move the K row
+// (256 B), lanes 16-31 the V row, 16 B each.
+__global__ void append_kernel(const __grid_constant__ DataParams p) {
+  const int r = blockIdx.y;
+  const DataGroup& g = p.g[p.req_group[r]];
+  if (!g.active) return;
+  const int lane = threadIdx.x & 31;
+  const int wglob = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int total = p.n_new * g.Hkv;
+  if (wglob >= total) return;
+  const int i = wglob / g.Hkv, h = wglob % g.Hkv;
+  const int handle = p.handles[r];
+  const int pos = p.req_tokens[handle] - p.n_new + i;
+  if (pos < 0) return;
+  const int2 e = p.req_table[(size_t)handle * p.cap + pos / kTpb];
+  const int kv = lane >> 4, c = lane & 15;
+  char* dst = p.pool + (long long)e.x * p.merged_stride + (long long)e.y * g.native_stride + g.layer_off +
+              (long long)h * g.head_stride + kv * (kTpb * kD * 2) + (pos % kTpb) * (kD * 2) + c * 16;
+  const int rl = r - g.req_begin;
+  const char* src = reinterpret_cast<const char*>(kv ? g.v : g.k) +
+                    (((size_t)rl * p.n_new + i) * g.Hkv + h) * (kD * 2) + c * 16;
+  *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(src);
+}
+
+__device__ __forceinline__ float synth_u(unsigned long long seed, unsigned long long i) {
+  unsigned long long z = seed + (i + 1ull) * 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  z ^= z >> 31;
+  return (float)(z >> 40) * (1.0f / 16777216.0f);
+}
+
+template <typename T>
+__global__ void synth_kernel(uint4* pool, size_t n16, unsigned long long seed, float amp) {
+  for (size_t v = blockIdx.x * (size_t)blockDim.x + threadIdx.x; v < n16; v += (size_t)gridDim.x * blockDim.x) {
+    float f[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) f[k] = (2.f * synth_u(seed, v * 8 + k) - 1.f) * amp;
+    pool[v] = Cvt<T>::from_f32(f);
+  }
+}
+
+int g_num_sms = 0;
+int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+template <typename T, int MAXG>
+void launch_decode_t(const DataParams& p, int grid, cudaStream_t s) {
+  const int smem = kWarps * kStages * kTile + kWarps * kStages * 8 + kWarps * kRing * 4;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(decode_kernel<T, MAXG>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  decode_kernel<T, MAXG><<<grid, kWarps * 32, smem, s>>>(p);
+}
+
+}  // namespace
+
+int decode_ctas_per_sm() { return 1; }
+
+void launch_decode_plan(const DataParams& p, cudaStream_t s) { plan_kernel<<<1, 1024, 0, s>>>(p); }
+
+void launch_decode(const DataParams& p, int max_g, int grid, cudaStream_t s) {
+  if (grid <= 0) grid = num_sms() * decode_ctas_per_sm();
+  if (p.dtype == 0) {
+    if (max_g <= 1) launch_decode_t<__half, 1>(p, grid, s);
+    else if (max_g <= 2) launch_decode_t<__half, 2>(p, grid, s);
+    else if (max_g <= 4) launch_decode_t<__half, 4>(p, grid, s);
+    else launch_decode_t<__half, 8>(p, grid, s);
+  } else {
+    if (max_g <= 1) launch_decode_t<__nv_bfloat16, 1>(p, grid, s);
+    else if (max_g <= 2) launch_decode_t<__nv_bfloat16, 2>(p, grid, s);
+    else if (max_g <= 4) launch_decode_t<__nv_bfloat16, 4>(p, grid, s);
+    else launch_decode_t<__nv_bfloat16, 8>(p, grid, s);
+  }
+}
+
+void launch_decode_combine(const DataParams& p, cudaStream_t s) {
+  dim3 grid(1, p.nreq);
+  if (p.dtype == 0) combine_kernel<__half><<<grid, 256, 0, s>>>(p);
+  else combine_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(p);
+}
+
+void launch_append(const DataParams& p, cudaStream_t s) {
+  int maxh = 1;
+  for (int i = 0; i < p.ngroups; ++i) maxh = max(maxh, p.g[i].Hkv);
+  const int warps = p.n_new * maxh;
+  dim3 grid((warps + 7) / 8, p.nreq);
+  append_kernel<<<grid, 256, 0, s>>>(p);
+}
+
+void launch_synth_fill(void* pool, size_t bytes, int dtype, unsigned long long seed, float amp,
+                       cudaStream_t s) {
+  const size_t n16 = bytes / 16;
+  const int grid = num_sms() * 8;
+  if (dtype == 0) synth_kernel<__half><<<grid, 256, 0, s>>>(reinterpret_cast<uint4*>(pool), n16, seed, amp);
+  else synth_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(reinterpret_cast<uint4*>(pool), n16, seed, amp);
+}
+
+}  // namespace skv

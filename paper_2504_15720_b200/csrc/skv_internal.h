@@ -1,0 +1,117 @@
+// skv_internal.h — structures shared by the host runtime (skv_capi.cpp) and the
+// sm_100a kernels (skv_alloc.cu, skv_attn.cu).  Not part of the public ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace skv {
+
+constexpr int kMaxModels = 16;   // services sharing one pool
+constexpr int kMaxGroups = 16;   // groups in one data-path batch
+constexpr int kMaxSub = 64;      // sub-slots per merged block (occupancy is a u64 mask)
+
+// ------------------------------------------------------------------ allocator state --
+// Device-resident canonical allocator state.  The reference keeps
+// std::set free list / partial sets and per-block slot_owner vectors
+// (kv_cache.hpp:173-177, 254-258); here they are bitmaps + flat arrays so a single
+// CTA can evaluate a whole batch of claims with block-wide scans.
+struct DevAlloc {
+  uint32_t* free_bits;           // [W]     1 = merged block on the free list
+  uint32_t* partial_bits;        // [M][W]  1 = claimed by model m and not full
+  int32_t* blk_model;            // [P]     owner model, -1 = free
+  unsigned long long* blk_occ;   // [P]     occupied sub-slot mask
+  unsigned long long* slot_owner;// [P*maxsub] request id per sub-slot (0 = empty)
+  long long* open;               // [M]     open_slots_ (kv_cache.hpp:254)
+  long long* free_count;         // [1]
+  int2* req_table;               // [R*cap] (merged block, sub index) per native block
+  int32_t* req_nslots;           // [R]
+  int32_t* req_tokens;           // [R]     tokens covered (decode context length)
+  int32_t* req_model;            // [R]
+  int32_t* status;               // [1]     device invariant violations (0 = ok)
+  int32_t* free_E;               // [M]     scratch: blocks emptied by the current free run
+  int32_t* free_R;               // [M]     scratch: slots released by the current free run
+};
+
+struct AllocParams {
+  int M, W, maxsub, cap;
+  long long P;
+  int sub[kMaxModels];
+};
+
+// One granted grow, decided on the host (mirror arithmetic, no device sync).
+struct GrowOp {
+  int32_t handle, model, have, claims;
+  int32_t tokens_after, pad;
+  unsigned long long id;
+};
+
+struct FreeOp {
+  int32_t handle, model, nslots, pad;
+};
+
+// Scratch for the grow kernel, sized by the host for the batch.
+struct GrowScratch {
+  int32_t* S;        // [n] model-local claim index of the op's first claim
+  int32_t* cbeg;     // [n] global claim prefix
+  int32_t* nnew;     // [n] new merged blocks taken by the op
+  int32_t* base;     // [n] global rank of the op's first new block
+  int32_t* nbfirst;  // [n] model-local index of the op's first new block
+  int32_t* newblk;   // [Nnew] the lowest free block ids, ascending
+  int32_t* newrank;  // [Nnew] (per-model regions) model-local new block -> global rank
+  int2* openlist;    // [Topen] (per-model regions) open (block, slot) pairs, lexicographic
+  long long* out_E;  // [M] (free runs) host-visible copy of emptied-block counts
+};
+
+void launch_grow(const DevAlloc& st, const AllocParams& pr, const GrowOp* ops, int n,
+                 const GrowScratch& sc, cudaStream_t s);
+void launch_free(const DevAlloc& st, const AllocParams& pr, const FreeOp* ops, int n,
+                 int32_t* out_E, cudaStream_t s);
+
+// ------------------------------------------------------------------ data path ------
+struct DataGroup {
+  const void* q;            // [B_g][Hq][D]
+  void* out;                // [B_g][Hq][D]
+  const void* k;            // append: [B_g][n_new][Hkv][D]
+  const void* v;
+  long long native_stride;  // bytes between sub-slots of this model
+  long long layer_off;      // bytes: (layer % phys_layers) * layer_stride
+  long long head_stride;    // bytes between kv heads
+  int Hq, Hkv, G, active;   // active = num_layers > layer
+  int req_begin, nreq;      // slice of the batch
+};
+
+struct DataParams {
+  DataGroup g[kMaxGroups];
+  int ngroups;
+  int nreq;                  // batch size
+  const int32_t* handles;    // [nreq]
+  const int32_t* req_group;  // [nreq]
+  const int32_t* req_tokens; // [R]
+  const int2* req_table;     // [R*cap]
+  int cap;
+  char* pool;
+  long long merged_stride;
+  int head_dim, tpb, dtype;
+  float scale_log2;          // softmax scale * log2(e)
+  int split_tokens;          // tokens per split (multiple of tpb)
+  int n_new;                 // append / prefill tokens per request
+  // decode plan
+  int4* items;               // [max_items] {req, (group<<16)|kv_head, tok_begin, tok_end}
+  int* n_items;
+  int* counter;              // dynamic work counter
+  int* pbase;                // [nreq] partial-slot base (split requests)
+  int* nsplit;               // [nreq]
+  float* ws_o;               // [slots][D] unnormalised partial outputs
+  float2* ws_ml;             // [slots] (running max (log2 domain), sum)
+};
+
+void launch_decode_plan(const DataParams& p, cudaStream_t s);
+void launch_decode(const DataParams& p, int max_g, int grid, cudaStream_t s);
+void launch_decode_combine(const DataParams& p, cudaStream_t s);
+void launch_append(const DataParams& p, cudaStream_t s);
+void launch_prefill(const DataParams& p, cudaStream_t s);
+void launch_synth_fill(void* pool, size_t bytes, int dtype, unsigned long long seed, float amp,
+                       cudaStream_t s);
+int decode_ctas_per_sm();
+
+}  // namespace skv

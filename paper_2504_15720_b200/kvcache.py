@@ -1,0 +1,488 @@
+"""Python mirror of ``seasim::UnifiedKvCache`` over the C-ABI of libseakv.so.
+
+Same method names, argument meaning and error behaviour as the reference
+(/root/reference/proj/include/seasim/kv_cache.hpp:46-267):
+
+* ``ConfigError``     — bad shape / tp / unknown model    (common.hpp:13-16)
+* ``ValidationError`` — negative tokens, id 0 (Q2)        (common.hpp:25-28)
+* ``LogicError``      — std::logic_error: unknown request, model change
+* CacheFull           — ``try_allocate`` returns ``False``  (kv_cache.hpp:110-112)
+
+Beyond the reference surface it exposes the data path: request batches,
+KV append, paged decode attention, synthetic fill and pool introspection.
+Every call goes to the CUDA library; there is no CPU fallback — importing
+this module without a built ``libseakv.so`` raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import os
+import subprocess
+from typing import Iterable, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libseakv.so")
+
+SKV_OK, SKV_CACHE_FULL = 0, 1
+SKV_ERR_CONFIG, SKV_ERR_VALIDATION, SKV_ERR_LOGIC, SKV_ERR_CUDA, SKV_ERR_ARG = -1, -2, -3, -4, -5
+FP16, BF16 = 0, 1
+
+
+class ConfigError(RuntimeError):
+    """seasim::ConfigError"""
+
+
+class ValidationError(RuntimeError):
+    """seasim::ValidationError"""
+
+
+class LogicError(RuntimeError):
+    """std::logic_error"""
+
+
+class CudaError(RuntimeError):
+    """CUDA runtime failure or device-side invariant violation."""
+
+
+class ArgError(ValueError):
+    """Bad argument / capacity exceeded."""
+
+
+_ERRS = {SKV_ERR_CONFIG: ConfigError, SKV_ERR_VALIDATION: ValidationError, SKV_ERR_LOGIC: LogicError,
+         SKV_ERR_CUDA: CudaError, SKV_ERR_ARG: ArgError}
+
+
+@dataclasses.dataclass
+class ModelSpec:
+    """seasim::ModelSpec (cost_model.hpp:19-40) fields the KV path reads, plus GQA."""
+
+    model_id: str
+    num_layers: int
+    num_heads: int  # KV heads (the reference's num_heads sizes the native block)
+    head_dim: int = 128
+    dtype_bytes: int = 2
+    num_q_heads: int = 0  # 0 -> num_heads
+
+
+@dataclasses.dataclass
+class CacheStats:
+    """seasim::CacheStats (kv_cache.hpp:35-40)."""
+
+    block_table_entries: int = 0
+    native_reads_writes: int = 0
+    internal_fragmentation_bytes: float = 0.0
+    peak_utilization: float = 0.0
+
+
+class _ModelDesc(C.Structure):
+    _fields_ = [("model_id", C.c_char_p), ("num_layers", C.c_int32), ("num_heads", C.c_int32),
+                ("num_q_heads", C.c_int32), ("head_dim", C.c_int32), ("dtype_bytes", C.c_int32)]
+
+
+class _Opts(C.Structure):
+    _fields_ = [("device", C.c_int32), ("dtype", C.c_int32), ("phys_layers", C.c_int32),
+                ("max_requests", C.c_int32), ("max_blocks_per_request", C.c_int32),
+                ("allocate_storage", C.c_int32)]
+
+
+class _Stats(C.Structure):
+    _fields_ = [("block_table_entries", C.c_uint64), ("native_reads_writes", C.c_uint64),
+                ("internal_fragmentation_bytes", C.c_double), ("peak_utilization", C.c_double)]
+
+
+class KvOp(C.Structure):
+    """KvOp (kv_cache.hpp:270-275): kind 0 = kGrow, 1 = kFree."""
+
+    _fields_ = [("kind", C.c_int32), ("model_idx", C.c_int32), ("request_id", C.c_uint64),
+                ("tokens", C.c_int64)]
+
+
+class Layout(C.Structure):
+    _fields_ = [("merged_stride", C.c_int64), ("native_stride", C.c_int64), ("layer_stride", C.c_int64),
+                ("head_stride", C.c_int64), ("kv_stride", C.c_int64), ("tpb", C.c_int32),
+                ("head_dim", C.c_int32), ("kv_heads", C.c_int32), ("q_heads", C.c_int32),
+                ("phys_layers", C.c_int32), ("dtype", C.c_int32)]
+
+
+class _DecodeArgs(C.Structure):
+    _fields_ = [("q", C.POINTER(C.c_void_p)), ("out", C.POINTER(C.c_void_p)), ("softmax_scale", C.c_float),
+                ("layer", C.c_int32), ("split_tokens", C.c_int32)]
+
+
+class _AppendArgs(C.Structure):
+    _fields_ = [("k", C.POINTER(C.c_void_p)), ("v", C.POINTER(C.c_void_p)), ("layer", C.c_int32),
+                ("n_new", C.c_int32)]
+
+
+class _PrefillArgs(C.Structure):
+    _fields_ = [("q", C.POINTER(C.c_void_p)), ("out", C.POINTER(C.c_void_p)), ("softmax_scale", C.c_float),
+                ("layer", C.c_int32), ("q_len", C.c_int32)]
+
+
+_lib = None
+
+
+def build() -> None:
+    """Compile libseakv.so for sm_100a (nvcc cross-compiles without a GPU)."""
+    subprocess.run(["make", "-s", "-C", os.path.join(_HERE, "csrc")], check=True)
+
+
+def lib() -> C.CDLL:
+    """The loaded CUDA library.  Raises if it is missing and cannot be built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        build()
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libseakv.so not built at {LIB_PATH}")
+    L = C.CDLL(LIB_PATH)
+    P, S, V = C.c_void_p, C.c_int, None
+    sig = {
+        "skv_version": (C.c_char_p, []),
+        "skv_default_opts": (V, [C.POINTER(_Opts)]),
+        "skv_native_block_bytes": (S, [C.POINTER(_ModelDesc), C.c_int32, C.c_int32, C.POINTER(C.c_double)]),
+        "skv_plan_merged_shape": (S, [C.POINTER(_ModelDesc), C.c_int32, C.c_int32, C.c_int32,
+                                      C.POINTER(C.c_double)]),
+        "skv_pool_create": (S, [C.POINTER(_ModelDesc), C.c_int32, C.c_int32, C.c_int32, C.c_size_t,
+                                C.POINTER(_Opts), C.POINTER(P)]),
+        "skv_pool_destroy": (V, [P]),
+        "skv_last_error": (C.c_char_p, [P]),
+        "skv_model_index": (S, [P, C.c_char_p, C.POINTER(C.c_int32)]),
+        "skv_sub_slots_per_merged": (C.c_int32, [P, C.c_int32]),
+        "skv_merged_block_bytes": (C.c_double, [P]),
+        "skv_pool_size": (C.c_size_t, [P]),
+        "skv_free_blocks": (C.c_size_t, [P]),
+        "skv_allocated_blocks": (C.c_size_t, [P]),
+        "skv_tokens_per_block": (C.c_int32, [P]),
+        "skv_native_blocks_for": (C.c_size_t, [P, C.c_int64]),
+        "skv_registered": (C.c_int32, [P, C.c_uint64]),
+        "skv_request_tokens": (C.c_int64, [P, C.c_uint64]),
+        "skv_available_slots": (C.c_size_t, [P, C.c_int32]),
+        "skv_can_grow_to": (S, [P, C.c_uint64, C.c_int32, C.c_int64, C.POINTER(C.c_int32)]),
+        "skv_try_allocate": (S, [P, C.c_uint64, C.c_int32, C.c_int64]),
+        "skv_free_request": (S, [P, C.c_uint64]),
+        "skv_record_context_read": (S, [P, C.c_uint64]),
+        "skv_block_table": (S, [P, C.c_uint64, P, C.c_size_t, C.POINTER(C.c_size_t)]),
+        "skv_owner_of": (S, [P, C.c_int32, C.c_int32, C.POINTER(C.c_uint64)]),
+        "skv_table_entries": (C.c_size_t, [P]),
+        "skv_fragmentation_bytes": (C.c_double, [P]),
+        "skv_stats": (S, [P, C.POINTER(_Stats)]),
+        "skv_replay": (S, [P, P, C.c_size_t, P]),
+        "skv_flush": (S, [P, P]),
+        "skv_synchronize": (S, [P]),
+        "skv_set_stream": (S, [P, P]),
+        "skv_get_stream": (P, [P]),
+        "skv_batch_create": (S, [P, P, P, C.c_int32, P, C.POINTER(P)]),
+        "skv_batch_destroy": (V, [P]),
+        "skv_batch_grow": (S, [P, P, C.c_int64, C.POINTER(C.c_int32)]),
+        "skv_batch_decode_bytes": (S, [P, P, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+        "skv_decode_attention": (S, [P, P, C.POINTER(_DecodeArgs), P]),
+        "skv_append_kv": (S, [P, P, C.POINTER(_AppendArgs), P]),
+        "skv_prefill_attention": (S, [P, P, C.POINTER(_PrefillArgs), P]),
+        "skv_model_layout": (S, [P, C.c_int32, C.POINTER(Layout)]),
+        "skv_storage": (P, [P, C.POINTER(C.c_size_t)]),
+        "skv_synth_fill": (S, [P, C.c_uint64, C.c_float, P]),
+        "skv_read_blocks": (S, [P, P, C.c_size_t, P]),
+        "skv_kernel_launches": (C.c_uint64, [P]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+def _desc(models: Sequence[ModelSpec]):
+    arr = (_ModelDesc * max(1, len(models)))()
+    keep = []
+    for i, m in enumerate(models):
+        b = m.model_id.encode()
+        keep.append(b)
+        arr[i] = _ModelDesc(b, m.num_layers, m.num_heads, m.num_q_heads, m.head_dim, m.dtype_bytes)
+    return arr, keep
+
+
+def _raise(st: int, pool=None):
+    if st in (SKV_OK, SKV_CACHE_FULL):
+        return
+    msg = lib().skv_last_error(pool)
+    raise _ERRS.get(st, RuntimeError)(msg.decode() if msg else f"status {st}")
+
+
+def native_block_bytes(model: ModelSpec, tokens_per_block: int = 16, tp_size: int = 1) -> float:
+    """kv_cache.hpp:17-22"""
+    arr, _k = _desc([model])
+    out = C.c_double()
+    _raise(lib().skv_native_block_bytes(arr, tokens_per_block, tp_size, C.byref(out)))
+    return out.value
+
+
+def plan_merged_shape(models: Sequence[ModelSpec], tokens_per_block: int = 16, tp_size: int = 1) -> float:
+    """kv_cache.hpp:26-33"""
+    arr, _k = _desc(models)
+    out = C.c_double()
+    _raise(lib().skv_plan_merged_shape(arr, len(models), tokens_per_block, tp_size, C.byref(out)))
+    return out.value
+
+
+def _ptr(x) -> int:
+    """Device/host address of a torch tensor, an int, or None."""
+    if x is None:
+        return 0
+    if isinstance(x, int):
+        return x
+    return int(x.data_ptr())
+
+
+def _stream_ptr(stream) -> int | None:
+    if stream is None:
+        return None
+    if isinstance(stream, int):
+        return stream
+    return int(stream.cuda_stream)
+
+
+class UnifiedKvCache:
+    """The unified merged-block KV pool on one GPU (kv_cache.hpp:46-267)."""
+
+    def __init__(self, models: Sequence[ModelSpec], tokens_per_block: int = 16, tp_size: int = 1,
+                 pool_blocks: int = 0, *, device: int = 0, dtype: int = FP16, phys_layers: int = 0,
+                 max_requests: int = 4096, max_blocks_per_request: int = 0, allocate_storage: bool = False):
+        L = lib()
+        self._lib = L
+        self.models = list(models)
+        arr, self._keep = _desc(self.models)
+        opts = _Opts()
+        L.skv_default_opts(C.byref(opts))
+        opts.device, opts.dtype, opts.phys_layers = device, dtype, phys_layers
+        opts.max_requests, opts.max_blocks_per_request = max_requests, max_blocks_per_request
+        opts.allocate_storage = 1 if allocate_storage else 0
+        h = C.c_void_p()
+        st = L.skv_pool_create(arr, len(self.models), tokens_per_block, tp_size, pool_blocks, C.byref(opts),
+                               C.byref(h))
+        _raise(st, None)
+        self._h = h.value
+        self.device = device
+        self.dtype = dtype
+
+    # -- lifetime ------------------------------------------------------------------------
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.skv_pool_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def _chk(self, st):
+        _raise(st, self._h)
+        return st
+
+    # -- reference surface (kv_cache.hpp:68-170) -------------------------------------------
+    def model_index(self, model_id: str) -> int:
+        out = C.c_int32()
+        self._chk(self._lib.skv_model_index(self._h, model_id.encode(), C.byref(out)))
+        return out.value
+
+    def sub_slots_per_merged(self, m: int) -> int:
+        return self._lib.skv_sub_slots_per_merged(self._h, m)
+
+    def merged_block_bytes(self) -> float:
+        return self._lib.skv_merged_block_bytes(self._h)
+
+    def pool_size(self) -> int:
+        return self._lib.skv_pool_size(self._h)
+
+    def free_blocks(self) -> int:
+        return self._lib.skv_free_blocks(self._h)
+
+    def allocated_blocks(self) -> int:
+        return self._lib.skv_allocated_blocks(self._h)
+
+    def tokens_per_block(self) -> int:
+        return self._lib.skv_tokens_per_block(self._h)
+
+    def native_blocks_for(self, tokens: int) -> int:
+        return self._lib.skv_native_blocks_for(self._h, tokens)
+
+    def registered(self, request_id: int) -> bool:
+        return bool(self._lib.skv_registered(self._h, request_id))
+
+    def request_tokens(self, request_id: int) -> int:
+        return self._lib.skv_request_tokens(self._h, request_id)
+
+    def available_slots(self, m: int) -> int:
+        return self._lib.skv_available_slots(self._h, m)
+
+    def can_grow_to(self, request_id: int, m: int, tokens: int) -> bool:
+        out = C.c_int32()
+        self._chk(self._lib.skv_can_grow_to(self._h, request_id, m, tokens, C.byref(out)))
+        return bool(out.value)
+
+    def try_allocate(self, request_id: int, m: int, tokens: int) -> bool:
+        return self._chk(self._lib.skv_try_allocate(self._h, request_id, m, tokens)) == SKV_OK
+
+    def try_allocate_rc(self, request_id: int, m: int, tokens: int) -> int:
+        """Raw status mapped to the oracle's codes: 0 granted, 1 full, -2 validation, -3 logic."""
+        st = self._lib.skv_try_allocate(self._h, request_id, m, tokens)
+        return st
+
+    def free_request(self, request_id: int) -> None:
+        self._chk(self._lib.skv_free_request(self._h, request_id))
+
+    def record_context_read(self, request_id: int) -> None:
+        self._chk(self._lib.skv_record_context_read(self._h, request_id))
+
+    def block_table_np(self, request_id: int) -> np.ndarray:
+        n = C.c_size_t()
+        self._chk(self._lib.skv_block_table(self._h, request_id, None, 0, C.byref(n)))
+        buf = np.zeros((n.value, 2), dtype=np.int32)
+        if n.value:
+            self._chk(self._lib.skv_block_table(self._h, request_id, buf.ctypes.data, n.value, C.byref(n)))
+        return buf
+
+    def block_table(self, request_id: int):
+        return [tuple(map(int, r)) for r in self.block_table_np(request_id)]
+
+    def owner_of(self, block: int, slot: int) -> int:
+        out = C.c_uint64()
+        self._chk(self._lib.skv_owner_of(self._h, block, slot, C.byref(out)))
+        return out.value
+
+    def table_entries(self) -> int:
+        return self._lib.skv_table_entries(self._h)
+
+    def fragmentation_bytes(self) -> float:
+        return self._lib.skv_fragmentation_bytes(self._h)
+
+    def stats(self) -> dict:
+        s = _Stats()
+        self._chk(self._lib.skv_stats(self._h, C.byref(s)))
+        return dict(block_table_entries=s.block_table_entries, native_reads_writes=s.native_reads_writes,
+                    internal_fragmentation_bytes=s.internal_fragmentation_bytes,
+                    peak_utilization=s.peak_utilization)
+
+    # -- batched / replay -------------------------------------------------------------------
+    def replay(self, ops: Iterable[tuple]) -> np.ndarray:
+        ops = list(ops)
+        arr = (KvOp * max(1, len(ops)))()
+        for i, (kind, rid, m, tok) in enumerate(ops):
+            arr[i] = KvOp(kind, m, rid, tok)
+        granted = np.zeros(max(1, len(ops)), dtype=np.int32)
+        self._chk(self._lib.skv_replay(self._h, arr, len(ops), granted.ctypes.data))
+        return granted[: len(ops)]
+
+    def flush(self, stream=None):
+        self._chk(self._lib.skv_flush(self._h, _stream_ptr(stream)))
+
+    def synchronize(self):
+        self._chk(self._lib.skv_synchronize(self._h))
+
+    def set_stream(self, stream):
+        self._chk(self._lib.skv_set_stream(self._h, _stream_ptr(stream)))
+
+    def kernel_launches(self) -> int:
+        return self._lib.skv_kernel_launches(self._h)
+
+    # -- storage ----------------------------------------------------------------------------
+    def layout(self, m: int) -> Layout:
+        out = Layout()
+        self._chk(self._lib.skv_model_layout(self._h, m, C.byref(out)))
+        return out
+
+    def storage(self):
+        n = C.c_size_t()
+        p = self._lib.skv_storage(self._h, C.byref(n))
+        return p, n.value
+
+    def synth_fill(self, seed: int, amp: float = 1.0, stream=None):
+        self._chk(self._lib.skv_synth_fill(self._h, seed, amp, _stream_ptr(stream)))
+
+    def read_blocks(self, ids) -> np.ndarray:
+        ids = np.ascontiguousarray(np.asarray(ids, dtype=np.int32))
+        stride = self.layout(0).merged_stride
+        out = np.zeros(len(ids) * stride, dtype=np.uint8)
+        if len(ids):
+            self._chk(self._lib.skv_read_blocks(self._h, ids.ctypes.data, len(ids), out.ctypes.data))
+        return out
+
+    def batch(self, groups: Sequence[tuple[int, Sequence[int]]]) -> "Batch":
+        return Batch(self, groups)
+
+
+class Batch:
+    """Requests covered by one data-path launch, grouped by service (model index)."""
+
+    def __init__(self, cache: UnifiedKvCache, groups: Sequence[tuple[int, Sequence[int]]]):
+        self.cache = cache
+        self.groups = [(int(m), [int(i) for i in ids]) for m, ids in groups]
+        gm = (C.c_int32 * len(self.groups))(*[m for m, _ in self.groups])
+        gs = (C.c_int32 * len(self.groups))(*[len(ids) for _, ids in self.groups])
+        flat = [i for _, ids in self.groups for i in ids]
+        idarr = (C.c_uint64 * max(1, len(flat)))(*flat)
+        h = C.c_void_p()
+        cache._chk(cache._lib.skv_batch_create(cache._h, gm, gs, len(self.groups), idarr, C.byref(h)))
+        self._h = h.value
+
+    def close(self):
+        if getattr(self, "_h", None) and self.cache._h:
+            self.cache._lib.skv_batch_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def grow(self, delta: int = 1) -> int:
+        n = C.c_int32()
+        self.cache._chk(self.cache._lib.skv_batch_grow(self.cache._h, self._h, delta, C.byref(n)))
+        return n.value
+
+    def decode_bytes(self, layer: int) -> tuple[float, float]:
+        kv, tot = C.c_double(), C.c_double()
+        self.cache._chk(self.cache._lib.skv_batch_decode_bytes(self.cache._h, self._h, layer, C.byref(kv),
+                                                               C.byref(tot)))
+        return kv.value, tot.value
+
+    def decode(self, q: Sequence, out: Sequence, layer: int, softmax_scale: float = 0.0, split_tokens: int = 0,
+               stream=None):
+        n = len(self.groups)
+        qa = (C.c_void_p * n)(*[_ptr(t) for t in q])
+        oa = (C.c_void_p * n)(*[_ptr(t) for t in out])
+        a = _DecodeArgs(C.cast(qa, C.POINTER(C.c_void_p)), C.cast(oa, C.POINTER(C.c_void_p)), softmax_scale,
+                        layer, split_tokens)
+        self.cache._chk(self.cache._lib.skv_decode_attention(self.cache._h, self._h, C.byref(a),
+                                                             _stream_ptr(stream)))
+
+    def append(self, k: Sequence, v: Sequence, layer: int, n_new: int = 1, stream=None):
+        n = len(self.groups)
+        ka = (C.c_void_p * n)(*[_ptr(t) for t in k])
+        va = (C.c_void_p * n)(*[_ptr(t) for t in v])
+        a = _AppendArgs(C.cast(ka, C.POINTER(C.c_void_p)), C.cast(va, C.POINTER(C.c_void_p)), layer, n_new)
+        self.cache._chk(self.cache._lib.skv_append_kv(self.cache._h, self._h, C.byref(a), _stream_ptr(stream)))
+
+    def prefill(self, q: Sequence, out: Sequence, layer: int, q_len: int, softmax_scale: float = 0.0,
+                stream=None):
+        n = len(self.groups)
+        qa = (C.c_void_p * n)(*[_ptr(t) for t in q])
+        oa = (C.c_void_p * n)(*[_ptr(t) for t in out])
+        a = _PrefillArgs(C.cast(qa, C.POINTER(C.c_void_p)), C.cast(oa, C.POINTER(C.c_void_p)), softmax_scale,
+                         layer, q_len)
+        self.cache._chk(self.cache._lib.skv_prefill_attention(self.cache._h, self._h, C.byref(a),
+                                                              _stream_ptr(stream)))

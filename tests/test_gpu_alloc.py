@@ -1,0 +1,233 @@
+"""GPU allocator parity: the CUDA block allocator behind the C-ABI must give
+bit-identical block tables, owners, counters and CacheStats to the reference
+semantics (oracle/kv_alloc_oracle.c, itself pinned to the reference in
+test_oracle_alloc.py; and the reference .so directly when shipped)."""
+import numpy as np
+import pytest
+
+import oracle_py as O
+import paper_2504_15720_b200 as P
+from _workloads import FREE, GROW, property_stream, random_stream
+
+pytestmark = pytest.mark.gpu
+
+
+def spec(layers, heads, q_heads=0, name=None):
+    return P.ModelSpec(name or f"m{layers}x{heads}", layers, heads, 128, 2, q_heads)
+
+
+def gpu_cache(shapes, pool, **kw):
+    return P.UnifiedKvCache([spec(*s) for s in shapes], 16, 1, pool, **kw)
+
+
+# --- kv_cache_test.cpp known answers through the GPU path ------------------------------------
+def test_same_architecture_packs_one_sub_slot():  # :31-36
+    c = gpu_cache([(32, 32), (32, 32)], 8)
+    assert (c.sub_slots_per_merged(0), c.sub_slots_per_merged(1)) == (1, 1)
+
+
+def test_small_model_packs_many_sub_slots():  # :49-55
+    c = gpu_cache([(2, 2), (8, 8)], 8)
+    assert (c.sub_slots_per_merged(0), c.sub_slots_per_merged(1)) == (16, 1)
+
+
+def test_zero_tokens_is_no_change():  # :61-66
+    c = gpu_cache([(4, 4)], 4)
+    assert c.try_allocate(1, 0, 0)
+    assert c.free_blocks() == 4
+    assert c.block_table(1) == []
+
+
+def test_cache_full_signal():  # :68-74
+    c = gpu_cache([(4, 4)], 2)
+    assert not c.try_allocate(1, 0, 33)
+    assert c.free_blocks() == 2
+    assert c.registered(1)
+
+
+def test_packing_uses_one_merged_block():  # :76-85
+    c = gpu_cache([(2, 2), (4, 4)], 8)
+    assert c.sub_slots_per_merged(0) == 4
+    assert c.try_allocate(1, 0, 48)
+    assert c.allocated_blocks() == 1
+    assert c.block_table(1) == [(0, 0), (0, 1), (0, 2)]
+
+
+def test_grow_reuses_existing_blocks():  # :87-94
+    c = gpu_cache([(4, 4)], 4)
+    assert c.try_allocate(1, 0, 10) and c.try_allocate(1, 0, 16)
+    assert len(c.block_table(1)) == 1
+    assert c.try_allocate(1, 0, 17)
+    assert len(c.block_table(1)) == 2
+
+
+def test_free_restores_free_list():  # :96-102
+    c = gpu_cache([(4, 4)], 4)
+    assert c.try_allocate(1, 0, 40)
+    assert c.free_blocks() == 1
+    c.free_request(1)
+    assert c.free_blocks() == 4
+
+
+def test_shared_merged_block_stays_allocated():  # :104-117
+    c = gpu_cache([(2, 2), (4, 4)], 2)
+    assert c.try_allocate(1, 0, 8) and c.try_allocate(2, 0, 8)
+    assert c.allocated_blocks() == 1
+    c.free_request(1)
+    assert c.allocated_blocks() == 1
+    c.free_request(2)
+    assert c.allocated_blocks() == 0
+
+
+def test_unknown_request_is_logic_error():  # :119-122
+    c = gpu_cache([(4, 4)], 4)
+    with pytest.raises(P.LogicError):
+        c.free_request(77)
+
+
+def test_errors_map_to_reference_exceptions():
+    c = gpu_cache([(4, 4), (2, 2)], 4)
+    with pytest.raises(P.ValidationError):
+        c.try_allocate(1, 0, -1)
+    assert c.try_allocate(1, 0, 20)
+    with pytest.raises(P.LogicError):
+        c.try_allocate(1, 1, 40)
+    with pytest.raises(P.ConfigError):
+        c.model_index("nope")
+    with pytest.raises(P.ValidationError):  # Q2 policy: id 0 is reserved
+        c.try_allocate(0, 0, 5)
+
+
+def test_peak_utilization_tracks_high_water():  # :228-235
+    c = gpu_cache([(4, 4)], 10)
+    assert c.try_allocate(1, 0, 96)
+    c.free_request(1)
+    assert c.try_allocate(2, 0, 32)
+    assert c.stats()["peak_utilization"] == 0.6
+
+
+# --- the reference's seeded 100k-op property test on the GPU ---------------------------------
+def test_property_100k_matches_reference_incl_q1_residual():
+    c = gpu_cache([(2, 2), (8, 8)], 64)
+    o = O.OracleCache([(2, 2, 128, 2), (8, 8, 128, 2)], pool=64)
+    gen = property_stream(2024, 100000, 2)
+    live = {}
+    step = 0
+    op = next(gen)
+    try:
+        while True:
+            kind, rid, mm, tok = op
+            if kind == GROW:
+                g = c.try_allocate(rid, mm, tok)
+                assert g == o.try_allocate(rid, mm, tok)
+                if g:
+                    live[rid] = (mm, tok)
+                op = gen.send(g)
+            else:
+                c.free_request(rid)
+                o.free_request(rid)
+                del live[rid]
+                op = next(gen)
+            if step % 5000 == 0:
+                assert c.allocated_blocks() + c.free_blocks() == 64
+                seen = set()
+                for i in live:
+                    bt = c.block_table(i)
+                    assert bt == o.block_table(i)
+                    for s in bt:
+                        assert s not in seen
+                        seen.add(s)
+                for b in range(64):
+                    for s in range(16):
+                        assert c.owner_of(b, s) == o.owner_of(b, s)
+            step += 1
+    except StopIteration:
+        pass
+    assert c.stats() == o.stats()
+    for i in list(live):
+        c.free_request(i)
+    assert c.free_blocks() == 64 and c.table_entries() == 0
+    assert c.fragmentation_bytes() == 34839396352.0  # == the reference's own residual (Q1)
+
+
+# --- differential replay: block tables bit for bit ------------------------------------------
+SHAPES = [
+    [(2, 2), (8, 8)],
+    [(32, 32), (40, 40)],
+    [(32, 8, 32), (32, 8, 32), (40, 40), (32, 32)],
+    [(3, 3), (8, 8), (4, 2), (5, 5)],
+    [(1, 1), (2, 1), (4, 4), (8, 8), (2, 2), (3, 1), (6, 2), (8, 4)],
+]
+
+
+def _oracle_for(shapes, pool):
+    return O.OracleCache([(s[0], s[1], 128, 2) for s in shapes], pool=pool)
+
+
+@pytest.mark.parametrize("si", range(len(SHAPES)))
+@pytest.mark.parametrize("seed", [3, 11])
+def test_replay_bit_exact(si, seed):
+    shapes = SHAPES[si]
+    P_ = 96
+    ops = random_stream(seed * 77 + si, 30000, len(shapes), max_live=120, max_grow=60)
+    c, o = gpu_cache(shapes, P_), _oracle_for(shapes, P_)
+    # in chunks, so frees and grows interleave across device flushes
+    for k in range(0, len(ops), 2500):
+        chunk = ops[k:k + 2500]
+        g1 = c.replay(chunk)
+        g2 = [o.try_allocate_rc(r, m, t) == 0 if kind == GROW else (o.free_request(r), 0)[1]
+              for kind, r, m, t in chunk]
+        assert list(g1) == [int(x) for x in g2]
+        for mm in range(len(shapes)):
+            assert c.available_slots(mm) == o.available_slots(mm)
+        live = {r for kind, r, m, t in ops[:k + 2500] if o.registered(r)}
+        for r in sorted(live):
+            assert np.array_equal(c.block_table_np(r), o.block_table_np(r)), r
+    assert c.stats() == o.stats()
+    assert c.fragmentation_bytes() == o.fragmentation_bytes()
+    assert c.free_blocks() == o.free_blocks()
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not shipped")
+def test_replay_vs_unmodified_reference():
+    shapes = SHAPES[2]
+    ops = random_stream(4242, 50000, 4, max_live=300, max_grow=300)
+    c = gpu_cache(shapes, 900)
+    r = O.RefCache([(s[0], s[1], 128, 2) for s in shapes], pool=900)
+    g = c.replay(ops)
+    for (kind, rid, mm, tok), gi in zip(ops, g):
+        pass
+    assert r.replay(ops) == int(g.sum())
+    assert c.stats() == r.stats()
+    for rid in sorted({op[1] for op in ops}):
+        if r.registered(rid):
+            assert np.array_equal(c.block_table_np(rid), np.array(r.block_table(rid), dtype=np.int32).reshape(-1, 2))
+
+
+def test_large_batch_grow_matches_oracle():
+    """Config-2 shapes: 4 services x 64 requests grown to 2048 tokens in one device batch,
+    then a decode-step batch (+1 token each) and a partial free/regrow churn."""
+    shapes = [(32, 8, 32), (32, 8, 32), (40, 40), (32, 32)]
+    P_ = 4 * 64 * 128 + 512
+    c = gpu_cache(shapes, P_, max_blocks_per_request=256)
+    o = _oracle_for(shapes, P_)
+    ids = []
+    for r in range(64):
+        for mm in range(4):
+            rid = 1 + r * 4 + mm
+            ids.append((rid, mm))
+            assert c.try_allocate(rid, mm, 2048) == o.try_allocate(rid, mm, 2048)
+    b = c.batch([(mm, [rid for rid, m2 in ids if m2 == mm]) for mm in range(4)])
+    assert b.grow(1) == 256
+    for rid, mm in ids:
+        assert o.try_allocate(rid, mm, 2049)
+    for rid, mm in ids[::7]:
+        c.free_request(rid)
+        o.free_request(rid)
+    for rid, mm in ids[::7]:
+        assert c.try_allocate(rid + 100000, mm, 333) == o.try_allocate(rid + 100000, mm, 333)
+    for rid, mm in ids:
+        for x in (rid, rid + 100000):
+            if o.registered(x):
+                assert np.array_equal(c.block_table_np(x), o.block_table_np(x))
+    assert c.stats() == o.stats()

@@ -1,0 +1,189 @@
+"""Decode-attention and KV-append parity on the GPU against the fp32 CPU oracle
+(oracle/attn_oracle.c), reading K/V through the GPU allocator's block tables.
+
+Tolerances (north star): fp16 max-abs <= 2e-3, bf16 <= 1e-2 against fp32.
+"""
+import numpy as np
+import pytest
+
+import oracle_py as O
+import paper_2504_15720_b200 as P
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+TOL = {P.FP16: 2e-3, P.BF16: 1e-2}
+
+
+def tdtype(dt):
+    return torch.float16 if dt == P.FP16 else torch.bfloat16
+
+
+def build_pool(shapes, ctxs, pool_blocks=None, dtype=P.FP16, phys_layers=0, seed=1234, amp=1.0):
+    """shapes: [(layers, kv_heads, q_heads)], ctxs: per model list of context lengths."""
+    models = [P.ModelSpec(f"s{i}", L, H, 128, 2, Hq) for i, (L, H, Hq) in enumerate(shapes)]
+    need = sum(len(c) * (max(c) // 16 + 2) for c in ctxs) + 8
+    cache = P.UnifiedKvCache(models, 16, 1, pool_blocks or need, dtype=dtype, phys_layers=phys_layers,
+                             allocate_storage=True, max_blocks_per_request=4096)
+    groups = []
+    rid = 1
+    order = []
+    for mi, cl in enumerate(ctxs):
+        ids = []
+        for t in cl:
+            ids.append(rid)
+            order.append((rid, mi, t))
+            rid += 1
+        groups.append((mi, ids))
+    # interleave services so merged blocks of different models alternate
+    order.sort(key=lambda x: (x[0] % 3, x[0]))
+    for r, mi, t in order:
+        assert cache.try_allocate(r, mi, t)
+    cache.synth_fill(seed, amp)
+    return cache, groups
+
+
+def host_image(cache):
+    return cache.read_blocks(np.arange(cache.pool_size(), dtype=np.int32))
+
+
+def oracle_layout(cache, m):
+    L = cache.layout(m)
+    return O.layout(L.merged_stride, L.native_stride, L.layer_stride, L.head_stride, L.kv_stride, L.tpb,
+                    L.head_dim, L.kv_heads, L.q_heads, L.phys_layers, L.dtype)
+
+
+def tables_of(cache, ids):
+    tabs = [cache.block_table_np(i) for i in ids]
+    width = max(1, max(len(t) for t in tabs))
+    out = np.zeros((len(ids), width, 2), dtype=np.int32)
+    for k, t in enumerate(tabs):
+        out[k, :len(t)] = t
+    return out
+
+
+def run_decode_check(shapes, ctxs, layer=0, dtype=P.FP16, split=0, phys_layers=0, qamp=1.0, seed=7):
+    cache, groups = build_pool(shapes, ctxs, dtype=dtype, phys_layers=phys_layers)
+    gen = torch.Generator(device="cuda").manual_seed(seed)
+    qs, outs = [], []
+    for (mi, ids), (L, H, Hq) in zip(groups, shapes):
+        q = (torch.rand((len(ids), Hq, 128), generator=gen, device="cuda") * 2 - 1) * qamp
+        qs.append(q.to(tdtype(dtype)).contiguous())
+        outs.append(torch.full((len(ids), Hq, 128), float("nan"), device="cuda", dtype=tdtype(dtype)))
+    b = cache.batch(groups)
+    b.decode(qs, outs, layer, split_tokens=split)
+    torch.cuda.synchronize()
+    img = host_image(cache)
+    worst = 0.0
+    for (mi, ids), q, o, (L, H, Hq) in zip(groups, qs, outs, shapes):
+        if layer >= L:
+            continue
+        ctx = np.array([ctxs[mi][k] for k in range(len(ids))], dtype=np.int64)
+        ref = O.decode_attention(oracle_layout(cache, mi), img, layer, tables_of(cache, ids), ctx,
+                                 q.view(torch.int16).cpu().numpy().view(np.uint16), 1.0 / np.sqrt(128.0))
+        got = o.float().cpu().numpy()
+        err = float(np.nanmax(np.abs(got - ref))) if got.size else 0.0
+        assert not np.isnan(got).any()
+        worst = max(worst, err)
+    assert worst <= TOL[dtype], worst
+    return worst
+
+
+def test_config1_shapes_fp16():
+    """7B (32L,32H) + 13B (40L,40H) sharing one pool; ctx 512 (config 1, fewer requests)."""
+    run_decode_check([(32, 32, 32), (40, 40, 40)], [[512] * 3, [512] * 3], layer=5)
+
+
+def test_gqa_and_mha_mixed_config2_shapes():
+    """Llama-3-8B / Mistral (8 KV, 32 Q heads) + 13B + OPT in one launch (config 2 shapes)."""
+    run_decode_check([(32, 8, 32), (32, 8, 32), (40, 40, 40), (32, 32, 32)],
+                     [[300, 17], [1, 64], [129, 40], [255, 16]], layer=31)
+
+
+def test_layers_beyond_shorter_models_are_skipped():
+    run_decode_check([(4, 8, 32), (6, 4, 4)], [[33, 70], [100]], layer=5)
+
+
+@pytest.mark.parametrize("ctx", [1, 15, 16, 17, 31, 32, 33, 257])
+def test_ragged_context_lengths(ctx):
+    run_decode_check([(2, 4, 16), (3, 2, 2)], [[ctx, ctx + 3], [ctx]], layer=1)
+
+
+def test_split_kv_long_context():
+    run_decode_check([(2, 8, 32), (2, 4, 4)], [[4000, 1111], [3000]], layer=1, split=512)
+
+
+def test_split_kv_automatic():
+    run_decode_check([(2, 2, 8)], [[5000]], layer=0)
+
+
+def test_bf16():
+    run_decode_check([(4, 8, 32), (4, 4, 4)], [[700, 33], [99, 1000]], layer=2, dtype=P.BF16)
+
+
+def test_gqa_ratio_2_and_8():
+    run_decode_check([(2, 8, 16), (2, 2, 16)], [[90, 300], [200]], layer=0)
+
+
+def test_peaky_queries_stress_online_softmax():
+    run_decode_check([(2, 8, 32), (2, 4, 4)], [[600], [800, 5]], layer=1, qamp=8.0)
+
+
+def test_layer_sliced_pool():
+    """phys_layers=2: logical layer l reads physical layer l % 2 (SURVEY Q6 run A)."""
+    run_decode_check([(32, 8, 32), (40, 40, 40)], [[200], [150]], layer=37, phys_layers=2)
+
+
+def test_append_then_decode_matches_oracle():
+    shapes = [(3, 8, 32), (3, 4, 4)]
+    ctxs = [[40, 7], [16]]
+    cache, groups = build_pool(shapes, ctxs)
+    b = cache.batch(groups)
+    assert b.grow(1) == 3  # decode step: one new token each
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    ks = [(torch.rand((len(ids), 1, H, 128), generator=gen, device="cuda") - 0.5).half()
+          for (mi, ids), (L, H, Hq) in zip(groups, shapes)]
+    vs = [(torch.rand((len(ids), 1, H, 128), generator=gen, device="cuda") - 0.5).half()
+          for (mi, ids), (L, H, Hq) in zip(groups, shapes)]
+    before = host_image(cache)
+    b.append(ks, vs, layer=2, n_new=1)
+    torch.cuda.synchronize()
+    after = host_image(cache)
+    # oracle: scatter into the host image of `before`
+    for (mi, ids), k, v in zip(groups, ks, vs):
+        pos = np.array([ctxs[mi][j] for j in range(len(ids))], dtype=np.int64)
+        O.append(oracle_layout(cache, mi), before, 2, tables_of(cache, ids), pos,
+                 k.view(torch.int16).cpu().numpy().view(np.uint16), v.view(torch.int16).cpu().numpy().view(np.uint16))
+    assert np.array_equal(before, after)
+    # and decode over the grown context sees the appended token
+    qs = [torch.randn((len(ids), Hq, 128), generator=gen, device="cuda").half() for (mi, ids), (L, H, Hq) in
+          zip(groups, shapes)]
+    outs = [torch.empty_like(q) for q in qs]
+    b.decode(qs, outs, 2)
+    torch.cuda.synchronize()
+    for (mi, ids), q, o in zip(groups, qs, outs):
+        ctx = np.array([ctxs[mi][j] + 1 for j in range(len(ids))], dtype=np.int64)
+        ref = O.decode_attention(oracle_layout(cache, mi), after, 2, tables_of(cache, ids), ctx,
+                                 q.view(torch.int16).cpu().numpy().view(np.uint16), 1.0 / np.sqrt(128.0))
+        assert np.abs(o.float().cpu().numpy() - ref).max() <= 2e-3
+
+
+def test_synth_fill_matches_oracle_generator():
+    cache, groups = build_pool([(2, 2, 2)], [[16]], seed=99, amp=1.0)
+    img = host_image(cache)[:4096].view(np.float16).astype(np.float32)
+    ref = np.array([O.synth_value(99, i, 1.0) for i in range(2048)], dtype=np.float32).astype(np.float16)
+    assert np.array_equal(img, ref.astype(np.float32))
+
+
+def test_decode_is_repeatable_and_launch_count():
+    cache, groups = build_pool([(2, 8, 32), (2, 4, 4)], [[100, 200], [300]])
+    b = cache.batch(groups)
+    qs = [torch.randn((2, 32, 128), device="cuda").half(), torch.randn((1, 4, 128), device="cuda").half()]
+    o1 = [torch.empty_like(q) for q in qs]
+    o2 = [torch.empty_like(q) for q in qs]
+    n0 = cache.kernel_launches()
+    b.decode(qs, o1, 1)
+    b.decode(qs, o2, 1)
+    torch.cuda.synchronize()
+    assert all(torch.equal(a, c) for a, c in zip(o1, o2))
+    assert cache.kernel_launches() > n0
