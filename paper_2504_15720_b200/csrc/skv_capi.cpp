@@ -584,15 +584,21 @@ skv_status skv_pool_create(const skv_model_desc* models, int32_t n, int32_t tpb,
       (st = dev_alloc(p, &d.free_E, n)) || (st = dev_alloc(p, &d.free_R, n)) ||
       (st = dev_alloc(p, &p->d_outE, (size_t)kResultSlots * n)))
     return bail(st);
-  if (cudaMemsetAsync(d.blk_model, 0xff, pool_blocks * sizeof(int32_t) + 4, p->stream) != cudaSuccess ||
-      cudaMemsetAsync(d.req_model, 0xff, (size_t)p->R * sizeof(int32_t), p->stream) != cudaSuccess)
-    return bail(fail(p, SKV_ERR_CUDA, "memset failed"));
+  {
+    cudaError_t e1 = cudaMemsetAsync(d.blk_model, 0xff, std::max<size_t>(pool_blocks, 1) * sizeof(int32_t), p->stream);
+    cudaError_t e2 = cudaMemsetAsync(d.req_model, 0xff, (size_t)p->R * sizeof(int32_t), p->stream);
+    if (e1 != cudaSuccess || e2 != cudaSuccess)
+      return bail(cuda_fail(p, e1 != cudaSuccess ? e1 : e2, "memset"));
+  }
   {  // free bitmap: blocks [0, P) set
     std::vector<uint32_t> fb(W, 0u);
     for (size_t b = 0; b < pool_blocks; ++b) fb[b >> 5] |= 1u << (b & 31);
     long long fc = (long long)pool_blocks;
-    if (cudaMemcpy(d.free_bits, fb.data(), W * sizeof(uint32_t), cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy(d.free_count, &fc, sizeof(fc), cudaMemcpyHostToDevice) != cudaSuccess)
+    // same stream as the zeroing memsets above (the pool stream does not sync with stream 0)
+    if (cudaMemcpyAsync(d.free_bits, fb.data(), W * sizeof(uint32_t), cudaMemcpyHostToDevice, p->stream) !=
+            cudaSuccess ||
+        cudaMemcpyAsync(d.free_count, &fc, sizeof(fc), cudaMemcpyHostToDevice, p->stream) != cudaSuccess ||
+        cudaStreamSynchronize(p->stream) != cudaSuccess)
       return bail(fail(p, SKV_ERR_CUDA, "init copy failed"));
   }
   if (cudaMallocHost(reinterpret_cast<void**>(&p->h_outE), sizeof(int32_t) * kResultSlots * n) != cudaSuccess)
@@ -846,8 +852,10 @@ skv_status skv_batch_create(skv_pool* p, const int32_t* group_models, const int3
     return st;
   }
   if (total) {
-    if (cudaMemcpy(b->d_handles, b->handles.data(), total * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
-        cudaMemcpy(b->d_group, grp.data(), total * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
+    if (cudaMemcpyAsync(b->d_handles, b->handles.data(), total * 4, cudaMemcpyHostToDevice, p->stream) !=
+            cudaSuccess ||
+        cudaMemcpyAsync(b->d_group, grp.data(), total * 4, cudaMemcpyHostToDevice, p->stream) != cudaSuccess ||
+        cudaStreamSynchronize(p->stream) != cudaSuccess) {
       skv_batch_destroy(b);
       return fail(p, SKV_ERR_CUDA, "batch upload failed");
     }

@@ -219,8 +219,10 @@ def test_large_batch_grow_matches_oracle():
             assert c.try_allocate(rid, mm, 2048) == o.try_allocate(rid, mm, 2048)
     b = c.batch([(mm, [rid for rid, m2 in ids if m2 == mm]) for mm in range(4)])
     assert b.grow(1) == 256
-    for rid, mm in ids:
-        assert o.try_allocate(rid, mm, 2049)
+    for mm in range(4):  # skv_batch_grow applies try_allocate in batch (group) order
+        for rid, m2 in ids:
+            if m2 == mm:
+                assert o.try_allocate(rid, mm, 2049)
     for rid, mm in ids[::7]:
         c.free_request(rid)
         o.free_request(rid)
