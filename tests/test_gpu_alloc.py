@@ -233,3 +233,23 @@ def test_large_batch_grow_matches_oracle():
             if o.registered(x):
                 assert np.array_equal(c.block_table_np(x), o.block_table_np(x))
     assert c.stats() == o.stats()
+
+
+# --- the reference's own test file, compiled UNMODIFIED against the GPU drop-in ----------------
+DROPIN_BIN = __import__("os").path.join(__import__("os").path.dirname(O.REF_TEST_BIN), "kv_cache_test_dropin")
+
+
+@pytest.mark.skipif(not __import__("os").path.exists(DROPIN_BIN), reason="drop-in test binary not built")
+def test_reference_kv_cache_test_against_gpu_dropin():
+    """proj/tests/kv_cache_test.cpp + include/seakv/unified_kv_cache.hpp + libseakv.so:
+    identical outcome to the reference itself — 17 pass, and the reference's own
+    failing assert (:180, quirk Q1) fails with the identical residual."""
+    import re
+    import subprocess
+
+    r = subprocess.run([DROPIN_BIN], capture_output=True, text=True, timeout=600)
+    out = r.stdout + r.stderr
+    assert "SUMMARY passed=17 failed=1" in out, out
+    fails = re.findall(r"FAILURE (\S+): (.*)", out)
+    assert len(fails) == 1 and fails[0][0].endswith("kv_cache_test.cpp:180"), fails
+    assert "lhs=34839396352 " in fails[0][1]
