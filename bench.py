@@ -124,7 +124,10 @@ def setup(P, torch, args, device):
             ops.append((0, 1 + r * len(SERVICES) + m, m, args.ctx))
     granted = cache.replay(ops)
     assert granted.all(), "pool too small for the workload"
-    stream = torch.cuda.current_stream(device)
+    # a dedicated (non-blocking) stream: the legacy default stream would serialise
+    # the e2e leg's copy stream against compute
+    stream = torch.cuda.Stream(device=device)
+    torch.cuda.set_stream(stream)
     cache.set_stream(stream)
     cache.synth_fill(20250421, 1.0, stream)
     batch = cache.batch(groups)
@@ -243,15 +246,38 @@ def run_gpu(args):
     h2d = sum(x.numel() * 2 for x in hq + hk + hv) * NLAYERS
     d2h = sum(x.numel() * 2 for x in ho) * NLAYERS
 
+    # double-buffered device inputs; H2D / D2H on a copy stream overlapped with compute
+    copy_stream = torch.cuda.Stream(device=local)
+    dq = [q, [torch.empty_like(x) for x in q]]
+    dk = [k, [torch.empty_like(x) for x in k]]
+    dv = [v, [torch.empty_like(x) for x in v]]
+    do = [out, [torch.empty_like(x) for x in out]]
+    h2d_ev = [torch.cuda.Event() for _ in range(2)]
+    comp_ev = [torch.cuda.Event() for _ in range(2)]
+    d2h_ev = [torch.cuda.Event() for _ in range(2)]
+    for e in comp_ev + d2h_ev:
+        e.record(stream)
+
     def step_e2e():
         batch.grow(1)
         for layer in range(NLAYERS):
-            for a, b in zip(q + k + v, hq + hk + hv):
-                a.copy_(b, non_blocking=True)
-            batch.append(k, v, layer, 1, stream)
-            batch.decode(q, out, layer, stream=stream)
-            for a, b in zip(ho, out):
-                a.copy_(b, non_blocking=True)
+            j = layer & 1
+            with torch.cuda.stream(copy_stream):
+                copy_stream.wait_event(comp_ev[j])  # compute of layer-2 done with buffer j
+                for a, b in zip(dq[j] + dk[j] + dv[j], hq + hk + hv):
+                    a.copy_(b, non_blocking=True)
+                h2d_ev[j].record(copy_stream)
+            stream.wait_event(h2d_ev[j])
+            stream.wait_event(d2h_ev[j])  # out buffer j drained to host
+            batch.append(dk[j], dv[j], layer, 1, stream)
+            batch.decode(dq[j], do[j], layer, stream=stream)
+            comp_ev[j].record(stream)
+            with torch.cuda.stream(copy_stream):
+                copy_stream.wait_event(comp_ev[j])
+                for a, b in zip(ho, do[j]):
+                    a.copy_(b, non_blocking=True)
+                d2h_ev[j].record(copy_stream)
+        stream.wait_stream(copy_stream)
 
     for _ in range(args.warmup):
         step_e2e()

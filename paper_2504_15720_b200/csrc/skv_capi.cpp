@@ -1089,10 +1089,28 @@ skv_status skv_append_kv(skv_pool* p, skv_batch* b, const skv_append_args* a, vo
 }
 
 skv_status skv_prefill_attention(skv_pool* p, skv_batch* b, const skv_prefill_args* a, void* stream) {
-  (void)b;
-  (void)a;
-  (void)stream;
-  return fail(p, SKV_ERR_ARG, "prefill attention: not built in this version");
+  skv_status st = check_batch(p, b);
+  if (st) return st;
+  if ((st = ensure_storage(p))) return st;
+  if (a->q_len < 1) return fail(p, SKV_ERR_ARG, "prefill: q_len must be >= 1");
+  for (int i = 0; i < b->nreq; ++i)
+    if (p->req[b->handles[i]].tokens < a->q_len)
+      return fail(p, SKV_ERR_ARG, "prefill: request " + std::to_string(b->ids[i]) + " holds fewer than q_len tokens");
+  DeviceGuard guard(p->device);
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : p->stream;
+  skv::DataParams dp;
+  if ((st = make_params(p, b, a->layer, &dp))) return st;
+  for (int g = 0; g < b->ngroups; ++g) {
+    dp.g[g].q = a->q[g];
+    dp.g[g].out = a->out[g];
+  }
+  const float scale = a->softmax_scale > 0.f ? a->softmax_scale : 1.0f / std::sqrt(128.0f);
+  dp.scale_log2 = scale * 1.4426950408889634f;
+  dp.n_new = a->q_len;
+  if ((st = order_streams(p, s))) return st;
+  skv::launch_prefill(dp, s);
+  p->launches++;
+  return after_data(p, s);
 }
 
 skv_status skv_model_layout(const skv_pool* p, int32_t m, skv_layout* out) {

@@ -1,0 +1,372 @@
+// skv_prefill.cu — causal chunked-prefill attention over the unified pool on the
+// 5th-generation tensor cores (tcgen05.mma, accumulators in TMEM), sm_100a.
+//
+// One CTA (4 warps, 128 threads) per (request, kv head, 128-row query tile).
+// GQA query rows are folded into M: row i of a tile is (token t0 + i/G, q head
+// kv_head*G + i%G), so one K/V tile feeds G query heads.  Per 128-key tile:
+//
+//   K_j, V_j  : gathered from the pool through the block table with cp.async
+//               (16 B per thread, written straight into the 128B-swizzled UMMA
+//               operand layout), double buffered so tile j+1 streams in while
+//               tile j is on the tensor cores;
+//   S   = Q·K_jᵀ    tcgen05.mma kind::f16, M=128 N=128 K=16 x8, fp32 in TMEM
+//   softmax         thread i owns row i: tcgen05.ld its S row from TMEM lanes,
+//                   causal mask, online max/sum in the log2 domain, P (fp16/bf16)
+//                   written to smem in the swizzled K-major layout;
+//   O_j = P·V_j     tcgen05.mma (B = V, MN-major), fp32 in TMEM, folded into the
+//                   per-thread fp32 output row with the softmax correction.
+//
+// UMMA operand layouts (cute canonical SW128): a [R rows x 128
+// d] fp16 tile is two 64-element column halves of R x 128 B; row r of a half at
+// (r/8)*1024 + (r%8)*128, 16-byte chunk c stored at chunk c ^ (r%8).  Q, K and P
+// use K-major descriptors (SBO = 1024 B, advance 32 B per K=16 step); V uses an
+// MN-major descriptor (LBO = 16 KiB between d-halves, SBO = 1024 B, advance
+// 2 KiB per 16 keys).
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "skv_internal.h"
+
+namespace skv {
+
+namespace {
+
+constexpr int kD = 128;
+constexpr int kTpb = 16;
+constexpr int kRows = 128;                  // M (query rows per CTA)
+constexpr int kKeys = 128;                  // N (keys per tile)
+constexpr int kTileBytes = kRows * kD * 2;  // 32 KiB per operand tile
+constexpr int kHalf = kRows * 128;          // bytes of one 64-element column half
+constexpr int kThreads = 128;
+constexpr int kSmem = 6 * kTileBytes + 1024 + 64;  // Q, K[2], V[2], P + alignment + barrier/tmem slot
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// byte offset of (row, 16B-chunk c in 0..15) in a swizzled [128 x 128] fp16 tile
+__device__ __forceinline__ uint32_t sw_off(int row, int c) {
+  const int half = c >> 3, cc = c & 7;
+  return half * kHalf + (row >> 3) * 1024 + (row & 7) * 128 + ((cc ^ (row & 7)) << 4);
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool valid) {
+  const int n = valid ? 16 : 0;  // n = 0: zero-fill (src not read)
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// SW128 UMMA shared-memory descriptor (cute::UMMA::SmemDescriptor, version 1).
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // version (Blackwell)
+  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+  return d;
+}
+
+// kind::f16 instruction descriptor: fp32 accumulate, M=128, N=128.
+__device__ __forceinline__ uint32_t make_idesc(int bf16, int b_mn_major) {
+  uint32_t d = 0;
+  d |= 1u << 4;                   // D format f32
+  d |= (uint32_t)bf16 << 7;       // A format (0 f16, 1 bf16)
+  d |= (uint32_t)bf16 << 10;      // B format
+  d |= (uint32_t)b_mn_major << 16;  // B major (0 K, 1 MN); A is K-major
+  d |= (uint32_t)(kKeys >> 3) << 17;  // N >> 3
+  d |= (uint32_t)(kRows >> 4) << 24;  // M >> 4
+  return d;
+}
+
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  }
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+        "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+        "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+        "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int k = 0; k < 32; ++k) v[k] = __uint_as_float(r[k]);
+}
+
+template <typename T>
+__device__ __forceinline__ uint32_t pack2(float a, float b);
+template <>
+__device__ __forceinline__ uint32_t pack2<__half>(float a, float b) {
+  __half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+template <>
+__device__ __forceinline__ uint32_t pack2<__nv_bfloat16>(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_constant__ DataParams p) {
+  extern __shared__ char smem_raw[];
+  char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  char* sQ = smem;
+  char* sK[2] = {smem + kTileBytes, smem + 2 * kTileBytes};
+  char* sV[2] = {smem + 3 * kTileBytes, smem + 4 * kTileBytes};
+  char* sP = smem + 5 * kTileBytes;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 6 * kTileBytes);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + 6 * kTileBytes + 16);
+
+  const int r = blockIdx.z, h = blockIdx.y, tile = blockIdx.x;
+  const int grp = p.req_group[r];
+  const DataGroup& g = p.g[grp];
+  const int G = g.G;
+  const int q_len = p.n_new;
+  if (!g.active || h >= g.Hkv || tile * kRows >= q_len * G) return;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int handle = p.handles[r];
+  const int ctx = p.req_tokens[handle];
+  const int start = ctx - q_len;
+  const int tpt = kRows / G;  // tokens per tile
+  const int t0 = tile * tpt;
+  const int n_keys = min(ctx, start + t0 + tpt);
+  const int n_kt = (n_keys + kKeys - 1) / kKeys;
+  const int2* row_tab = p.req_table + (size_t)handle * p.cap;
+  const char* kv_base = p.pool + g.layer_off + (long long)h * g.head_stride;
+  const int rl = r - g.req_begin;
+
+  if (warp == 0) {  // TMEM: S in columns [0,128), O tile in [128,256)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem_S = tmem, tmem_O = tmem + 128;
+  const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+
+  // ---- Q tile: row i = (token t0 + i/G, head h*G + i%G); coalesced 16 B per thread --------
+  {
+    const int c = tid & 15;
+    for (int i = 0; i < 16; ++i) {
+      const int row = (tid >> 4) + 8 * i;
+      const int tok = t0 + row / G, gg = row % G;
+      const bool ok = tok < q_len;
+      const char* src = reinterpret_cast<const char*>(g.q) +
+                        (((size_t)rl * q_len + (ok ? tok : 0)) * g.Hq + h * G + gg) * (kD * 2) + c * 16;
+      cp_async16(smem_u32(sQ) + sw_off(row, c), src, ok);
+    }
+  }
+  auto load_kv = [&](int j, int buf) {
+    const int c = tid & 15;
+    for (int i = 0; i < 16; ++i) {
+      const int key = (tid >> 4) + 8 * i;
+      const int a = j * kKeys + key;
+      const bool ok = a < n_keys;
+      int2 e = make_int2(0, 0);
+      if (ok) e = row_tab[a / kTpb];
+      const char* src = kv_base + (long long)e.x * p.merged_stride + (long long)e.y * g.native_stride +
+                        (a % kTpb) * (kD * 2) + c * 16;
+      cp_async16(smem_u32(sK[buf]) + sw_off(key, c), src, ok);
+      cp_async16(smem_u32(sV[buf]) + sw_off(key, c), src + kTpb * kD * 2, ok);
+    }
+  };
+  load_kv(0, 0);
+  cp_async_commit();
+
+  const uint32_t idesc_qk = make_idesc(p.dtype, 0);
+  const uint32_t idesc_pv = make_idesc(p.dtype, 1);
+  const int row = tid;  // this thread's query row (TMEM lane)
+  const int my_tok = t0 + row / G;
+  const bool row_ok = my_tok < q_len;
+  const int my_pos = start + my_tok;  // absolute position: keys <= my_pos are visible
+  float o[kD];
+#pragma unroll
+  for (int k = 0; k < kD; ++k) o[k] = 0.f;
+  float m = -INFINITY, l = 0.f;
+  uint32_t phase = 0;
+
+  for (int j = 0; j < n_kt; ++j) {
+    if (j + 1 < n_kt) {
+      load_kv(j + 1, (j + 1) & 1);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    fence_async_smem();
+    __syncthreads();
+    const int buf = j & 1;
+    if (tid == 0) {
+      tc_fence_after();
+#pragma unroll
+      for (int k = 0; k < kD / 16; ++k) {
+        const uint32_t off = (k >> 2) * kHalf + (k & 3) * 32;
+        mma_f16(tmem_S, make_desc(smem_u32(sQ) + off, 16, 1024), make_desc(smem_u32(sK[buf]) + off, 16, 1024),
+                idesc_qk, k > 0);
+      }
+      mma_commit(bar);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    tc_fence_after();
+
+    // ---- softmax on this thread's row ---------------------------------------------------
+    float mx = -INFINITY;
+    float s[32];
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) {
+      tmem_ld32(tmem_S + lane_off + cc * 32, s);
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        const int a = j * kKeys + cc * 32 + k;
+        const float v = (row_ok && a <= my_pos) ? s[k] * p.scale_log2 : -INFINITY;
+        mx = fmaxf(mx, v);
+      }
+    }
+    const float m_new = fmaxf(m, mx);
+    const float alpha = (m_new == -INFINITY) ? 1.f : exp2f(m - m_new);
+    float lsum = 0.f;
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) {
+      tmem_ld32(tmem_S + lane_off + cc * 32, s);
+      uint32_t packed[16];
+#pragma unroll
+      for (int k = 0; k < 32; k += 2) {
+        const int a = j * kKeys + cc * 32 + k;
+        const float v0 = (row_ok && a <= my_pos) ? exp2f(s[k] * p.scale_log2 - m_new) : 0.f;
+        const float v1 = (row_ok && a + 1 <= my_pos) ? exp2f(s[k + 1] * p.scale_log2 - m_new) : 0.f;
+        lsum += v0 + v1;
+        packed[k >> 1] = pack2<T>(v0, v1);
+      }
+      // 32 keys = 64 B = chunks 4cc .. 4cc+3 of the P row
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) {
+        const uint4 val = make_uint4(packed[4 * q4], packed[4 * q4 + 1], packed[4 * q4 + 2], packed[4 * q4 + 3]);
+        *reinterpret_cast<uint4*>(sP + sw_off(row, cc * 4 + q4)) = val;
+      }
+    }
+    l = l * alpha + lsum;
+    m = m_new;
+    tc_fence_before();
+    fence_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+#pragma unroll
+      for (int k = 0; k < kKeys / 16; ++k) {
+        const uint32_t aoff = (k >> 2) * kHalf + (k & 3) * 32;
+        mma_f16(tmem_O, make_desc(smem_u32(sP) + aoff, 16, 1024),
+                make_desc(smem_u32(sV[buf]) + k * 2048, kHalf, 1024), idesc_pv, k > 0);
+      }
+      mma_commit(bar);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    tc_fence_after();
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) {
+      tmem_ld32(tmem_O + lane_off + cc * 32, s);
+#pragma unroll
+      for (int k = 0; k < 32; ++k) o[cc * 32 + k] = o[cc * 32 + k] * alpha + s[k];
+    }
+    tc_fence_before();
+    __syncthreads();  // S/O TMEM and K/V/P buffers are free for the next tile
+  }
+
+  if (row_ok) {
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    char* dst = reinterpret_cast<char*>(g.out) +
+                (((size_t)rl * q_len + my_tok) * g.Hq + h * G + row % G) * (kD * 2);
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+      uint4 v;
+      v.x = pack2<T>(o[8 * c] * inv, o[8 * c + 1] * inv);
+      v.y = pack2<T>(o[8 * c + 2] * inv, o[8 * c + 3] * inv);
+      v.z = pack2<T>(o[8 * c + 4] * inv, o[8 * c + 5] * inv);
+      v.w = pack2<T>(o[8 * c + 6] * inv, o[8 * c + 7] * inv);
+      *reinterpret_cast<uint4*>(dst + c * 16) = v;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+  }
+}
+
+template <typename T>
+void launch_prefill_t(const DataParams& p, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(prefill_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    attr = true;
+  }
+  int tiles = 1, heads = 1;
+  for (int i = 0; i < p.ngroups; ++i) {
+    tiles = max(tiles, (p.n_new * p.g[i].G + kRows - 1) / kRows);
+    heads = max(heads, p.g[i].Hkv);
+  }
+  dim3 grid(tiles, heads, p.nreq);
+  prefill_kernel<T><<<grid, kThreads, kSmem, s>>>(p);
+}
+
+}  // namespace
+
+void launch_prefill(const DataParams& p, cudaStream_t s) {
+  if (p.nreq <= 0) return;
+  if (p.dtype == 0) launch_prefill_t<__half>(p, s);
+  else launch_prefill_t<__nv_bfloat16>(p, s);
+}
+
+}  // namespace skv
