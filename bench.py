@@ -246,8 +246,10 @@ def run_gpu(args):
     h2d = sum(x.numel() * 2 for x in hq + hk + hv) * NLAYERS
     d2h = sum(x.numel() * 2 for x in ho) * NLAYERS
 
-    # double-buffered device inputs; H2D / D2H on a copy stream overlapped with compute
-    copy_stream = torch.cuda.Stream(device=local)
+    # double-buffered device inputs; H2D and D2H each on their own stream so the
+    # copies of layer l+1 / l-1 overlap the attention of layer l
+    h2d_stream = torch.cuda.Stream(device=local)
+    d2h_stream = torch.cuda.Stream(device=local)
     dq = [q, [torch.empty_like(x) for x in q]]
     dk = [k, [torch.empty_like(x) for x in k]]
     dv = [v, [torch.empty_like(x) for x in v]]
@@ -262,22 +264,23 @@ def run_gpu(args):
         batch.grow(1)
         for layer in range(NLAYERS):
             j = layer & 1
-            with torch.cuda.stream(copy_stream):
-                copy_stream.wait_event(comp_ev[j])  # compute of layer-2 done with buffer j
+            with torch.cuda.stream(h2d_stream):
+                h2d_stream.wait_event(comp_ev[j])  # compute of layer-2 is done with buffer j
                 for a, b in zip(dq[j] + dk[j] + dv[j], hq + hk + hv):
                     a.copy_(b, non_blocking=True)
-                h2d_ev[j].record(copy_stream)
+                h2d_ev[j].record(h2d_stream)
             stream.wait_event(h2d_ev[j])
             stream.wait_event(d2h_ev[j])  # out buffer j drained to host
             batch.append(dk[j], dv[j], layer, 1, stream)
             batch.decode(dq[j], do[j], layer, stream=stream)
             comp_ev[j].record(stream)
-            with torch.cuda.stream(copy_stream):
-                copy_stream.wait_event(comp_ev[j])
+            with torch.cuda.stream(d2h_stream):
+                d2h_stream.wait_event(comp_ev[j])
                 for a, b in zip(ho, do[j]):
                     a.copy_(b, non_blocking=True)
-                d2h_ev[j].record(copy_stream)
-        stream.wait_stream(copy_stream)
+                d2h_ev[j].record(d2h_stream)
+        stream.wait_stream(d2h_stream)
+        stream.wait_stream(h2d_stream)
 
     for _ in range(args.warmup):
         step_e2e()
