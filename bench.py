@@ -96,32 +96,86 @@ class Clocks:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def pool_blocks_for(P, ctx_max, nreq):
-    tot = 0
-    for name, L, H, Hq in SERVICES:
-        spec = P.ModelSpec(name, L, H, 128, 2, Hq)
-        sub = int(P.plan_merged_shape([P.ModelSpec(n, l, h, 128, 2, q) for n, l, h, q in SERVICES]) //
-                  P.native_block_bytes(spec))
-        slots = nreq * ((ctx_max + 15) // 16)
-        tot += (slots + sub - 1) // sub
-    return tot + 64
+SERVICES_C1 = [("llama-2-7b", 32, 32, 32), ("llama-2-13b", 40, 40, 40)]
+
+
+class Workload:
+    """services [(name, layers, kv_heads, q_heads)], per-service request contexts,
+    physical layers per native block (0 = faithful all-layer layout), pool blocks."""
+
+    def __init__(self, name, services, ctxs, phys_layers, pool_blocks, desc):
+        self.name, self.services, self.ctxs = name, services, ctxs
+        self.phys_layers, self.pool_blocks, self.desc = phys_layers, pool_blocks, desc
+        self.nlayers = max(L for _, L, _, _ in services)
+
+
+def _subs(P, services):
+    specs = [P.ModelSpec(n, L, H, 128, 2, Hq) for n, L, H, Hq in services]
+    merged = P.plan_merged_shape(specs)
+    return [int(merged // P.native_block_bytes(s)) for s in specs], merged
+
+
+def _blocks(P, services, ctxs, grow):
+    subs, _ = _subs(P, services)
+    return sum(-(-sum((c + grow + 15) // 16 for c in cl) // sub) for sub, cl in zip(subs, ctxs)) + 64
+
+
+def make_workload(P, args):
+    grow = args.warmup * 2 + args.steps * 2 + 8
+    if args.workload == "config1":
+        ctxs = [[args.ctx or 512] * (args.requests or 32) for _ in SERVICES_C1]
+        return Workload("config1", SERVICES_C1, ctxs, 0, _blocks(P, SERVICES_C1, ctxs, grow),
+                        f"config1: llama-2-7b + llama-2-13b shapes, {len(ctxs[0])} decode requests each, ctx "
+                        f"{ctxs[0][0]}+, fp16, faithful all-layer merged-block pool")
+    if args.workload == "config4":
+        # long context, skewed lengths: seeded lognormal (median 4K tokens) capped at 32K,
+        # services round-robin until the requests fill ~95 % of a ~150 GB pool
+        subs, merged = _subs(P, SERVICES)
+        pool = int(150e9 // merged)
+        rng = np.random.default_rng(32768)
+        ctxs = [[] for _ in SERVICES]
+        used = [0] * len(SERVICES)  # native slots per service
+        m = 0
+        while True:
+            c = int(min(32768, max(256, rng.lognormal(np.log(4096), 1.0))))
+            trial = list(used)
+            trial[m] += (c + grow + 15) // 16
+            if sum(-(-u // sb) for u, sb in zip(trial, subs)) > 0.95 * pool:
+                break
+            used = trial
+            ctxs[m].append(c)
+            m = (m + 1) % len(SERVICES)
+        return Workload("config4", SERVICES, ctxs, 0, pool,
+                        f"config4: 4 services (config-2 shapes), {sum(map(len, ctxs))} requests, ctx lognormal "
+                        f"(median 4096, max 32768; max drawn {max(max(c) for c in ctxs)}), faithful all-layer pool of "
+                        f"{pool} merged blocks (~150 GB) filled to ~95 %, split-KV decode")
+    nreq = args.requests or 256
+    ctx = args.ctx or 2048
+    ctxs = [[ctx] * nreq for _ in SERVICES]
+    return Workload("config2", SERVICES, ctxs, args.phys_layers, _blocks(P, SERVICES, ctxs, grow),
+                    f"config2-layer-sliced: 4 services (llama-3-8b, mistral-7b, llama-2-13b, opt-6.7b) x {nreq} "
+                    f"decode requests, ctx {ctx}+, one unified pool; {args.phys_layers} physical layers per native "
+                    f"block (logical l -> l % {args.phys_layers}), 40 layer-index launches per step")
 
 
 def setup(P, torch, args, device):
-    models = [P.ModelSpec(n, L, H, 128, 2, Hq) for n, L, H, Hq in SERVICES]
-    nreq = args.requests
-    ctx_max = args.ctx + args.warmup + args.steps * 2 + 8
-    pool_blocks = pool_blocks_for(P, ctx_max, nreq)
-    cache = P.UnifiedKvCache(models, 16, 1, pool_blocks, device=device, dtype=P.FP16,
-                             phys_layers=args.phys_layers, max_requests=4 * nreq + 16,
+    wl = make_workload(P, args)
+    models = [P.ModelSpec(n, L, H, 128, 2, Hq) for n, L, H, Hq in wl.services]
+    ctx_max = max(max(c) for c in wl.ctxs if c) + args.warmup * 2 + args.steps * 2 + 8
+    nreq_total = sum(len(c) for c in wl.ctxs)
+    cache = P.UnifiedKvCache(models, 16, 1, wl.pool_blocks, device=device, dtype=P.FP16,
+                             phys_layers=wl.phys_layers, max_requests=nreq_total + 16,
                              max_blocks_per_request=(ctx_max + 15) // 16 + 1, allocate_storage=True)
-    groups = []
+    ns = len(wl.services)
+    groups = [(m, []) for m in range(ns)]
     ops = []
-    for m in range(len(SERVICES)):
-        groups.append((m, [1 + r * len(SERVICES) + m for r in range(nreq)]))
-    for r in range(nreq):  # interleaved arrival order across services
-        for m in range(len(SERVICES)):
-            ops.append((0, 1 + r * len(SERVICES) + m, m, args.ctx))
+    rid = 1
+    for r in range(max(len(c) for c in wl.ctxs)):  # interleaved arrival order across services
+        for m in range(ns):
+            if r < len(wl.ctxs[m]):
+                ops.append((0, rid, m, wl.ctxs[m][r]))
+                groups[m][1].append(rid)
+                rid += 1
     granted = cache.replay(ops)
     assert granted.all(), "pool too small for the workload"
     # a dedicated (non-blocking) stream: the legacy default stream would serialise
@@ -132,21 +186,21 @@ def setup(P, torch, args, device):
     cache.synth_fill(20250421, 1.0, stream)
     batch = cache.batch(groups)
     g = torch.Generator(device=device).manual_seed(1)
-    q = [torch.randn((nreq, Hq, 128), generator=g, device=device).half() for _, _, _, Hq in SERVICES]
+    sizes = [len(ids) for _, ids in groups]
+    q = [torch.randn((n, Hq, 128), generator=g, device=device).half() for n, (_, _, _, Hq) in zip(sizes, wl.services)]
     out = [torch.empty_like(x) for x in q]
-    k = [torch.randn((nreq, 1, H, 128), generator=g, device=device).half() * 0.5 for _, _, H, _ in SERVICES]
-    v = [torch.randn((nreq, 1, H, 128), generator=g, device=device).half() * 0.5 for _, _, H, _ in SERVICES]
+    k = [torch.randn((n, 1, H, 128), generator=g, device=device).half() * 0.5 for n, (_, _, H, _) in
+         zip(sizes, wl.services)]
+    v = [torch.randn((n, 1, H, 128), generator=g, device=device).half() * 0.5 for n, (_, _, H, _) in
+         zip(sizes, wl.services)]
     torch.cuda.synchronize(device)
-    return cache, batch, q, out, k, v, stream
+    return wl, cache, batch, q, out, k, v, stream
 
 
-NLAYERS = max(L for _, L, _, _ in SERVICES)
-
-
-def step_device(batch, q, out, k, v, stream, ev=None):
+def step_device(batch, q, out, k, v, stream, nlayers, ev=None):
     """One decode step; optional per-layer decode events for the kernel roofline."""
     batch.grow(1)
-    for layer in range(NLAYERS):
+    for layer in range(nlayers):
         batch.append(k, v, layer, 1, stream)
         if ev is not None:
             ev[layer][0].record(stream)
@@ -155,9 +209,9 @@ def step_device(batch, q, out, k, v, stream, ev=None):
             ev[layer][1].record(stream)
 
 
-def step_bytes(batch):
+def step_bytes(batch, nlayers):
     kv = tot = 0.0
-    for layer in range(NLAYERS):
+    for layer in range(nlayers):
         a, b = batch.decode_bytes(layer)
         kv += a
         tot += b
@@ -177,7 +231,8 @@ def run_gpu(args):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    cache, batch, q, out, k, v, stream = setup(P, torch, args, local)
+    wl, cache, batch, q, out, k, v, stream = setup(P, torch, args, local)
+    NLAYERS = wl.nlayers
 
     def barrier():
         torch.cuda.synchronize()
@@ -200,7 +255,7 @@ def run_gpu(args):
 
     # ---- device-resident timed region (value) ------------------------------------------
     for _ in range(args.warmup):
-        step_device(batch, q, out, k, v, stream)
+        step_device(batch, q, out, k, v, stream, NLAYERS)
     barrier()
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(NLAYERS)]
     kv_total = all_total = 0.0
@@ -216,9 +271,9 @@ def run_gpu(args):
             s0 = torch.cuda.Event(enable_timing=True)
             s1 = torch.cuda.Event(enable_timing=True)
             s0.record(stream)
-            step_device(batch, q, out, k, v, stream, ev)
+            step_device(batch, q, out, k, v, stream, NLAYERS, ev)
             s1.record(stream)
-            kvb, totb = step_bytes(batch)  # host mirror: exact context of this step
+            kvb, totb = step_bytes(batch, NLAYERS)  # host mirror: exact context of this step
             kv_total += kvb
             all_total += totb
             dec_bytes += totb
@@ -231,10 +286,20 @@ def run_gpu(args):
     elapsed_ms = max_over_ranks(t0.elapsed_time(t1))
     kv_all = sum_over_ranks(kv_total)
     value = kv_all / (elapsed_ms / 1e3) / 1e9
-    tokens_s = sum_over_ranks(float(args.requests * len(SERVICES) * args.steps)) / (elapsed_ms / 1e3)
+    tokens_s = sum_over_ranks(float(sum(len(c) for c in wl.ctxs) * args.steps)) / (elapsed_ms / 1e3)
     hbm, peak_kind = peaks()
     achieved = dec_bytes / (dec_ms / 1e3) / 1e9  # algorithmic bytes / decode launch time
     n_launch = args.steps * NLAYERS
+
+    # ---- allocator: decode-step growth of the whole batch (host mirror + GPU placement) ---
+    torch.cuda.synchronize()
+    a0 = time.perf_counter()
+    na = 16
+    for _ in range(na):
+        batch.grow(1)
+        cache.flush(stream)
+    torch.cuda.synchronize()
+    alloc_ns = (time.perf_counter() - a0) / (na * sum(len(c) for c in wl.ctxs)) * 1e9
 
     # ---- e2e through the C-ABI with host buffers -----------------------------------------
     hq = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in q]
@@ -290,7 +355,7 @@ def run_gpu(args):
     e0.record(stream)
     for _ in range(args.steps):
         step_e2e()
-        kv_e2e += step_bytes(batch)[0]
+        kv_e2e += step_bytes(batch, NLAYERS)[0]
     e1.record(stream)
     barrier()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1))
@@ -311,16 +376,13 @@ def run_gpu(args):
         "data": "synthetic (SplitMix64 K/V pool, randn q/k/v); no checkpoints",
         "tokens_per_s": round(tokens_s, 1),
         "config": {
-            "workload": "config2-layer-sliced: 4 services (llama-3-8b, mistral-7b, llama-2-13b, opt-6.7b) x "
-                        f"{args.requests} decode requests, ctx {args.ctx}+, one unified pool; "
-                        f"{args.phys_layers} physical layers per native block (logical l -> l % "
-                        f"{args.phys_layers}), 40 layer-index launches per step",
-            "requests": args.requests * len(SERVICES) * world,
-            "ctx": args.ctx,
+            "workload": wl.desc,
+            "requests": sum(len(c) for c in wl.ctxs) * world,
+            "ctx_mean": round(float(np.mean([c for cl in wl.ctxs for c in cl])), 1),
             "pool_blocks": cache.pool_size(),
             "merged_block_bytes": cache.merged_block_bytes(),
             "pool_gb": round(cache.storage()[1] / 1e9, 2),
-            "l2": "inputs larger than L2 (23.6 GB per layer launch vs 126 MB L2); no flush",
+            "l2": "inputs larger than L2 (>= 0.6 GB K/V per layer launch vs 126 MB L2); no flush",
             "parallelism": f"placement-sharded replicas x{world} (tp=1 groups, no collective)",
         },
         "e2e": {"value": round(e2e_value, 1), "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
@@ -330,6 +392,8 @@ def run_gpu(args):
                      "frac": round(achieved / hbm, 4), "traffic": None,
                      "avg_launch_ms": round(dec_ms / n_launch, 4),
                      "bytes_per_launch": round(dec_bytes / n_launch, 1)},
+        "allocator": {"ns_per_grow_op": round(alloc_ns, 2),
+                      "note": "batch.grow(1) of every request + GPU placement kernel, wall clock incl. sync"},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
@@ -397,7 +461,8 @@ def cpu_baseline(cache, batch, q, args, budget_s=None):
     dt = time.perf_counter() - t0
     return {"value": round(nbytes * reps / dt / 1e9, 3), "unit": "GB/s", "cores": cores, "kind": "port",
             "sample": f"fp32 oracle decode, layer 0, first {per} requests of each of the 4 services at ctx "
-                      f"~{args.ctx}, {reps} reps in {dt:.1f} s (attention has no reference implementation; "
+                      f"~{int(np.mean([c for c in (cache.request_tokens(r) for _, ids in groups for r in ids[:per])]))}, "
+                      f"{reps} reps in {dt:.1f} s (attention has no reference implementation; "
                       "oracle/attn_oracle.c)"}
 
 
@@ -411,16 +476,19 @@ def run_reference(args):
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle_py as O
 
+    services = SERVICES_C1 if args.workload == "config1" else SERVICES
+    ctx_default = {"config1": 512, "config2": 2048, "config4": 4096}[args.workload]
+    args.ctx = args.ctx or ctx_default
     cores = os.cpu_count() or 1
     # synthetic host pool for a bounded sample: per service `per` requests at ctx
     per = args.cpu_requests
-    models = [(L, H, 128, 2) for _, L, H, _ in SERVICES]
+    models = [(L, H, 128, 2) for _, L, H, _ in services]
     allocator = O.RefCache(models, pool=200000) if O.ref_available() else O.OracleCache(models, pool=200000)
     kind = "reference" if O.ref_available() else "port"
     rid = 1
-    ids = {m: [] for m in range(len(SERVICES))}
+    ids = {m: [] for m in range(len(services))}
     for r in range(per):
-        for m in range(len(SERVICES)):
+        for m in range(len(services)):
             assert allocator.try_allocate(rid, m, args.ctx)
             ids[m].append(rid)
             rid += 1
@@ -434,11 +502,11 @@ def run_reference(args):
     Lp = args.phys_layers
     stride = 0
     lays = []
-    for m, (name, L, H, Hq) in enumerate(SERVICES):
+    for m, (name, L, H, Hq) in enumerate(services):
         layer_stride = H * 2 * 16 * 128 * 2
         native = min(Lp, L) * layer_stride
         lays.append((L, H, Hq, layer_stride, native))
-    sub = [int(merged // (16 * L * 2 * H * 128 * 2)) for _, L, H, _ in SERVICES]
+    sub = [int(merged // (16 * L * 2 * H * 128 * 2)) for _, L, H, _ in services]
     stride = max(s * l[4] for s, l in zip(sub, lays))
     stride = (stride + 255) // 256 * 256
     img = rng.integers(0, 0x3C00, size=len(used) * stride // 2, dtype=np.uint16).view(np.uint8)
@@ -462,9 +530,19 @@ def run_reference(args):
     times = [one_step() for _ in range(args.steps)]
     dt = sum(times)
     value = nbytes * len(times) / dt / 1e9
-    ops = [(0, i, m, args.ctx + 1) for m in ids for i in ids[m]]
+    # allocator: the decode-step op stream of the workload's request count (every request
+    # +1 token per step, 64 steps), replayed through the reference allocator single-threaded
+    # (kv_cache.hpp:45); the array is built before the timer starts
+    n_alloc_req = (args.requests or {"config1": 32, "config2": 256, "config4": 32}[args.workload])
+    nsteps = 64
+    acache = (O.RefCache if kind == "reference" else O.OracleCache)(models, pool=400000)
+    aops = [(0, 1 + r * len(services) + m, m, args.ctx) for r in range(n_alloc_req) for m in range(len(services))]
+    acache.replay(aops)
+    ops = [(0, 1 + r * len(services) + m, m, args.ctx + s_ + 1) for s_ in range(nsteps)
+           for r in range(n_alloc_req) for m in range(len(services))]
+    arr = O.ops_array(ops)
     t = time.perf_counter()
-    allocator.replay(ops)
+    acache.replay_array(arr, len(ops))
     alloc_ns = (time.perf_counter() - t) / max(1, len(ops)) * 1e9
     res = {
         "impl": "reference",
@@ -472,12 +550,12 @@ def run_reference(args):
         "value": round(value, 3), "unit": "GB/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt / len(times) * 1e3, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
-        "data": "synthetic", "config": {"workload": "config2 decode, bounded CPU sample", "ctx": args.ctx,
+        "data": "synthetic", "config": {"workload": f"{args.workload} decode, bounded CPU sample", "ctx": args.ctx,
                                         "requests_per_service": per},
         "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": cores, "kind": "port",
                          "sample": f"fp32 oracle decode (no reference attention exists), {per} requests per "
                                    f"service at ctx {args.ctx}, 1 layer per step; allocator: {kind} "
-                                   f"replay {alloc_ns:.1f} ns/op"},
+                                   f"replay of {len(ops)} decode-step grows, {alloc_ns:.1f} ns/op"},
         "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "allocator_ns_per_op": round(alloc_ns, 2), "allocator_kind": kind,
     }
@@ -490,11 +568,12 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--requests", type=int, default=256, help="decode requests per service")
-    ap.add_argument("--ctx", type=int, default=2048)
+    ap.add_argument("--workload", default="config2", choices=["config1", "config2", "config4"])
+    ap.add_argument("--requests", type=int, default=0, help="decode requests per service (0 = workload default)")
+    ap.add_argument("--ctx", type=int, default=0, help="context length (0 = workload default)")
     ap.add_argument("--phys-layers", dest="phys_layers", type=int, default=4)
     ap.add_argument("--cpu-seconds", dest="cpu_seconds", type=float, default=8.0)
-    ap.add_argument("--cpu-requests", dest="cpu_requests", type=int, default=4)
+    ap.add_argument("--cpu-requests", dest="cpu_requests", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", dest="no_cpu_baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":

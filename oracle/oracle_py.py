@@ -188,8 +188,11 @@ class _Api:
         return (tokens + self.tpb - 1) // self.tpb
 
     def replay(self, ops):
-        arr = ops_array(ops)
-        return self._fn("replay", C.c_long, [C.c_void_p, C.c_size_t])(self.h, arr, len(ops))
+        return self.replay_array(ops_array(ops), len(ops))
+
+    def replay_array(self, arr, n):
+        """Replays a prebuilt ops_array (so a timing of this call excludes Python)."""
+        return self._fn("replay", C.c_long, [C.c_void_p, C.c_size_t])(self.h, arr, n)
 
 
 class OracleCache(_Api):

@@ -1,0 +1,55 @@
+"""Head-sharded (tp=2) service on the GPU kernels: two rank-local pools (tp_size=2)
+plus an unsharded pool on one GPU, identical K/V written through the append
+kernel; Σ_ranks (local decode · W_o row slice) must equal the unsharded result.
+(The cross-GPU AllReduce itself is covered with gloo in test_multi_gloo.py; this
+run has one GPU.)"""
+import numpy as np
+import pytest
+
+import paper_2504_15720_b200 as P
+from paper_2504_15720_b200.tp import HeadShardedDecode, gpu_attend, head_slice
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+L, H, HQ, D, HID = 2, 8, 16, 128, 512
+CTX = [37, 100, 16, 250, 129]
+
+
+def _pool(tp, tp_rank, kv):
+    cache = P.UnifiedKvCache([P.ModelSpec("big", L, H, D, 2, HQ), P.ModelSpec("small", 2, 4, D, 2, 4)], 16, tp, 128,
+                             allocate_storage=True)
+    for i, c in enumerate(CTX):
+        assert cache.try_allocate(i + 1, 0, c)
+        assert cache.try_allocate(100 + i, 1, 2 * c + 3)
+    hs = head_slice(H, tp, tp_rank)
+    for i, c in enumerate(CTX):  # write each request's full context through the append kernel
+        b = cache.batch([(0, [i + 1])])
+        for layer in range(L):
+            k = kv[i][layer][:c, hs, 0].contiguous()[None]
+            v = kv[i][layer][:c, hs, 1].contiguous()[None]
+            b.append([k], [v], layer, n_new=c)
+    return cache
+
+
+def test_tp2_shards_sum_to_unsharded():
+    g = torch.Generator(device="cuda").manual_seed(3)
+    kv = [[(torch.randn((c, H, 2, D), generator=g, device="cuda") * 0.5).half() for _ in range(L)] for c in CTX]
+    q = torch.randn((len(CTX), HQ, D), generator=g, device="cuda").half()
+    w_o = torch.randn((HQ * D, HID), generator=g, device="cuda") / 32
+    full = _pool(1, 0, kv)
+    shards = [_pool(2, r, kv) for r in range(2)]
+    for r in range(2):
+        assert all(np.array_equal(shards[r].block_table_np(i + 1), full.block_table_np(i + 1)) for i in range(len(CTX)))
+    ids = [i + 1 for i in range(len(CTX))]
+    fb = full.batch([(0, ids)])
+    ref_step = HeadShardedDecode(w_o, HQ, D, 1, 0, attend=gpu_attend(fb, 0, 1))
+    for layer in range(L):
+        y_full = ref_step(q, layer)
+        y = torch.zeros_like(y_full)
+        for r in range(2):
+            sb = shards[r].batch([(0, ids)])
+            step = HeadShardedDecode(w_o, HQ, D, 2, r, attend=gpu_attend(sb, 0, 1))
+            y += step.partial(q[:, step.q_heads].contiguous(), layer)  # AllReduce(sum) over the TP group
+        torch.cuda.synchronize()
+        assert (y - y_full).abs().max().item() <= 1e-3 * max(1.0, y_full.abs().max().item())
