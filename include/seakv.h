@@ -143,6 +143,10 @@ void* skv_get_stream(const skv_pool* p);
 skv_status skv_batch_create(skv_pool* p, const int32_t* group_models, const int32_t* group_sizes,
                             int32_t n_groups, const uint64_t* request_ids, skv_batch** out);
 void skv_batch_destroy(skv_batch* b);
+/* Re-points an existing batch at a new request list (same semantics as create); device
+ * buffers are reused when large enough, so a serving loop can rebatch every iteration. */
+skv_status skv_batch_reset(skv_pool* p, skv_batch* b, const int32_t* group_models,
+                           const int32_t* group_sizes, int32_t n_groups, const uint64_t* request_ids);
 /* Decode-step growth: try_allocate(id, model, tokens + delta) for every request of
  * the batch, in batch order.  *n_granted = number granted (may be NULL). */
 skv_status skv_batch_grow(skv_pool* p, skv_batch* b, int64_t delta_tokens, int32_t* n_granted);

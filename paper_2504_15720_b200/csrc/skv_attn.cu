@@ -143,7 +143,7 @@ __device__ __forceinline__ float reduce_scatter16(const float (&v)[8], int lane)
 
 // One 16-token K/V tile for G query heads sharing a KV head.
 // Lane (c = lane&15, hf = lane>>4) reads dims [8c, 8c+8) of tokens 2i+hf.
-template <typename T, int G>
+template <typename T, int G, bool PARTIAL>
 __device__ __forceinline__ void consume_tile(const char* tile, int lane, int valid,
                                              const float (&q)[G][8], float (&o)[G][8],
                                              float (&mx)[G], float (&l)[G]) {
@@ -184,7 +184,8 @@ __device__ __forceinline__ void consume_tile(const char* tile, int lane, int val
   const char* vt = tile + kTpb * kD * 2;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    const uint4 raw = *reinterpret_cast<const uint4*>(vt + (2 * i + hf) * (kD * 2) + c * 16);
+    uint4 raw = *reinterpret_cast<const uint4*>(vt + (2 * i + hf) * (kD * 2) + c * 16);
+    if (PARTIAL && 2 * i + hf >= valid) raw = make_uint4(0u, 0u, 0u, 0u);  // unwritten slots may hold NaN
     float vf[8];
     Cvt<T>::to_f32(raw, vf);
     const int src = (hf << 4) | (i << 1);
@@ -298,7 +299,8 @@ __device__ __forceinline__ void process_item(const DataParams& p, Producer& P, c
     const uint32_t phase = (P.consumed / kStages) & 1u;
     mbar_wait(&w.bars[stage], phase);
     const int valid = min(kTpb, it.w - b * kTpb);
-    consume_tile<T, G>(w.tiles + stage * kTile, lane, valid, q, o, mx, l);
+    if (valid == kTpb) consume_tile<T, G, false>(w.tiles + stage * kTile, lane, valid, q, o, mx, l);
+    else consume_tile<T, G, true>(w.tiles + stage * kTile, lane, valid, q, o, mx, l);
     __syncwarp();
     P.consumed++;
     fill(p, P, w);

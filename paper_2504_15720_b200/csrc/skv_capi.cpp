@@ -122,8 +122,12 @@ struct skv_batch {
   std::vector<int> gmodel, gsize, gbegin;
   std::vector<uint64_t> ids;
   std::vector<int> handles;
+  std::vector<int32_t> h_group;
   int32_t* d_handles = nullptr;
   int32_t* d_group = nullptr;
+  size_t req_cap = 0;
+  void* h_stage = nullptr;  // pinned upload staging
+  cudaEvent_t stage_ev = nullptr;
   int nreq = 0;
   // decode plan workspace
   int4* d_items = nullptr;
@@ -808,60 +812,86 @@ skv_status skv_set_stream(skv_pool* p, void* stream) {
 void* skv_get_stream(const skv_pool* p) { return p->stream; }
 
 // ------------------------------------------------------------------ batches --------
-skv_status skv_batch_create(skv_pool* p, const int32_t* group_models, const int32_t* group_sizes,
-                            int32_t n_groups, const uint64_t* request_ids, skv_batch** out) {
-  *out = nullptr;
+static skv_status batch_fill(skv_pool* p, skv_batch* b, const int32_t* group_models, const int32_t* group_sizes,
+                             int32_t n_groups, const uint64_t* request_ids) {
   if (n_groups <= 0 || n_groups > skv::kMaxGroups) return fail(p, SKV_ERR_ARG, "batch: 1..16 groups");
-  auto b = new skv_batch();
-  b->pool = p;
   b->ngroups = n_groups;
+  b->gmodel.clear();
+  b->gsize.clear();
+  b->gbegin.clear();
+  b->ids.clear();
+  b->handles.clear();
+  b->h_group.clear();
   int total = 0;
-  std::vector<int32_t> grp;
   for (int g = 0; g < n_groups; ++g) {
-    if (group_models[g] < 0 || group_models[g] >= p->M || group_sizes[g] < 0) {
-      delete b;
+    if (group_models[g] < 0 || group_models[g] >= p->M || group_sizes[g] < 0)
       return fail(p, SKV_ERR_ARG, "batch: bad group");
-    }
     b->gmodel.push_back(group_models[g]);
     b->gsize.push_back(group_sizes[g]);
     b->gbegin.push_back(total);
     for (int i = 0; i < group_sizes[g]; ++i) {
       const uint64_t id = request_ids[total + i];
       auto it = p->id2h.find(id);
-      if (it == p->id2h.end()) {
-        delete b;
-        return fail(p, SKV_ERR_LOGIC, "batch: unknown request " + std::to_string(id));
-      }
-      if (p->req[it->second].nslots > 0 && p->req[it->second].model != group_models[g]) {
-        delete b;
+      if (it == p->id2h.end()) return fail(p, SKV_ERR_LOGIC, "batch: unknown request " + std::to_string(id));
+      if (p->req[it->second].nslots > 0 && p->req[it->second].model != group_models[g])
         return fail(p, SKV_ERR_LOGIC, "batch: request belongs to another model");
-      }
       b->ids.push_back(id);
       b->handles.push_back(it->second);
-      grp.push_back(g);
+      b->h_group.push_back(g);
     }
     total += group_sizes[g];
   }
   b->nreq = total;
   DeviceGuard guard(p->device);
-  skv_status st;
-  if ((st = dev_alloc(p, &b->d_handles, total, false)) || (st = dev_alloc(p, &b->d_group, total, false)) ||
-      (st = dev_alloc(p, &b->d_nitems, 1)) || (st = dev_alloc(p, &b->d_counter, 1)) ||
-      (st = dev_alloc(p, &b->d_pbase, total)) || (st = dev_alloc(p, &b->d_nsplit, total))) {
+  if ((size_t)total > b->req_cap) {
+    SKV_CUDA(p, cudaStreamSynchronize(p->stream));
+    for (void* q : {(void*)b->d_handles, (void*)b->d_group, (void*)b->d_pbase, (void*)b->d_nsplit})
+      if (q) cudaFree(q);
+    b->req_cap = std::max<size_t>((size_t)total * 2, 64);
+    skv_status st;
+    if ((st = dev_alloc(p, &b->d_handles, b->req_cap, false)) || (st = dev_alloc(p, &b->d_group, b->req_cap, false)) ||
+        (st = dev_alloc(p, &b->d_pbase, b->req_cap)) || (st = dev_alloc(p, &b->d_nsplit, b->req_cap)))
+      return st;
+    if (b->h_stage) cudaFreeHost(b->h_stage);
+    SKV_CUDA(p, cudaMallocHost(&b->h_stage, b->req_cap * 2 * sizeof(int32_t)));
+  }
+  if (!b->d_nitems) {
+    skv_status st;
+    if ((st = dev_alloc(p, &b->d_nitems, 1)) || (st = dev_alloc(p, &b->d_counter, 1))) return st;
+  }
+  if (total) {
+    // stage through pinned memory on the pool stream (wait for the previous upload first)
+    if (b->stage_ev) SKV_CUDA(p, cudaEventSynchronize(b->stage_ev));
+    int32_t* hs = static_cast<int32_t*>(b->h_stage);
+    std::memcpy(hs, b->handles.data(), total * 4);
+    std::memcpy(hs + b->req_cap, b->h_group.data(), total * 4);
+    SKV_CUDA(p, cudaMemcpyAsync(b->d_handles, hs, total * 4, cudaMemcpyHostToDevice, p->stream));
+    SKV_CUDA(p, cudaMemcpyAsync(b->d_group, hs + b->req_cap, total * 4, cudaMemcpyHostToDevice, p->stream));
+    if (!b->stage_ev) SKV_CUDA(p, cudaEventCreateWithFlags(&b->stage_ev, cudaEventDisableTiming));
+    SKV_CUDA(p, cudaEventRecord(b->stage_ev, p->stream));
+  }
+  b->plan_epoch = ~0ull;
+  return SKV_OK;
+}
+
+skv_status skv_batch_create(skv_pool* p, const int32_t* group_models, const int32_t* group_sizes,
+                            int32_t n_groups, const uint64_t* request_ids, skv_batch** out) {
+  *out = nullptr;
+  auto b = new skv_batch();
+  b->pool = p;
+  skv_status st = batch_fill(p, b, group_models, group_sizes, n_groups, request_ids);
+  if (st) {
     skv_batch_destroy(b);
     return st;
   }
-  if (total) {
-    if (cudaMemcpyAsync(b->d_handles, b->handles.data(), total * 4, cudaMemcpyHostToDevice, p->stream) !=
-            cudaSuccess ||
-        cudaMemcpyAsync(b->d_group, grp.data(), total * 4, cudaMemcpyHostToDevice, p->stream) != cudaSuccess ||
-        cudaStreamSynchronize(p->stream) != cudaSuccess) {
-      skv_batch_destroy(b);
-      return fail(p, SKV_ERR_CUDA, "batch upload failed");
-    }
-  }
   *out = b;
   return SKV_OK;
+}
+
+skv_status skv_batch_reset(skv_pool* p, skv_batch* b, const int32_t* group_models, const int32_t* group_sizes,
+                           int32_t n_groups, const uint64_t* request_ids) {
+  if (!b || b->pool != p) return fail(p, SKV_ERR_ARG, "batch belongs to another pool");
+  return batch_fill(p, b, group_models, group_sizes, n_groups, request_ids);
 }
 
 void skv_batch_destroy(skv_batch* b) {
@@ -872,6 +902,8 @@ void skv_batch_destroy(skv_batch* b) {
                   (void*)b->d_counter, (void*)b->d_pbase, (void*)b->d_nsplit, (void*)b->d_ws_o,
                   (void*)b->d_ws_ml})
     if (q) cudaFree(q);
+  if (b->h_stage) cudaFreeHost(b->h_stage);
+  if (b->stage_ev) cudaEventDestroy(b->stage_ev);
   delete b;
 }
 

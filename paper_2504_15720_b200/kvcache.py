@@ -178,6 +178,7 @@ def lib() -> C.CDLL:
         "skv_get_stream": (P, [P]),
         "skv_batch_create": (S, [P, P, P, C.c_int32, P, C.POINTER(P)]),
         "skv_batch_destroy": (V, [P]),
+        "skv_batch_reset": (S, [P, P, P, P, C.c_int32, P]),
         "skv_batch_grow": (S, [P, P, C.c_int64, C.POINTER(C.c_int32)]),
         "skv_batch_decode_bytes": (S, [P, P, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
         "skv_decode_attention": (S, [P, P, C.POINTER(_DecodeArgs), P]),
@@ -437,6 +438,15 @@ class Batch:
         h = C.c_void_p()
         cache._chk(cache._lib.skv_batch_create(cache._h, gm, gs, len(self.groups), idarr, C.byref(h)))
         self._h = h.value
+
+    def reset(self, groups: Sequence[tuple[int, Sequence[int]]]):
+        """Re-point this batch at new requests, reusing its device buffers."""
+        self.groups = [(int(m), [int(i) for i in ids]) for m, ids in groups]
+        gm = (C.c_int32 * len(self.groups))(*[m for m, _ in self.groups])
+        gs = (C.c_int32 * len(self.groups))(*[len(ids) for _, ids in self.groups])
+        flat = [i for _, ids in self.groups for i in ids]
+        idarr = (C.c_uint64 * max(1, len(flat)))(*flat)
+        self.cache._chk(self.cache._lib.skv_batch_reset(self.cache._h, self._h, gm, gs, len(self.groups), idarr))
 
     def close(self):
         if getattr(self, "_h", None) and self.cache._h:

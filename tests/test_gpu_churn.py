@@ -1,0 +1,66 @@
+"""Config-3 churn on the GPU: bursty arrivals, chunked prefill, decode, frees and
+preemptions through the engine loop; the recorded KvOp stream replayed through the
+oracle must give bit-identical block tables and CacheStats."""
+import numpy as np
+import pytest
+
+import oracle_py as O
+import paper_2504_15720_b200 as P
+from paper_2504_15720_b200.churn import ChurnEngine, ServiceProfile, generate_trace
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+def test_generate_trace_is_deterministic_and_skewed():
+    prof = [ServiceProfile(f"s{i}", i % 2, 50, 10, 20, 5) for i in range(4)]
+    a = generate_trace(prof, rate=20.0, duration=5.0, skewness=4, seed=3)
+    b = generate_trace(prof, rate=20.0, duration=5.0, skewness=4, seed=3)
+    assert [(x.t, x.svc, x.in_len, x.out_len) for x in a] == [(x.t, x.svc, x.in_len, x.out_len) for x in b]
+    assert all(a[i].svc == (i // 4) % 4 for i in range(len(a)))  # runs of `skewness` per service
+    c = generate_trace(prof, rate=20.0, duration=5.0, skewness=4, seed=3, step_time=2.5, step_factor=3.0)
+    early = sum(x.t < 2.5 for x in c)
+    assert len(c) - early > early  # bursty: the rate triples after the step
+
+
+def test_churn_engine_block_tables_bit_exact_vs_oracle():
+    shapes = [(2, 4, 16), (3, 8, 8)]  # (layers, kv heads, q heads); GQA 4 and MHA
+    models = [P.ModelSpec(f"m{i}", L, H, 128, 2, Hq) for i, (L, H, Hq) in enumerate(shapes)]
+    pool = 48
+    cache = P.UnifiedKvCache(models, 16, 1, pool, allocate_storage=True, max_blocks_per_request=512)
+    s = torch.cuda.Stream()
+    torch.cuda.set_stream(s)
+    cache.set_stream(s)
+    cache.synth_fill(5, 1.0, s)
+    prof = [ServiceProfile("chat0", 0, 60, 30, 25, 10), ServiceProfile("summ0", 0, 400, 100, 6, 2),
+            ServiceProfile("chat1", 1, 50, 20, 30, 10), ServiceProfile("summ1", 1, 300, 80, 5, 2)]
+    trace = generate_trace(prof, rate=40.0, duration=3.0, skewness=2, seed=11, step_time=1.5, step_factor=2.0)
+    eng = ChurnEngine(cache, shapes, prof, chunk=64, occupancy=0.7, max_decode=64, max_prefill=4, stream=s)
+    dt, t, k = 0.05, 0.0, 0
+    oracle = O.OracleCache([(L, H, 128, 2) for L, H, _ in shapes], pool=pool)
+    n_checked = 0
+    for it in range(80):
+        t += dt
+        new = []
+        while k < len(trace) and trace[k].t <= t:
+            new.append(trace[k])
+            k += 1
+        eng.add_arrivals(new)
+        start = len(eng.ops)
+        eng.step()
+        for kind, rid, m, tok in eng.ops[start:]:  # replay this iteration's ops
+            if kind == 0:
+                oracle.try_allocate(rid, m, tok)
+            else:
+                oracle.free_request(rid)
+        if it % 10 == 9:
+            for rid in eng.running:
+                assert np.array_equal(cache.block_table_np(rid), oracle.block_table_np(rid))
+                n_checked += 1
+            assert cache.stats() == oracle.stats()
+            assert cache.free_blocks() == oracle.free_blocks()
+    summ = eng.summary()
+    assert summ["finished"] > 5 and summ["grow_ops"] > 100 and n_checked > 10
+    assert cache.fragmentation_bytes() == oracle.fragmentation_bytes()
+    for o in eng.o_dec:
+        assert torch.isfinite(o[:4]).all()

@@ -187,3 +187,33 @@ def test_decode_is_repeatable_and_launch_count():
     torch.cuda.synchronize()
     assert all(torch.equal(a, c) for a, c in zip(o1, o2))
     assert cache.kernel_launches() > n0
+
+
+def test_unwritten_tail_slots_with_nan_are_ignored():
+    """A recycled block still holds the previous owner's bytes (here NaN) past the new
+    request's context: masked tail tokens must not leak into the output (0*NaN)."""
+    cache = P.UnifiedKvCache([P.ModelSpec("a", 2, 4, 128, 2, 8)], 16, 1, 8, allocate_storage=True)
+    assert cache.try_allocate(1, 0, 48)
+    b1 = cache.batch([(0, [1])])
+    nan = torch.full((1, 48, 4, 128), float("nan"), device="cuda").half()
+    for layer in range(2):
+        b1.append([nan], [nan], layer, n_new=48)
+    torch.cuda.synchronize()
+    del b1
+    cache.free_request(1)
+    assert cache.try_allocate(2, 0, 37)  # reuses blocks 0..2; tokens 37..47 keep NaN
+    b2 = cache.batch([(0, [2])])
+    g = torch.Generator(device="cuda").manual_seed(0)
+    k = torch.randn((1, 37, 4, 128), generator=g, device="cuda").half()
+    v = torch.randn((1, 37, 4, 128), generator=g, device="cuda").half()
+    b2.append([k], [v], 1, n_new=37)
+    q = torch.randn((1, 8, 128), generator=g, device="cuda").half()
+    out = torch.empty_like(q)
+    b2.decode([q], [out], 1)
+    torch.cuda.synchronize()
+    assert torch.isfinite(out).all()
+    kk, vv = k[0].float(), v[0].float()  # [37, 4, 128]
+    for h in range(8):
+        s = (kk[:, h // 2] @ q[0, h].float()) / np.sqrt(128.0)
+        ref = torch.softmax(s, 0) @ vv[:, h // 2]
+        assert (out[0, h].float() - ref).abs().max().item() <= 2e-3
