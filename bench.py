@@ -459,6 +459,57 @@ def cpu_baseline(cache, batch, q, args, budget_s=None):
                       "oracle/attn_oracle.c)"}
 
 
+def run_churn(args):
+    """Config 3: 8 services (4 shapes x {chat, summarisation}) on one faithful pool, bursty
+    Poisson trace (skewness 4, rate step x2 halfway), chunked prefill C=512, 70 % occupancy."""
+    import torch
+
+    import paper_2504_15720_b200 as P
+    from paper_2504_15720_b200.churn import ChurnEngine, generate_trace, paper_services
+
+    torch.cuda.set_device(0)
+    models = [P.ModelSpec(n, L, H, 128, 2, Hq) for n, L, H, Hq in SERVICES]
+    merged = P.plan_merged_shape(models)
+    pool = int(args.pool_gb * 1e9 // merged)
+    cache = P.UnifiedKvCache(models, 16, 1, pool, allocate_storage=True, max_requests=8192,
+                             max_blocks_per_request=2048)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    cache.set_stream(stream)
+    cache.synth_fill(3, 1.0, stream)
+    shapes = [(L, H, Hq) for _, L, H, Hq in SERVICES]
+    prof = paper_services(len(SERVICES))
+    iters = args.steps * 10 + args.warmup * 10
+    dt = 0.1
+    trace = generate_trace(prof, rate=args.rate, duration=iters * dt, skewness=4, seed=2025,
+                           step_time=iters * dt / 2, step_factor=2.0)
+    eng = ChurnEngine(cache, shapes, prof, chunk=512, occupancy=0.70, max_decode=1024, max_prefill=8,
+                      stream=stream)
+    t, k = 0.0, 0
+    launches0 = cache.kernel_launches()
+    with Clocks(0) as clk:
+        for it in range(iters):
+            t += dt
+            new = []
+            while k < len(trace) and trace[k].t <= t:
+                new.append(trace[k])
+                k += 1
+            eng.add_arrivals(new)
+            eng.step()
+    summ = eng.summary()
+    res = {
+        "metric": "unified-KV paged decode attention HBM GB/s under churn (config 3)",
+        "value": summ["decode_GBps"], "unit": "GB/s", "n_gpus": 1, "steps": iters, "warmup": 0,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp16",
+        "data": "synthetic trace (reference generate_trace semantics) + synthetic K/V",
+        "config": {"workload": f"config3: 8 services (4 shapes x chat/summarisation, PAPER Table 1 lengths), "
+                               f"Poisson rate {args.rate}/s, skewness 4, rate x2 at half time, chunk 512, "
+                               f"occupancy target 0.70, faithful pool {pool} merged blocks ({args.pool_gb} GB)"},
+        "churn": summ, "gpu_launches": int(cache.kernel_launches() - launches0), "clocks": clk.summary(),
+    }
+    print(json.dumps(res), flush=True)
+
+
 def run_reference(args):
     """Reference arm: the reference's own CPU path for this workload on the host cores —
     the reference has no attention, so the fp32 oracle port stands in for decode and the
@@ -470,7 +521,7 @@ def run_reference(args):
     import oracle_py as O
 
     services = SERVICES_C1 if args.workload == "config1" else SERVICES
-    ctx_default = {"config1": 512, "config2": 2048, "config4": 4096}[args.workload]
+    ctx_default = {"config1": 512, "config2": 2048, "config3": 2048, "config4": 4096}[args.workload]
     args.ctx = args.ctx or ctx_default
     cores = os.cpu_count() or 1
     # synthetic host pool for a bounded sample: per service `per` requests at ctx
@@ -526,7 +577,7 @@ def run_reference(args):
     # allocator: the decode-step op stream of the workload's request count (every request
     # +1 token per step, 64 steps), replayed through the reference allocator single-threaded
     # (kv_cache.hpp:45); the array is built before the timer starts
-    n_alloc_req = (args.requests or {"config1": 32, "config2": 256, "config4": 32}[args.workload])
+    n_alloc_req = (args.requests or {"config1": 32, "config2": 256, "config3": 64, "config4": 32}[args.workload])
     nsteps = 64
     acache = (O.RefCache if kind == "reference" else O.OracleCache)(models, pool=400000)
     aops = [(0, 1 + r * len(services) + m, m, args.ctx) for r in range(n_alloc_req) for m in range(len(services))]
@@ -561,7 +612,9 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="config2", choices=["config1", "config2", "config4"])
+    ap.add_argument("--workload", default="config2", choices=["config1", "config2", "config3", "config4"])
+    ap.add_argument("--rate", type=float, default=20.0, help="config3 arrival rate (requests/s)")
+    ap.add_argument("--pool-gb", dest="pool_gb", type=float, default=100.0, help="config3 pool size")
     ap.add_argument("--requests", type=int, default=0, help="decode requests per service (0 = workload default)")
     ap.add_argument("--ctx", type=int, default=0, help="context length (0 = workload default)")
     ap.add_argument("--phys-layers", dest="phys_layers", type=int, default=4)
@@ -571,6 +624,8 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload == "config3":
+        run_churn(args)
     else:
         run_gpu(args)
 
