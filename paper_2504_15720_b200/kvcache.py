@@ -240,12 +240,22 @@ def _ptr(x) -> int:
     return int(x.data_ptr())
 
 
+_CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy: torch's default stream has handle 0, which the C-ABI reads as "pool stream"
+
+
 def _stream_ptr(stream) -> int | None:
+    """Stream handle for the C-ABI.  None -> torch's current stream when torch is in use, so
+    kernels are ordered after the torch ops that produced their inputs (and before those
+    that consume their outputs); the pool's own stream only when torch is not loaded."""
     if stream is None:
-        return None
+        import sys
+        torch = sys.modules.get("torch")
+        if torch is None or not torch.cuda.is_available() or not torch.cuda.is_initialized():
+            return None
+        stream = torch.cuda.current_stream()
     if isinstance(stream, int):
-        return stream
-    return int(stream.cuda_stream)
+        return stream or _CUDA_STREAM_LEGACY
+    return int(stream.cuda_stream) or _CUDA_STREAM_LEGACY
 
 
 class UnifiedKvCache:
