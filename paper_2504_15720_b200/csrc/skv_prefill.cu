@@ -150,36 +150,85 @@ __device__ __forceinline__ uint32_t pack2<__nv_bfloat16>(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-template <typename T>
-__global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_constant__ DataParams p) {
-  extern __shared__ char smem_raw[];
-  char* smem = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  char* sQ = smem;
-  char* sK[2] = {smem + kTileBytes, smem + 2 * kTileBytes};
-  char* sV[2] = {smem + 3 * kTileBytes, smem + 4 * kTileBytes};
-  char* sP = smem + 5 * kTileBytes;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 6 * kTileBytes);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + 6 * kTileBytes + 16);
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]),
+      "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]),
+      "f"(v[17]), "f"(v[18]), "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]),
+      "f"(v[25]), "f"(v[26]), "f"(v[27]), "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31]));
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
 
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// v2: 64-key tiles (112 KiB smem -> two CTAs per SM overlap each other's MMA and
+// softmax phases), O accumulated across tiles by the tensor core in TMEM with a
+// lazy (threshold 2^8) softmax-max correction, single-pass softmax, masking only on
+// tiles that cross the causal diagonal or the chunk end.
+constexpr int kKT = 64;                    // keys per tile
+constexpr int kKVHalf = kKT * 128;         // 8 KiB: one 64-element d-half of a K/V tile
+constexpr int kKVBytes = 2 * kKVHalf;      // 16 KiB per K or V tile
+constexpr int kPBytes = kRows * 128;       // P tile: 128 rows x 64 keys fp16 (one half)
+constexpr int kSmem2 = kTileBytes + 4 * kKVBytes + kPBytes + 64;
+constexpr float kRescale = 8.0f;           // log2 threshold for the lazy correction
+
+__device__ __forceinline__ uint32_t sw_kv(int row, int c) {  // [64 rows x 128 d] tile
+  const int half = c >> 3, cc = c & 7;
+  return half * kKVHalf + (row >> 3) * 1024 + (row & 7) * 128 + ((cc ^ (row & 7)) << 4);
+}
+__device__ __forceinline__ uint32_t sw_p(int row, int c) {  // [128 rows x 64 keys] tile, c in 0..7
+  return (row >> 3) * 1024 + (row & 7) * 128 + ((c ^ (row & 7)) << 4);
+}
+
+__device__ __forceinline__ uint32_t make_idesc_n(int bf16, int b_mn_major, int n) {
+  uint32_t d = 0;
+  d |= 1u << 4;
+  d |= (uint32_t)bf16 << 7;
+  d |= (uint32_t)bf16 << 10;
+  d |= (uint32_t)b_mn_major << 16;
+  d |= (uint32_t)(n >> 3) << 17;
+  d |= (uint32_t)(kRows >> 4) << 24;
+  return d;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads, 2) prefill_kernel(const __grid_constant__ DataParams p) {
+  extern __shared__ __align__(1024) char smem[];
+  char* sQ = smem;
+  char* sK[2] = {smem + kTileBytes, smem + kTileBytes + kKVBytes};
+  char* sV[2] = {smem + kTileBytes + 2 * kKVBytes, smem + kTileBytes + 3 * kKVBytes};
+  char* sP = smem + kTileBytes + 4 * kKVBytes;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sP + kPBytes);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sP + kPBytes + 16);
+
+  if (smem_u32(smem) & 1023) __trap();  // SW128 operand tiles need 1 KiB alignment
   const int r = blockIdx.z, h = blockIdx.y, tile = blockIdx.x;
   const int grp = p.req_group[r];
   const DataGroup& g = p.g[grp];
   const int G = g.G;
   const int q_len = p.n_new;
   if (!g.active || h >= g.Hkv || tile * kRows >= q_len * G) return;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, warp = tid >> 5;
   const int handle = p.handles[r];
   const int ctx = p.req_tokens[handle];
   const int start = ctx - q_len;
   const int tpt = kRows / G;  // tokens per tile
   const int t0 = tile * tpt;
   const int n_keys = min(ctx, start + t0 + tpt);
-  const int n_kt = (n_keys + kKeys - 1) / kKeys;
+  const int n_kt = (n_keys + kKT - 1) / kKT;
   const int2* row_tab = p.req_table + (size_t)handle * p.cap;
   const char* kv_base = p.pool + g.layer_off + (long long)h * g.head_stride;
   const int rl = r - g.req_begin;
+  const bool tail_rows = t0 + tpt > q_len;  // some rows of this tile are past the chunk end
 
-  if (warp == 0) {  // TMEM: S in columns [0,128), O tile in [128,256)
+  if (warp == 0) {  // TMEM: S in columns [0,64), O in [64,192)
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
@@ -191,12 +240,12 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tmem_S = tmem, tmem_O = tmem + 128;
   const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+  const uint32_t tS = tmem + lane_off, tO = tmem + 64 + lane_off;
 
-  // ---- Q tile: row i = (token t0 + i/G, head h*G + i%G); coalesced 16 B per thread --------
-  {
+  {  // Q tile, coalesced: 8 rows x 256 B per instruction across the CTA
     const int c = tid & 15;
+#pragma unroll 4
     for (int i = 0; i < 16; ++i) {
       const int row = (tid >> 4) + 8 * i;
       const int tok = t0 + row / G, gg = row % G;
@@ -208,36 +257,36 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
   }
   auto load_kv = [&](int j, int buf) {
     const int c = tid & 15;
-    for (int i = 0; i < 16; ++i) {
+#pragma unroll 4
+    for (int i = 0; i < 8; ++i) {
       const int key = (tid >> 4) + 8 * i;
-      const int a = j * kKeys + key;
+      const int a = j * kKT + key;
       const bool ok = a < n_keys;
       int2 e = make_int2(0, 0);
       if (ok) e = row_tab[a / kTpb];
       const char* src = kv_base + (long long)e.x * p.merged_stride + (long long)e.y * g.native_stride +
                         (a % kTpb) * (kD * 2) + c * 16;
-      cp_async16(smem_u32(sK[buf]) + sw_off(key, c), src, ok);
-      cp_async16(smem_u32(sV[buf]) + sw_off(key, c), src + kTpb * kD * 2, ok);
+      cp_async16(smem_u32(sK[buf]) + sw_kv(key, c), src, ok);
+      cp_async16(smem_u32(sV[buf]) + sw_kv(key, c), src + kTpb * kD * 2, ok);
     }
   };
   load_kv(0, 0);
   cp_async_commit();
 
-  const uint32_t idesc_qk = make_idesc(p.dtype, 0);
-  const uint32_t idesc_pv = make_idesc(p.dtype, 1);
-  const int row = tid;  // this thread's query row (TMEM lane)
+  const uint32_t idesc_qk = make_idesc_n(p.dtype, 0, kKT);
+  const uint32_t idesc_pv = make_idesc_n(p.dtype, 1, kD);
+  const int row = tid;
   const int my_tok = t0 + row / G;
   const bool row_ok = my_tok < q_len;
-  const int my_pos = start + my_tok;  // absolute position: keys <= my_pos are visible
-  float o[kD];
-#pragma unroll
-  for (int k = 0; k < kD; ++k) o[k] = 0.f;
+  const int my_pos = start + my_tok;
+  const float c2 = p.scale_log2;
   float m = -INFINITY, l = 0.f;
   uint32_t phase = 0;
 
   for (int j = 0; j < n_kt; ++j) {
+    const int buf = j & 1;
     if (j + 1 < n_kt) {
-      load_kv(j + 1, (j + 1) & 1);
+      load_kv(j + 1, buf ^ 1);
       cp_async_commit();
       cp_async_wait<1>();
     } else {
@@ -245,13 +294,13 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
     }
     fence_async_smem();
     __syncthreads();
-    const int buf = j & 1;
     if (tid == 0) {
       tc_fence_after();
 #pragma unroll
       for (int k = 0; k < kD / 16; ++k) {
-        const uint32_t off = (k >> 2) * kHalf + (k & 3) * 32;
-        mma_f16(tmem_S, make_desc(smem_u32(sQ) + off, 16, 1024), make_desc(smem_u32(sK[buf]) + off, 16, 1024),
+        const uint32_t qoff = (k >> 2) * kHalf + (k & 3) * 32;
+        const uint32_t koff = (k >> 2) * kKVHalf + (k & 3) * 32;
+        mma_f16(tmem, make_desc(smem_u32(sQ) + qoff, 16, 1024), make_desc(smem_u32(sK[buf]) + koff, 16, 1024),
                 idesc_qk, k > 0);
       }
       mma_commit(bar);
@@ -260,81 +309,95 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_kernel(const __grid_const
     phase ^= 1;
     tc_fence_after();
 
-    // ---- softmax on this thread's row ---------------------------------------------------
-    float mx = -INFINITY;
-    float s[32];
-#pragma unroll
-    for (int cc = 0; cc < 4; ++cc) {
-      tmem_ld32(tmem_S + lane_off + cc * 32, s);
+    float s[64];
+    {
+      float a0[32], a1[32];
+      tmem_ld32(tS, a0);
+      tmem_ld32(tS + 32, a1);
 #pragma unroll
       for (int k = 0; k < 32; ++k) {
-        const int a = j * kKeys + cc * 32 + k;
-        const float v = (row_ok && a <= my_pos) ? s[k] * p.scale_log2 : -INFINITY;
-        mx = fmaxf(mx, v);
+        s[k] = a0[k];
+        s[32 + k] = a1[k];
       }
     }
-    const float m_new = fmaxf(m, mx);
-    const float alpha = (m_new == -INFINITY) ? 1.f : exp2f(m - m_new);
+    // tiles crossing the causal diagonal / chunk end need per-key masks (CTA-uniform test)
+    const bool masked = (j * kKT + kKT - 1 > start + t0) || tail_rows;
+    if (masked) {
+#pragma unroll
+      for (int k = 0; k < 64; ++k)
+        if (!(row_ok && j * kKT + k <= my_pos)) s[k] = -INFINITY;
+    }
+    float mx = s[0];
+#pragma unroll
+    for (int k = 1; k < 64; ++k) mx = fmaxf(mx, s[k]);
+    const float mt = mx * c2;  // tile max, log2 domain
+    const bool need = mt > m + kRescale;
+    float alpha = 1.f;
+    if (need) {
+      alpha = ex2(m - mt);  // m = -inf -> 0
+      l *= alpha;
+      m = mt;
+    }
+    if (j > 0 && __any_sync(0xffffffffu, need)) {  // correct the TMEM accumulator rows that moved
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        float o[32];
+        tmem_ld32(tO + cc * 32, o);
+#pragma unroll
+        for (int k = 0; k < 32; ++k) o[k] *= alpha;
+        tmem_st32(tO + cc * 32, o);
+      }
+    }
+    const float mu = (m == -INFINITY) ? 0.f : m;
     float lsum = 0.f;
 #pragma unroll
-    for (int cc = 0; cc < 4; ++cc) {
-      tmem_ld32(tmem_S + lane_off + cc * 32, s);
-      uint32_t packed[16];
+    for (int cc = 0; cc < 8; ++cc) {
+      uint32_t pk[4];
 #pragma unroll
-      for (int k = 0; k < 32; k += 2) {
-        const int a = j * kKeys + cc * 32 + k;
-        const float v0 = (row_ok && a <= my_pos) ? exp2f(s[k] * p.scale_log2 - m_new) : 0.f;
-        const float v1 = (row_ok && a + 1 <= my_pos) ? exp2f(s[k + 1] * p.scale_log2 - m_new) : 0.f;
+      for (int k = 0; k < 8; k += 2) {
+        const float v0 = ex2(fmaf(s[cc * 8 + k], c2, -mu));
+        const float v1 = ex2(fmaf(s[cc * 8 + k + 1], c2, -mu));
         lsum += v0 + v1;
-        packed[k >> 1] = pack2<T>(v0, v1);
+        pk[k >> 1] = pack2<T>(v0, v1);
       }
-      // 32 keys = 64 B = chunks 4cc .. 4cc+3 of the P row
-#pragma unroll
-      for (int q4 = 0; q4 < 4; ++q4) {
-        const uint4 val = make_uint4(packed[4 * q4], packed[4 * q4 + 1], packed[4 * q4 + 2], packed[4 * q4 + 3]);
-        *reinterpret_cast<uint4*>(sP + sw_off(row, cc * 4 + q4)) = val;
-      }
+      *reinterpret_cast<uint4*>(sP + sw_p(row, cc)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
     }
-    l = l * alpha + lsum;
-    m = m_new;
+    l += lsum;
     tc_fence_before();
     fence_async_smem();
     __syncthreads();
     if (tid == 0) {
       tc_fence_after();
 #pragma unroll
-      for (int k = 0; k < kKeys / 16; ++k) {
-        const uint32_t aoff = (k >> 2) * kHalf + (k & 3) * 32;
-        mma_f16(tmem_O, make_desc(smem_u32(sP) + aoff, 16, 1024),
-                make_desc(smem_u32(sV[buf]) + k * 2048, kHalf, 1024), idesc_pv, k > 0);
-      }
+      for (int k = 0; k < kKT / 16; ++k)
+        mma_f16(tmem + 64, make_desc(smem_u32(sP) + k * 32, 16, 1024),
+                make_desc(smem_u32(sV[buf]) + k * 2048, kKVHalf, 1024), idesc_pv, (j > 0 || k > 0) ? 1u : 0u);
       mma_commit(bar);
     }
     mbar_wait(bar, phase);
     phase ^= 1;
     tc_fence_after();
-#pragma unroll
-    for (int cc = 0; cc < 4; ++cc) {
-      tmem_ld32(tmem_O + lane_off + cc * 32, s);
-#pragma unroll
-      for (int k = 0; k < 32; ++k) o[cc * 32 + k] = o[cc * 32 + k] * alpha + s[k];
-    }
-    tc_fence_before();
-    __syncthreads();  // S/O TMEM and K/V/P buffers are free for the next tile
   }
 
-  if (row_ok) {
+  {
     const float inv = l > 0.f ? 1.f / l : 0.f;
     char* dst = reinterpret_cast<char*>(g.out) +
-                (((size_t)rl * q_len + my_tok) * g.Hq + h * G + row % G) * (kD * 2);
+                (((size_t)rl * q_len + (row_ok ? my_tok : 0)) * g.Hq + h * G + row % G) * (kD * 2);
 #pragma unroll
-    for (int c = 0; c < 16; ++c) {
-      uint4 v;
-      v.x = pack2<T>(o[8 * c] * inv, o[8 * c + 1] * inv);
-      v.y = pack2<T>(o[8 * c + 2] * inv, o[8 * c + 3] * inv);
-      v.z = pack2<T>(o[8 * c + 4] * inv, o[8 * c + 5] * inv);
-      v.w = pack2<T>(o[8 * c + 6] * inv, o[8 * c + 7] * inv);
-      *reinterpret_cast<uint4*>(dst + c * 16) = v;
+    for (int cc = 0; cc < 4; ++cc) {
+      float o[32];
+      tmem_ld32(tO + cc * 32, o);  // warp-collective: every lane loads, valid rows store
+      if (row_ok) {
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          uint4 v;
+          v.x = pack2<T>(o[8 * q4] * inv, o[8 * q4 + 1] * inv);
+          v.y = pack2<T>(o[8 * q4 + 2] * inv, o[8 * q4 + 3] * inv);
+          v.z = pack2<T>(o[8 * q4 + 4] * inv, o[8 * q4 + 5] * inv);
+          v.w = pack2<T>(o[8 * q4 + 6] * inv, o[8 * q4 + 7] * inv);
+          *reinterpret_cast<uint4*>(dst + cc * 64 + q4 * 16) = v;
+        }
+      }
     }
   }
   tc_fence_before();
@@ -349,7 +412,7 @@ template <typename T>
 void launch_prefill_t(const DataParams& p, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(prefill_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    cudaFuncSetAttribute(prefill_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2);
     attr = true;
   }
   int tiles = 1, heads = 1;
@@ -358,7 +421,7 @@ void launch_prefill_t(const DataParams& p, cudaStream_t s) {
     heads = max(heads, p.g[i].Hkv);
   }
   dim3 grid(tiles, heads, p.nreq);
-  prefill_kernel<T><<<grid, kThreads, kSmem, s>>>(p);
+  prefill_kernel<T><<<grid, kThreads, kSmem2, s>>>(p);
 }
 
 }  // namespace
