@@ -255,23 +255,38 @@ __global__ void __launch_bounds__(kThreads, 2) prefill_kernel(const __grid_const
       cp_async16(smem_u32(sQ) + sw_off(row, c), src, ok);
     }
   }
-  auto load_kv = [&](int j, int buf) {
+  // a 64-key tile spans 4 native blocks; every thread needs the same 4 table entries,
+  // fetched one tile ahead so the cp.async address math never waits on a global load
+  const int n_blk = (n_keys + kTpb - 1) / kTpb;
+  auto fetch_tab = [&](int j, int2 (&e)[4]) {
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int bi = j * 4 + b;
+      e[b] = bi < n_blk ? row_tab[bi] : make_int2(0, 0);
+    }
+  };
+  auto load_kv = [&](int j, int buf, const int2 (&e)[4]) {
     const int c = tid & 15;
-#pragma unroll 4
+#pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int key = (tid >> 4) + 8 * i;
       const int a = j * kKT + key;
       const bool ok = a < n_keys;
-      int2 e = make_int2(0, 0);
-      if (ok) e = row_tab[a / kTpb];
-      const char* src = kv_base + (long long)e.x * p.merged_stride + (long long)e.y * g.native_stride +
+      const int2 eb = e[i >> 1];
+      const char* src = kv_base + (long long)eb.x * p.merged_stride + (long long)eb.y * g.native_stride +
                         (a % kTpb) * (kD * 2) + c * 16;
       cp_async16(smem_u32(sK[buf]) + sw_kv(key, c), src, ok);
       cp_async16(smem_u32(sV[buf]) + sw_kv(key, c), src + kTpb * kD * 2, ok);
     }
   };
-  load_kv(0, 0);
-  cp_async_commit();
+  int2 tab_next[4];
+  {
+    int2 tab0[4];
+    fetch_tab(0, tab0);
+    load_kv(0, 0, tab0);
+    cp_async_commit();
+    fetch_tab(1, tab_next);
+  }
 
   const uint32_t idesc_qk = make_idesc_n(p.dtype, 0, kKT);
   const uint32_t idesc_pv = make_idesc_n(p.dtype, 1, kD);
@@ -286,8 +301,9 @@ __global__ void __launch_bounds__(kThreads, 2) prefill_kernel(const __grid_const
   for (int j = 0; j < n_kt; ++j) {
     const int buf = j & 1;
     if (j + 1 < n_kt) {
-      load_kv(j + 1, buf ^ 1);
+      load_kv(j + 1, buf ^ 1, tab_next);
       cp_async_commit();
+      fetch_tab(j + 2, tab_next);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
@@ -327,10 +343,10 @@ __global__ void __launch_bounds__(kThreads, 2) prefill_kernel(const __grid_const
       for (int k = 0; k < 64; ++k)
         if (!(row_ok && j * kKT + k <= my_pos)) s[k] = -INFINITY;
     }
-    float mx = s[0];
+    float mx4[4] = {s[0], s[1], s[2], s[3]};  // 4 independent chains
 #pragma unroll
-    for (int k = 1; k < 64; ++k) mx = fmaxf(mx, s[k]);
-    const float mt = mx * c2;  // tile max, log2 domain
+    for (int k = 4; k < 64; ++k) mx4[k & 3] = fmaxf(mx4[k & 3], s[k]);
+    const float mt = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * c2;  // tile max, log2 domain
     const bool need = mt > m + kRescale;
     float alpha = 1.f;
     if (need) {
@@ -349,7 +365,7 @@ __global__ void __launch_bounds__(kThreads, 2) prefill_kernel(const __grid_const
       }
     }
     const float mu = (m == -INFINITY) ? 0.f : m;
-    float lsum = 0.f;
+    float ls[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int cc = 0; cc < 8; ++cc) {
       uint32_t pk[4];
@@ -357,12 +373,12 @@ __global__ void __launch_bounds__(kThreads, 2) prefill_kernel(const __grid_const
       for (int k = 0; k < 8; k += 2) {
         const float v0 = ex2(fmaf(s[cc * 8 + k], c2, -mu));
         const float v1 = ex2(fmaf(s[cc * 8 + k + 1], c2, -mu));
-        lsum += v0 + v1;
+        ls[k >> 1] += v0 + v1;
         pk[k >> 1] = pack2<T>(v0, v1);
       }
       *reinterpret_cast<uint4*>(sP + sw_p(row, cc)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
     }
-    l += lsum;
+    l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
     tc_fence_before();
     fence_async_smem();
     __syncthreads();
