@@ -25,6 +25,8 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include <cstdlib>
+
 #include "skv_internal.h"
 
 namespace skv {
@@ -424,11 +426,284 @@ __global__ void __launch_bounds__(kThreads, 2) prefill_kernel(const __grid_const
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// v3: warp-specialised ping-pong (FA4-style).  One CTA = two 128-row query tiles (A, B)
+// sharing every K/V tile; warps 0-3 run the softmax of tile A, warps 4-7 of tile B (both
+// warpgroups address TMEM lanes 0-127 via warp%4, in different columns), warp 8 issues
+// all tcgen05.mma, warps 9-10 stream Q and a 3-stage K/V ring with cp.async signalled
+// through mbarriers.  Tensor-core order: QK_A QK_B | PV_A QK_A' | PV_B QK_B' | ... so the
+// tensor core works on one tile while the other tile's softmax runs on the CUDA cores.
+constexpr int kStagesV3 = 3;
+constexpr int kThreadsV3 = 11 * 32;
+constexpr int kLoadThreads = 64;
+constexpr int kSmemV3 = 2 * kTileBytes + kStagesV3 * 2 * kKVBytes + 2 * kPBytes + 256;
+
+__device__ __forceinline__ void mbar_init_n(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(n));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive(uint64_t* b) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v3(const __grid_constant__ DataParams p) {
+  extern __shared__ __align__(1024) char smem[];
+  if (smem_u32(smem) & 1023) __trap();
+  char* sQ[2] = {smem, smem + kTileBytes};
+  char* kvbase = smem + 2 * kTileBytes;
+  char* sP[2] = {kvbase + kStagesV3 * 2 * kKVBytes, kvbase + kStagesV3 * 2 * kKVBytes + kPBytes};
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP[1] + kPBytes);
+  uint64_t* kv_full = bars;                 // [3] count 64 (cp.async arrive.noinc per loader thread)
+  uint64_t* kv_empty = bars + 3;            // [3] count 1 (tcgen05.commit after PV_B)
+  uint64_t* q_full = bars + 6;              // count 64
+  uint64_t* s_full = bars + 7;              // [2] count 1
+  uint64_t* p_full = bars + 9;              // [2] count 128
+  uint64_t* pv_done = bars + 11;            // [2] count 1
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+
+  const int r = blockIdx.z, h = blockIdx.y;
+  const int grp = p.req_group[r];
+  const DataGroup& g = p.g[grp];
+  const int G = g.G;
+  const int q_len = p.n_new;
+  const int tileA = 2 * blockIdx.x;
+  if (!g.active || h >= g.Hkv || tileA * kRows >= q_len * G) return;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int handle = p.handles[r];
+  const int ctx = p.req_tokens[handle];
+  const int start = ctx - q_len;
+  const int tpt = kRows / G;
+  const int t0A = tileA * tpt;
+  const int n_keys = min(ctx, start + t0A + 2 * tpt);  // the last row of tile B
+  const int n_kt = (n_keys + kKT - 1) / kKT;
+  const int rl = r - g.req_begin;
+
+  if (warp == 8) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < 3; ++i) {
+      mbar_init_n(&kv_full[i], kLoadThreads);
+      mbar_init_n(&kv_empty[i], 1);
+    }
+    mbar_init_n(q_full, kLoadThreads);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init_n(&s_full[i], 1);
+      mbar_init_n(&p_full[i], 128);
+      mbar_init_n(&pv_done[i], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp >= 9) {  // ------------------------------------------------------- loaders
+    const int lt = tid - 9 * 32;  // 0..63
+    const int c = lt & 15;
+    // Q tiles A and B: 256 rows x 16 chunks
+    for (int i = 0; i < 64; ++i) {
+      const int idx = (lt >> 4) + 4 * i;  // 0..255
+      const int x = idx >> 7, row = idx & 127;
+      const int tok = t0A + x * tpt + row / G, gg = row % G;
+      const bool ok = tok < q_len;
+      const char* src = reinterpret_cast<const char*>(g.q) +
+                        (((size_t)rl * q_len + (ok ? tok : 0)) * g.Hq + h * G + gg) * (kD * 2) + c * 16;
+      cp_async16(smem_u32(sQ[x]) + sw_off(row, c), src, ok);
+    }
+    cp_async_arrive(q_full);
+    const int2* row_tab = p.req_table + (size_t)handle * p.cap;
+    const char* kv_src = p.pool + g.layer_off + (long long)h * g.head_stride;
+    const int n_blk = (n_keys + kTpb - 1) / kTpb;
+    for (int j = 0; j < n_kt; ++j) {
+      const int st = j % kStagesV3;
+      if (j >= kStagesV3) mbar_wait(&kv_empty[st], ((j / kStagesV3) - 1) & 1);
+      int2 e[4];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) e[b] = (j * 4 + b < n_blk) ? row_tab[j * 4 + b] : make_int2(0, 0);
+      char* sK = kvbase + st * 2 * kKVBytes;
+      char* sV = sK + kKVBytes;
+#pragma unroll 4
+      for (int i = 0; i < 16; ++i) {
+        const int key = (lt >> 4) + 4 * i;  // 0..63
+        const int a = j * kKT + key;
+        const bool ok = a < n_keys;
+        const int2 eb = e[key >> 4];
+        const char* src = kv_src + (long long)eb.x * p.merged_stride + (long long)eb.y * g.native_stride +
+                          (a % kTpb) * (kD * 2) + c * 16;
+        cp_async16(smem_u32(sK) + sw_kv(key, c), src, ok);
+        cp_async16(smem_u32(sV) + sw_kv(key, c), src + kTpb * kD * 2, ok);
+      }
+      cp_async_arrive(&kv_full[st]);
+    }
+    cp_async_wait<0>();
+  } else if (warp == 8) {  // --------------------------------------------------- MMA issue
+    if (lane == 0) {
+      const uint32_t idesc_qk = make_idesc_n(p.dtype, 0, kKT);
+      const uint32_t idesc_pv = make_idesc_n(p.dtype, 1, kD);
+      auto qk = [&](int x, int j) {
+        const int st = j % kStagesV3;
+        const uint32_t sK = smem_u32(kvbase + st * 2 * kKVBytes);
+#pragma unroll
+        for (int k = 0; k < kD / 16; ++k) {
+          const uint32_t qoff = (k >> 2) * kHalf + (k & 3) * 32;
+          const uint32_t koff = (k >> 2) * kKVHalf + (k & 3) * 32;
+          mma_f16(tmem + x * 64, make_desc(smem_u32(sQ[x]) + qoff, 16, 1024), make_desc(sK + koff, 16, 1024),
+                  idesc_qk, k > 0);
+        }
+        mma_commit(&s_full[x]);
+      };
+      auto pv = [&](int x, int j) {
+        const int st = j % kStagesV3;
+        const uint32_t sV = smem_u32(kvbase + st * 2 * kKVBytes + kKVBytes);
+#pragma unroll
+        for (int k = 0; k < kKT / 16; ++k)
+          mma_f16(tmem + 128 + x * 128, make_desc(smem_u32(sP[x]) + k * 32, 16, 1024),
+                  make_desc(sV + k * 2048, kKVHalf, 1024), idesc_pv, (j > 0 || k > 0) ? 1u : 0u);
+        mma_commit(&pv_done[x]);
+      };
+      mbar_wait(q_full, 0);
+      mbar_wait(&kv_full[0], 0);
+      fence_async_smem();  // cp.async (generic proxy) data -> tensor-core (async proxy) reads
+      tc_fence_after();
+      qk(0, 0);
+      qk(1, 0);
+      for (int j = 0; j < n_kt; ++j) {
+        mbar_wait(&p_full[0], j & 1);
+        tc_fence_after();
+        pv(0, j);
+        if (j + 1 < n_kt) {
+          mbar_wait(&kv_full[(j + 1) % kStagesV3], ((j + 1) / kStagesV3) & 1);
+          fence_async_smem();
+          tc_fence_after();
+          qk(0, j + 1);
+        }
+        mbar_wait(&p_full[1], j & 1);
+        tc_fence_after();
+        pv(1, j);
+        mma_commit(&kv_empty[j % kStagesV3]);
+        if (j + 1 < n_kt) qk(1, j + 1);
+      }
+    }
+    __syncwarp();
+  } else {  // ------------------------------------------------------------- softmax WGs
+    const int x = warp >> 2;  // 0 = tile A, 1 = tile B
+    const int row = tid & 127;
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const uint32_t tS = tmem + x * 64 + lane_off, tO = tmem + 128 + x * 128 + lane_off;
+    const int t0 = t0A + x * tpt;
+    const int my_tok = t0 + row / G;
+    const bool row_ok = my_tok < q_len;
+    const int my_pos = start + my_tok;
+    const bool tail_rows = t0 + tpt > q_len;
+    const float c2 = p.scale_log2;
+    float m = -INFINITY, l = 0.f;
+    char* sPx = sP[x];
+    for (int j = 0; j < n_kt; ++j) {
+      mbar_wait(&s_full[x], j & 1);
+      tc_fence_after();
+      float s[64];
+      {
+        float a0[32], a1[32];
+        tmem_ld32(tS, a0);
+        tmem_ld32(tS + 32, a1);
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          s[k] = a0[k];
+          s[32 + k] = a1[k];
+        }
+      }
+      const bool masked = (j * kKT + kKT - 1 > start + t0) || tail_rows;
+      if (masked) {
+#pragma unroll
+        for (int k = 0; k < 64; ++k)
+          if (!(row_ok && j * kKT + k <= my_pos)) s[k] = -INFINITY;
+      }
+      float mx4[4] = {s[0], s[1], s[2], s[3]};
+#pragma unroll
+      for (int k = 4; k < 64; ++k) mx4[k & 3] = fmaxf(mx4[k & 3], s[k]);
+      const float mt = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * c2;
+      const bool need = mt > m + kRescale;
+      float alpha = 1.f;
+      if (need) {
+        alpha = ex2(m - mt);
+        l *= alpha;
+        m = mt;
+      }
+      if (j > 0) {
+        mbar_wait(&pv_done[x], (j - 1) & 1);  // PV(j-1) finished: O stable, P buffer free
+        tc_fence_after();
+        if (__any_sync(0xffffffffu, need)) {
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) {
+            float o[32];
+            tmem_ld32(tO + cc * 32, o);
+#pragma unroll
+            for (int k = 0; k < 32; ++k) o[k] *= alpha;
+            tmem_st32(tO + cc * 32, o);
+          }
+        }
+      }
+      const float mu = (m == -INFINITY) ? 0.f : m;
+      float ls[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc) {
+        uint32_t pk[4];
+#pragma unroll
+        for (int k = 0; k < 8; k += 2) {
+          const float v0 = ex2(fmaf(s[cc * 8 + k], c2, -mu));
+          const float v1 = ex2(fmaf(s[cc * 8 + k + 1], c2, -mu));
+          ls[k >> 1] += v0 + v1;
+          pk[k >> 1] = pack2<T>(v0, v1);
+        }
+        *reinterpret_cast<uint4*>(sPx + sw_p(row, cc)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      }
+      l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+      fence_async_smem();
+      tc_fence_before();
+      mbar_arrive(&p_full[x]);
+    }
+    mbar_wait(&pv_done[x], (n_kt - 1) & 1);
+    tc_fence_after();
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    char* dst = reinterpret_cast<char*>(g.out) +
+                (((size_t)rl * q_len + (row_ok ? my_tok : 0)) * g.Hq + h * G + row % G) * (kD * 2);
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) {
+      float o[32];
+      tmem_ld32(tO + cc * 32, o);
+      if (row_ok) {
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          uint4 v;
+          v.x = pack2<T>(o[8 * q4] * inv, o[8 * q4 + 1] * inv);
+          v.y = pack2<T>(o[8 * q4 + 2] * inv, o[8 * q4 + 3] * inv);
+          v.z = pack2<T>(o[8 * q4 + 4] * inv, o[8 * q4 + 5] * inv);
+          v.w = pack2<T>(o[8 * q4 + 6] * inv, o[8 * q4 + 7] * inv);
+          *reinterpret_cast<uint4*>(dst + cc * 64 + q4 * 16) = v;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 8) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
 template <typename T>
 void launch_prefill_t(const DataParams& p, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(prefill_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2);
+    cudaFuncSetAttribute(prefill_kernel_v3<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemV3);
     attr = true;
   }
   int tiles = 1, heads = 1;
@@ -436,8 +711,17 @@ void launch_prefill_t(const DataParams& p, cudaStream_t s) {
     tiles = max(tiles, (p.n_new * p.g[i].G + kRows - 1) / kRows);
     heads = max(heads, p.g[i].Hkv);
   }
-  dim3 grid(tiles, heads, p.nreq);
-  prefill_kernel<T><<<grid, kThreads, kSmem2, s>>>(p);
+  static const int version = [] {
+    const char* e = getenv("SEAKV_PREFILL_V");
+    return e ? atoi(e) : 3;
+  }();
+  if (version == 2) {
+    dim3 grid(tiles, heads, p.nreq);
+    prefill_kernel<T><<<grid, kThreads, kSmem2, s>>>(p);
+  } else {
+    dim3 grid((tiles + 1) / 2, heads, p.nreq);
+    prefill_kernel_v3<T><<<grid, kThreadsV3, kSmemV3, s>>>(p);
+  }
 }
 
 }  // namespace
