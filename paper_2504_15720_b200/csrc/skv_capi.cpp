@@ -12,6 +12,8 @@
 //    attention kernels read, and executes frees.  After a free run the host only
 //    needs the number of merged blocks each model emptied (E_m), read back once
 //    before the next admission decision.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -112,6 +114,8 @@ struct skv_pool {
 
   void* storage = nullptr;
   size_t storage_bytes = 0;
+  alignas(64) CUtensorMap kv_tmap;
+  bool has_tmap = false;
   uint64_t launches = 0;
   std::string err;
 };
@@ -440,6 +444,30 @@ skv_status free_impl(skv_pool* p, uint64_t id) {  // kv_cache.hpp:126-134
   return SKV_OK;
 }
 
+// TMA descriptor for the pool: 2-D [rows of 256 B][128 x 16-bit], box {64, 16}, SW128.
+bool encode_pool_tmap(skv_pool* p) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
+  if (!encode) return false;
+  for (const ModelInfo& mi : p->models)
+    if (mi.d != 128 || mi.e != 2 || p->tpb != 16) return false;
+  const cuuint64_t rows = p->storage_bytes / 256;
+  if (rows == 0 || rows > 0x7fffffffull) return false;  // TMA coordinates are signed 32-bit
+  const cuuint64_t dims[2] = {128, rows};
+  const cuuint64_t strides[1] = {256};
+  const cuuint32_t box[2] = {64, 16};
+  const cuuint32_t estr[2] = {1, 1};
+  return encode(&p->kv_tmap, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, p->storage, dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 skv_status ensure_storage(skv_pool* p) {
   if (p->storage) return SKV_OK;
   DeviceGuard g(p->device);
@@ -447,6 +475,7 @@ skv_status ensure_storage(skv_pool* p) {
   if (bytes == 0) return fail(p, SKV_ERR_ARG, "empty pool");
   SKV_CUDA(p, cudaMalloc(&p->storage, bytes));
   p->storage_bytes = bytes;
+  p->has_tmap = encode_pool_tmap(p);
   return SKV_OK;
 }
 
@@ -954,7 +983,7 @@ skv_status skv_batch_decode_bytes(skv_pool* p, skv_batch* b, int32_t layer, doub
 
 // Common DataParams for one batch / layer.
 static skv_status make_params(skv_pool* p, skv_batch* b, int layer, skv::DataParams* dp) {
-  std::memset(dp, 0, sizeof(*dp));
+  std::memset(static_cast<void*>(dp), 0, sizeof(*dp));
   dp->ngroups = b->ngroups;
   dp->nreq = b->nreq;
   dp->handles = b->d_handles;
@@ -963,6 +992,8 @@ static skv_status make_params(skv_pool* p, skv_batch* b, int layer, skv::DataPar
   dp->req_table = p->dev.req_table;
   dp->cap = p->cap;
   dp->pool = static_cast<char*>(p->storage);
+  dp->has_tmap = p->has_tmap ? 1 : 0;
+  if (p->has_tmap) dp->kv_tmap = p->kv_tmap;
   dp->merged_stride = p->merged_stride;
   dp->tpb = p->tpb;
   dp->dtype = p->dtype;

@@ -1,6 +1,7 @@
 // skv_internal.h — structures shared by the host runtime (skv_capi.cpp) and the
 // sm_100a kernels (skv_alloc.cu, skv_attn.cu).  Not part of the public ABI.
 #pragma once
+#include <cuda.h>  // CUtensorMap (header only; the driver entry point is resolved at run time)
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -81,6 +82,11 @@ struct DataGroup {
 };
 
 struct DataParams {
+  // TMA descriptor of the whole pool viewed as a 2-D fp16 tensor [pool_bytes/256 rows][128]
+  // (one row = one token's head_dim run), box {64, 16}, 128B swizzle: one box = one
+  // 64-element half of a native block's K or V tile, landing in UMMA operand layout.
+  alignas(64) CUtensorMap kv_tmap;
+  int has_tmap;
   DataGroup g[kMaxGroups];
   int ngroups;
   int nreq;                  // batch size

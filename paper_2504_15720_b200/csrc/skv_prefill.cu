@@ -434,15 +434,28 @@ __global__ void __launch_bounds__(kThreads, 2) prefill_kernel(const __grid_const
 // through mbarriers.  Tensor-core order: QK_A QK_B | PV_A QK_A' | PV_B QK_B' | ... so the
 // tensor core works on one tile while the other tile's softmax runs on the CUDA cores.
 constexpr int kStagesV3 = 3;
-constexpr int kThreadsV3 = 11 * 32;
-constexpr int kLoadThreads = 64;
-constexpr int kSmemV3 = 2 * kTileBytes + kStagesV3 * 2 * kKVBytes + 2 * kPBytes + 256;
+constexpr int kSoftmaxWarps = 16;            // 8 per query tile; warps w and w+4 share TMEM lanes
+constexpr int kMmaWarp = kSoftmaxWarps;      // warp 16
+constexpr int kLoadWarp = kSoftmaxWarps + 1; // warp 17
+constexpr int kThreadsV3 = (kSoftmaxWarps + 2) * 32;
+constexpr int kLoadThreads = 32;
+constexpr int kSmemV3 = 2 * kTileBytes + kStagesV3 * 2 * kKVBytes + 2 * kPBytes + 256 + 2 * 2 * 128 * 4;
 
 __device__ __forceinline__ void mbar_init_n(uint64_t* b, uint32_t n) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(n));
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* tmap, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx_v3(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void cp_async_arrive(uint64_t* b) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(b)) : "memory");
@@ -456,13 +469,14 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v3(const __grid_
   char* kvbase = smem + 2 * kTileBytes;
   char* sP[2] = {kvbase + kStagesV3 * 2 * kKVBytes, kvbase + kStagesV3 * 2 * kKVBytes + kPBytes};
   uint64_t* bars = reinterpret_cast<uint64_t*>(sP[1] + kPBytes);
-  uint64_t* kv_full = bars;                 // [3] count 64 (cp.async arrive.noinc per loader thread)
+  uint64_t* kv_full = bars;                 // [3] count 32 (cp.async arrive.noinc per loader thread)
   uint64_t* kv_empty = bars + 3;            // [3] count 1 (tcgen05.commit after PV_B)
-  uint64_t* q_full = bars + 6;              // count 64
+  uint64_t* q_full = bars + 6;              // count 32
   uint64_t* s_full = bars + 7;              // [2] count 1
-  uint64_t* p_full = bars + 9;              // [2] count 128
+  uint64_t* p_full = bars + 9;              // [2] count 256
   uint64_t* pv_done = bars + 11;            // [2] count 1
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+  float* xmax = reinterpret_cast<float*>(bars + 32);  // [2 tiles][2 column halves][128 rows]
 
   const int r = blockIdx.z, h = blockIdx.y;
   const int grp = p.req_group[r];
@@ -481,19 +495,19 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v3(const __grid_
   const int n_kt = (n_keys + kKT - 1) / kKT;
   const int rl = r - g.req_begin;
 
-  if (warp == 8) {
+  if (warp == kMmaWarp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
     for (int i = 0; i < 3; ++i) {
-      mbar_init_n(&kv_full[i], kLoadThreads);
+      mbar_init_n(&kv_full[i], 1);  // the TMA thread's arrive.expect_tx
       mbar_init_n(&kv_empty[i], 1);
     }
     mbar_init_n(q_full, kLoadThreads);
     for (int i = 0; i < 2; ++i) {
       mbar_init_n(&s_full[i], 1);
-      mbar_init_n(&p_full[i], 128);
+      mbar_init_n(&p_full[i], 256);
       mbar_init_n(&pv_done[i], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -503,12 +517,12 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v3(const __grid_
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp >= 9) {  // ------------------------------------------------------- loaders
-    const int lt = tid - 9 * 32;  // 0..63
+  if (warp == kLoadWarp) {  // ----------------------------------------------- loader
+    const int lt = lane;  // 0..31
     const int c = lt & 15;
     // Q tiles A and B: 256 rows x 16 chunks
-    for (int i = 0; i < 64; ++i) {
-      const int idx = (lt >> 4) + 4 * i;  // 0..255
+    for (int i = 0; i < 128; ++i) {
+      const int idx = (lt >> 4) + 2 * i;  // 0..255
       const int x = idx >> 7, row = idx & 127;
       const int tok = t0A + x * tpt + row / G, gg = row % G;
       const bool ok = tok < q_len;
@@ -517,32 +531,38 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v3(const __grid_
       cp_async16(smem_u32(sQ[x]) + sw_off(row, c), src, ok);
     }
     cp_async_arrive(q_full);
-    const int2* row_tab = p.req_table + (size_t)handle * p.cap;
-    const char* kv_src = p.pool + g.layer_off + (long long)h * g.head_stride;
-    const int n_blk = (n_keys + kTpb - 1) / kTpb;
-    for (int j = 0; j < n_kt; ++j) {
-      const int st = j % kStagesV3;
-      if (j >= kStagesV3) mbar_wait(&kv_empty[st], ((j / kStagesV3) - 1) & 1);
-      int2 e[4];
+    if (lane == 0) {  // one thread streams K/V: 16 TMA boxes (2 KiB each) per 64-key tile
+      const int2* row_tab = p.req_table + (size_t)handle * p.cap;
+      const long long base_off = g.layer_off + (long long)h * g.head_stride;
+      const int n_blk = (n_keys + kTpb - 1) / kTpb;
+      for (int j = 0; j < n_kt; ++j) {
+        const int st = j % kStagesV3;
+        if (j >= kStagesV3) mbar_wait(&kv_empty[st], ((j / kStagesV3) - 1) & 1);
+        int2 e[4];
+        int nb = 0;
 #pragma unroll
-      for (int b = 0; b < 4; ++b) e[b] = (j * 4 + b < n_blk) ? row_tab[j * 4 + b] : make_int2(0, 0);
-      char* sK = kvbase + st * 2 * kKVBytes;
-      char* sV = sK + kKVBytes;
-#pragma unroll 4
-      for (int i = 0; i < 16; ++i) {
-        const int key = (lt >> 4) + 4 * i;  // 0..63
-        const int a = j * kKT + key;
-        const bool ok = a < n_keys;
-        const int2 eb = e[key >> 4];
-        const char* src = kv_src + (long long)eb.x * p.merged_stride + (long long)eb.y * g.native_stride +
-                          (a % kTpb) * (kD * 2) + c * 16;
-        cp_async16(smem_u32(sK) + sw_kv(key, c), src, ok);
-        cp_async16(smem_u32(sV) + sw_kv(key, c), src + kTpb * kD * 2, ok);
+        for (int b = 0; b < 4; ++b) {
+          const int bi = j * 4 + b;
+          e[b] = bi < n_blk ? row_tab[bi] : make_int2(-1, 0);
+          nb += bi < n_blk;
+        }
+        mbar_expect_tx_v3(&kv_full[st], nb * 4 * 2048);
+        const uint32_t sK = smem_u32(kvbase + st * 2 * kKVBytes), sV = sK + kKVBytes;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          if (e[b].x < 0) continue;
+          const int row0 = (int)(((long long)e[b].x * p.merged_stride + (long long)e[b].y * g.native_stride +
+                                  base_off) >> 8);
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            tma_load_2d(sK + hh * kKVHalf + b * 2048, &p.kv_tmap, hh * 64, row0, &kv_full[st]);
+            tma_load_2d(sV + hh * kKVHalf + b * 2048, &p.kv_tmap, hh * 64, row0 + kTpb, &kv_full[st]);
+          }
+        }
       }
-      cp_async_arrive(&kv_full[st]);
     }
     cp_async_wait<0>();
-  } else if (warp == 8) {  // --------------------------------------------------- MMA issue
+  } else if (warp == kMmaWarp) {  // -------------------------------------------- MMA issue
     if (lane == 0) {
       const uint32_t idesc_qk = make_idesc_n(p.dtype, 0, kKT);
       const uint32_t idesc_pv = make_idesc_n(p.dtype, 1, kD);
@@ -591,11 +611,18 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v3(const __grid_
       }
     }
     __syncwarp();
-  } else {  // ------------------------------------------------------------- softmax WGs
-    const int x = warp >> 2;  // 0 = tile A, 1 = tile B
-    const int row = tid & 127;
-    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-    const uint32_t tS = tmem + x * 64 + lane_off, tO = tmem + 128 + x * 128 + lane_off;
+  } else {  // ------------------------------------------------------------- softmax warps
+    // warp w in [0,16): tile x = w/8; lanes (w%4)*32..+31 (its rows); column half hc = (w/4)%2
+    // of the 64 keys (and of the 128 O columns).  Warps w and w+4 cover the same rows and meet
+    // at named barrier 1 + w%8 to combine row maxima.
+    const int x = warp >> 3, hc = (warp >> 2) & 1, wq = warp & 3;
+    const int row = wq * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
+    const uint32_t tS = tmem + x * 64 + hc * 32 + lane_off;
+    const uint32_t tO = tmem + 128 + x * 128 + hc * 64 + lane_off;
+    const int bar_id = 1 + x * 4 + wq;
+    float* my_max = xmax + (x * 2 + hc) * 128;
+    float* other_max = xmax + (x * 2 + (hc ^ 1)) * 128;
     const int t0 = t0A + x * tpt;
     const int my_tok = t0 + row / G;
     const bool row_ok = my_tok < q_len;
@@ -607,27 +634,31 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v3(const __grid_
     for (int j = 0; j < n_kt; ++j) {
       mbar_wait(&s_full[x], j & 1);
       tc_fence_after();
-      float s[64];
-      {
-        float a0[32], a1[32];
-        tmem_ld32(tS, a0);
-        tmem_ld32(tS + 32, a1);
-#pragma unroll
-        for (int k = 0; k < 32; ++k) {
-          s[k] = a0[k];
-          s[32 + k] = a1[k];
-        }
+      if (x == 0 && hc == 0 && j == n_kt - 1 && (j + 1) * kKT > ctx) {
+        // last tile: rows of loaded blocks past ctx are not K/V of this request
+        char* sV = kvbase + (j % kStagesV3) * 2 * kKVBytes + kKVBytes;
+        const int c = row & 15;
+        for (int key = row >> 4; key < kKT; key += 8)
+          if (j * kKT + key >= ctx) *reinterpret_cast<uint4*>(sV + sw_kv(key, c)) = make_uint4(0, 0, 0, 0);
       }
+      float s[32];
+      tmem_ld32(tS, s);
+      const int kbase = j * kKT + hc * 32;
       const bool masked = (j * kKT + kKT - 1 > start + t0) || tail_rows;
       if (masked) {
 #pragma unroll
-        for (int k = 0; k < 64; ++k)
-          if (!(row_ok && j * kKT + k <= my_pos)) s[k] = -INFINITY;
+        for (int k = 0; k < 32; ++k)
+          if (!(row_ok && kbase + k <= my_pos)) s[k] = -INFINITY;
       }
       float mx4[4] = {s[0], s[1], s[2], s[3]};
 #pragma unroll
-      for (int k = 4; k < 64; ++k) mx4[k & 3] = fmaxf(mx4[k & 3], s[k]);
-      const float mt = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * c2;
+      for (int k = 4; k < 32; ++k) mx4[k & 3] = fmaxf(mx4[k & 3], s[k]);
+      float mh = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+      my_max[row] = mh;
+      asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+      mh = fmaxf(mh, other_max[row]);
+      asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");  // both read before the next write
+      const float mt = mh * c2;
       const bool need = mt > m + kRescale;
       float alpha = 1.f;
       if (need) {
@@ -640,7 +671,7 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v3(const __grid_
         tc_fence_after();
         if (__any_sync(0xffffffffu, need)) {
 #pragma unroll
-          for (int cc = 0; cc < 4; ++cc) {
+          for (int cc = 0; cc < 2; ++cc) {
             float o[32];
             tmem_ld32(tO + cc * 32, o);
 #pragma unroll
@@ -652,7 +683,7 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v3(const __grid_
       const float mu = (m == -INFINITY) ? 0.f : m;
       float ls[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int cc = 0; cc < 8; ++cc) {
+      for (int cc = 0; cc < 4; ++cc) {
         uint32_t pk[4];
 #pragma unroll
         for (int k = 0; k < 8; k += 2) {
@@ -661,20 +692,24 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v3(const __grid_
           ls[k >> 1] += v0 + v1;
           pk[k >> 1] = pack2<T>(v0, v1);
         }
-        *reinterpret_cast<uint4*>(sPx + sw_p(row, cc)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        *reinterpret_cast<uint4*>(sPx + sw_p(row, hc * 4 + cc)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
       }
       l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
       fence_async_smem();
       tc_fence_before();
       mbar_arrive(&p_full[x]);
     }
+    // row sum = both column halves' partial sums
+    my_max[row] = l;
+    asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+    const float ltot = l + other_max[row];
     mbar_wait(&pv_done[x], (n_kt - 1) & 1);
     tc_fence_after();
-    const float inv = l > 0.f ? 1.f / l : 0.f;
+    const float inv = ltot > 0.f ? 1.f / ltot : 0.f;
     char* dst = reinterpret_cast<char*>(g.out) +
-                (((size_t)rl * q_len + (row_ok ? my_tok : 0)) * g.Hq + h * G + row % G) * (kD * 2);
+                (((size_t)rl * q_len + (row_ok ? my_tok : 0)) * g.Hq + h * G + row % G) * (kD * 2) + hc * 128;
 #pragma unroll
-    for (int cc = 0; cc < 4; ++cc) {
+    for (int cc = 0; cc < 2; ++cc) {
       float o[32];
       tmem_ld32(tO + cc * 32, o);
       if (row_ok) {
@@ -692,7 +727,7 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v3(const __grid_
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 8) {
+  if (warp == kMmaWarp) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
   }
@@ -715,7 +750,7 @@ void launch_prefill_t(const DataParams& p, cudaStream_t s) {
     const char* e = getenv("SEAKV_PREFILL_V");
     return e ? atoi(e) : 3;
   }();
-  if (version == 2) {
+  if (version == 2 || !p.has_tmap) {
     dim3 grid(tiles, heads, p.nreq);
     prefill_kernel<T><<<grid, kThreads, kSmem2, s>>>(p);
   } else {
