@@ -433,13 +433,13 @@ __global__ void __launch_bounds__(kThreads, 2) prefill_kernel(const __grid_const
 // all tcgen05.mma, warps 9-10 stream Q and a 3-stage K/V ring with cp.async signalled
 // through mbarriers.  Tensor-core order: QK_A QK_B | PV_A QK_A' | PV_B QK_B' | ... so the
 // tensor core works on one tile while the other tile's softmax runs on the CUDA cores.
-constexpr int kStagesV3 = 3;
-constexpr int kSoftmaxWarps = 16;            // 8 per query tile; warps w and w+4 share TMEM lanes
+constexpr int kStagesV3 = 4;
+constexpr int kSoftmaxWarps = 8;             // 4 per query tile, one thread per query row
 constexpr int kMmaWarp = kSoftmaxWarps;      // warp 16
 constexpr int kLoadWarp = kSoftmaxWarps + 1; // warp 17
 constexpr int kThreadsV3 = (kSoftmaxWarps + 2) * 32;
 constexpr int kLoadThreads = 32;
-constexpr int kSmemV3 = 2 * kTileBytes + kStagesV3 * 2 * kKVBytes + 2 * kPBytes + 256 + 2 * 2 * 128 * 4;
+constexpr int kSmemV3 = 2 * kTileBytes + kStagesV3 * 2 * kKVBytes + 2 * kPBytes + 256;
 
 __device__ __forceinline__ void mbar_init_n(uint64_t* b, uint32_t n) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(n));
@@ -469,14 +469,13 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v3(const __grid_
   char* kvbase = smem + 2 * kTileBytes;
   char* sP[2] = {kvbase + kStagesV3 * 2 * kKVBytes, kvbase + kStagesV3 * 2 * kKVBytes + kPBytes};
   uint64_t* bars = reinterpret_cast<uint64_t*>(sP[1] + kPBytes);
-  uint64_t* kv_full = bars;                 // [3] count 32 (cp.async arrive.noinc per loader thread)
-  uint64_t* kv_empty = bars + 3;            // [3] count 1 (tcgen05.commit after PV_B)
-  uint64_t* q_full = bars + 6;              // count 32
-  uint64_t* s_full = bars + 7;              // [2] count 1
-  uint64_t* p_full = bars + 9;              // [2] count 256
-  uint64_t* pv_done = bars + 11;            // [2] count 1
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
-  float* xmax = reinterpret_cast<float*>(bars + 32);  // [2 tiles][2 column halves][128 rows]
+  uint64_t* kv_full = bars;                 // [stages] count 1 (TMA arrive.expect_tx)
+  uint64_t* kv_empty = bars + 4;            // [stages] count 1 (tcgen05.commit after PV_B)
+  uint64_t* q_full = bars + 8;              // count 32 (cp.async arrive.noinc per loader lane)
+  uint64_t* s_full = bars + 9;              // [tile][S buffer] count 1
+  uint64_t* p_full = bars + 13;             // [2] count 128
+  uint64_t* pv_done = bars + 15;            // [2] count 1
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
 
   const int r = blockIdx.z, h = blockIdx.y;
   const int grp = p.req_group[r];
@@ -500,14 +499,14 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v3(const __grid_
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < kStagesV3; ++i) {
       mbar_init_n(&kv_full[i], 1);  // the TMA thread's arrive.expect_tx
       mbar_init_n(&kv_empty[i], 1);
     }
     mbar_init_n(q_full, kLoadThreads);
+    for (int i = 0; i < 4; ++i) mbar_init_n(&s_full[i], 1);
     for (int i = 0; i < 2; ++i) {
-      mbar_init_n(&s_full[i], 1);
-      mbar_init_n(&p_full[i], 256);
+      mbar_init_n(&p_full[i], 128);
       mbar_init_n(&pv_done[i], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -566,63 +565,64 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v3(const __grid_
     if (lane == 0) {
       const uint32_t idesc_qk = make_idesc_n(p.dtype, 0, kKT);
       const uint32_t idesc_pv = make_idesc_n(p.dtype, 1, kD);
-      auto qk = [&](int x, int j) {
+      auto qk = [&](int x, int j) {  // S[x][j&1] = Q_x . K_j^T
         const int st = j % kStagesV3;
         const uint32_t sK = smem_u32(kvbase + st * 2 * kKVBytes);
 #pragma unroll
         for (int k = 0; k < kD / 16; ++k) {
           const uint32_t qoff = (k >> 2) * kHalf + (k & 3) * 32;
           const uint32_t koff = (k >> 2) * kKVHalf + (k & 3) * 32;
-          mma_f16(tmem + x * 64, make_desc(smem_u32(sQ[x]) + qoff, 16, 1024), make_desc(sK + koff, 16, 1024),
-                  idesc_qk, k > 0);
+          mma_f16(tmem + x * 128 + (j & 1) * 64, make_desc(smem_u32(sQ[x]) + qoff, 16, 1024),
+                  make_desc(sK + koff, 16, 1024), idesc_qk, k > 0);
         }
-        mma_commit(&s_full[x]);
+        mma_commit(&s_full[x * 2 + (j & 1)]);
       };
-      auto pv = [&](int x, int j) {
+      auto pv = [&](int x, int j) {  // O[x] += P_x . V_j
         const int st = j % kStagesV3;
         const uint32_t sV = smem_u32(kvbase + st * 2 * kKVBytes + kKVBytes);
 #pragma unroll
         for (int k = 0; k < kKT / 16; ++k)
-          mma_f16(tmem + 128 + x * 128, make_desc(smem_u32(sP[x]) + k * 32, 16, 1024),
+          mma_f16(tmem + 256 + x * 128, make_desc(smem_u32(sP[x]) + k * 32, 16, 1024),
                   make_desc(sV + k * 2048, kKVHalf, 1024), idesc_pv, (j > 0 || k > 0) ? 1u : 0u);
         mma_commit(&pv_done[x]);
       };
+      auto wait_kv = [&](int j) {
+        mbar_wait(&kv_full[j % kStagesV3], (j / kStagesV3) & 1);
+        fence_async_smem();  // cp.async / TMA data -> tensor-core reads
+        tc_fence_after();
+      };
+      // QK runs two tiles ahead of PV (S double-buffered in TMEM), so the softmax of
+      // tile j+1 never waits for PV(j): order QK_A0 QK_B0 QK_A1 QK_B1 | PV_A0 QK_A2 PV_B0 QK_B2 | ...
       mbar_wait(q_full, 0);
-      mbar_wait(&kv_full[0], 0);
-      fence_async_smem();  // cp.async (generic proxy) data -> tensor-core (async proxy) reads
-      tc_fence_after();
+      wait_kv(0);
       qk(0, 0);
       qk(1, 0);
+      if (n_kt > 1) {
+        wait_kv(1);
+        qk(0, 1);
+        qk(1, 1);
+      }
       for (int j = 0; j < n_kt; ++j) {
         mbar_wait(&p_full[0], j & 1);
         tc_fence_after();
         pv(0, j);
-        if (j + 1 < n_kt) {
-          mbar_wait(&kv_full[(j + 1) % kStagesV3], ((j + 1) / kStagesV3) & 1);
-          fence_async_smem();
-          tc_fence_after();
-          qk(0, j + 1);
+        if (j + 2 < n_kt) {
+          wait_kv(j + 2);
+          qk(0, j + 2);
         }
         mbar_wait(&p_full[1], j & 1);
         tc_fence_after();
         pv(1, j);
         mma_commit(&kv_empty[j % kStagesV3]);
-        if (j + 1 < n_kt) qk(1, j + 1);
+        if (j + 2 < n_kt) qk(1, j + 2);
       }
     }
     __syncwarp();
   } else {  // ------------------------------------------------------------- softmax warps
-    // warp w in [0,16): tile x = w/8; lanes (w%4)*32..+31 (its rows); column half hc = (w/4)%2
-    // of the 64 keys (and of the 128 O columns).  Warps w and w+4 cover the same rows and meet
-    // at named barrier 1 + w%8 to combine row maxima.
-    const int x = warp >> 3, hc = (warp >> 2) & 1, wq = warp & 3;
-    const int row = wq * 32 + lane;
-    const uint32_t lane_off = (uint32_t)(wq * 32) << 16;
-    const uint32_t tS = tmem + x * 64 + hc * 32 + lane_off;
-    const uint32_t tO = tmem + 128 + x * 128 + hc * 64 + lane_off;
-    const int bar_id = 1 + x * 4 + wq;
-    float* my_max = xmax + (x * 2 + hc) * 128;
-    float* other_max = xmax + (x * 2 + (hc ^ 1)) * 128;
+    const int x = warp >> 2;  // 0 = tile A, 1 = tile B; both warpgroups address TMEM lanes 0-127
+    const int row = tid & 127;
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const uint32_t tS0 = tmem + x * 128 + lane_off, tO = tmem + 256 + x * 128 + lane_off;
     const int t0 = t0A + x * tpt;
     const int my_tok = t0 + row / G;
     const bool row_ok = my_tok < q_len;
@@ -632,33 +632,37 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v3(const __grid_
     float m = -INFINITY, l = 0.f;
     char* sPx = sP[x];
     for (int j = 0; j < n_kt; ++j) {
-      mbar_wait(&s_full[x], j & 1);
+      mbar_wait(&s_full[x * 2 + (j & 1)], (j >> 1) & 1);
       tc_fence_after();
-      if (x == 0 && hc == 0 && j == n_kt - 1 && (j + 1) * kKT > ctx) {
-        // last tile: rows of loaded blocks past ctx are not K/V of this request
+      const uint32_t tS = tS0 + (j & 1) * 64;
+      if (x == 0 && j == n_kt - 1 && (j + 1) * kKT > ctx) {
+        // last tile: rows of TMA-loaded blocks past ctx are not this request's K/V (may be NaN)
         char* sV = kvbase + (j % kStagesV3) * 2 * kKVBytes + kKVBytes;
         const int c = row & 15;
         for (int key = row >> 4; key < kKT; key += 8)
           if (j * kKT + key >= ctx) *reinterpret_cast<uint4*>(sV + sw_kv(key, c)) = make_uint4(0, 0, 0, 0);
       }
-      float s[32];
-      tmem_ld32(tS, s);
-      const int kbase = j * kKT + hc * 32;
+      float s[64];
+      {
+        float a0[32], a1[32];
+        tmem_ld32(tS, a0);
+        tmem_ld32(tS + 32, a1);
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          s[k] = a0[k];
+          s[32 + k] = a1[k];
+        }
+      }
       const bool masked = (j * kKT + kKT - 1 > start + t0) || tail_rows;
       if (masked) {
 #pragma unroll
-        for (int k = 0; k < 32; ++k)
-          if (!(row_ok && kbase + k <= my_pos)) s[k] = -INFINITY;
+        for (int k = 0; k < 64; ++k)
+          if (!(row_ok && j * kKT + k <= my_pos)) s[k] = -INFINITY;
       }
       float mx4[4] = {s[0], s[1], s[2], s[3]};
 #pragma unroll
-      for (int k = 4; k < 32; ++k) mx4[k & 3] = fmaxf(mx4[k & 3], s[k]);
-      float mh = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
-      my_max[row] = mh;
-      asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
-      mh = fmaxf(mh, other_max[row]);
-      asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");  // both read before the next write
-      const float mt = mh * c2;
+      for (int k = 4; k < 64; ++k) mx4[k & 3] = fmaxf(mx4[k & 3], s[k]);
+      const float mt = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * c2;
       const bool need = mt > m + kRescale;
       float alpha = 1.f;
       if (need) {
@@ -671,7 +675,7 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v3(const __grid_
         tc_fence_after();
         if (__any_sync(0xffffffffu, need)) {
 #pragma unroll
-          for (int cc = 0; cc < 2; ++cc) {
+          for (int cc = 0; cc < 4; ++cc) {
             float o[32];
             tmem_ld32(tO + cc * 32, o);
 #pragma unroll
@@ -683,7 +687,7 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v3(const __grid_
       const float mu = (m == -INFINITY) ? 0.f : m;
       float ls[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int cc = 0; cc < 4; ++cc) {
+      for (int cc = 0; cc < 8; ++cc) {
         uint32_t pk[4];
 #pragma unroll
         for (int k = 0; k < 8; k += 2) {
@@ -692,24 +696,20 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v3(const __grid_
           ls[k >> 1] += v0 + v1;
           pk[k >> 1] = pack2<T>(v0, v1);
         }
-        *reinterpret_cast<uint4*>(sPx + sw_p(row, hc * 4 + cc)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        *reinterpret_cast<uint4*>(sPx + sw_p(row, cc)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
       }
       l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
       fence_async_smem();
       tc_fence_before();
       mbar_arrive(&p_full[x]);
     }
-    // row sum = both column halves' partial sums
-    my_max[row] = l;
-    asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
-    const float ltot = l + other_max[row];
     mbar_wait(&pv_done[x], (n_kt - 1) & 1);
     tc_fence_after();
-    const float inv = ltot > 0.f ? 1.f / ltot : 0.f;
+    const float inv = l > 0.f ? 1.f / l : 0.f;
     char* dst = reinterpret_cast<char*>(g.out) +
-                (((size_t)rl * q_len + (row_ok ? my_tok : 0)) * g.Hq + h * G + row % G) * (kD * 2) + hc * 128;
+                (((size_t)rl * q_len + (row_ok ? my_tok : 0)) * g.Hq + h * G + row % G) * (kD * 2);
 #pragma unroll
-    for (int cc = 0; cc < 2; ++cc) {
+    for (int cc = 0; cc < 4; ++cc) {
       float o[32];
       tmem_ld32(tO + cc * 32, o);
       if (row_ok) {
