@@ -218,6 +218,24 @@ def step_bytes(batch, nlayers):
     return kv, tot
 
 
+def profiled_traffic(wl, args):
+    """dram__bytes_read.sum + dram__bytes_write.sum per decode launch from the committed ncu
+    capture of this same workload (profiles/r01_decode_traffic_config2.csv: single-pass
+    metrics, so ncu did not save/restore the 122 GB pool), or None."""
+    path = os.path.join(ROOT, "profiles", "r01_decode_traffic_config2.csv")
+    if wl.name != "config2" or (args.requests or 256) != 256 or (args.ctx or 2048) != 2048 or not os.path.exists(path):
+        return None, None
+    import csv
+    rows = list(csv.reader(open(path)))
+    hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
+    h = rows[hi]
+    tot = {}
+    for r in rows[hi + 1:]:
+        if len(r) > 5 and r[h.index("Metric Name")].startswith("dram__bytes_"):
+            tot[r[0]] = tot.get(r[0], 0.0) + float(r[h.index("Metric Value")].replace(",", ""))
+    return (sum(tot.values()) / len(tot) if tot else None), os.path.relpath(path, ROOT)
+
+
 def run_gpu(args):
     import torch
 
@@ -282,6 +300,8 @@ def run_gpu(args):
     tokens_s = sum_over_ranks(float(sum(len(c) for c in wl.ctxs) * args.steps)) / (elapsed_ms / 1e3)
     hbm, peak_kind = peaks()
     achieved = dec_bytes / (dec_ms / 1e3) / 1e9  # algorithmic bytes / decode launch time
+    traffic, traffic_src = profiled_traffic(wl, args)
+    layer0_bytes = batch.decode_bytes(0)[1]
     n_launch = args.steps * NLAYERS
 
     # ---- allocator: decode-step growth of the whole batch (host mirror + GPU placement) ---
@@ -382,7 +402,9 @@ def run_gpu(args):
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e2e_ms / args.steps, 3)},
         "roofline": {"bound": "hbm", "kernel": "skv decode_kernel (+plan/combine)",
                      "achieved": round(achieved, 1), "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": round(achieved / hbm, 4), "traffic": None,
+                     "frac": round(achieved / hbm, 4), "traffic": traffic, "traffic_source": traffic_src,
+                     "traffic_note": "4-service layer launch (layers 0-31); algorithmic bytes of that launch "
+                                     f"~{layer0_bytes:.4g}",
                      "avg_launch_ms": round(dec_ms / n_launch, 4),
                      "bytes_per_launch": round(dec_bytes / n_launch, 1)},
         "allocator": {"ns_per_grow_op": round(alloc_ns, 2),
