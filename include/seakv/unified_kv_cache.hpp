@@ -17,9 +17,16 @@
 //                                      that mutates the cache, as in the reference)
 //   compare_schemes      :352-369      GPU merged scheme + host SplitCacheCounter
 //
-// Differences, all documented in DESIGN.md §5: request id 0 is rejected with
-// ValidationError (the reference's empty-slot sentinel, quirk Q2); the object is
-// move-only (it owns device memory).
+// Request ids cross the C-ABI as id+1, so id 0 — which the reference uses as its
+// empty-slot sentinel and which its simulator hands out (simulation.hpp:169-172) —
+// is a normal request here (the reference's Q2 aliasing for id 0 is not reproduced;
+// UINT64_MAX is the one id that cannot be represented).  The object is move-only (it
+// owns device memory), as the simulator's Engine already requires (simulation.hpp:219).
+//
+// Define SEAKV_USE_REFERENCE_TYPES before including this header to take ModelSpec,
+// kGiB, the exception types and detail::Rng from the reference's own common.hpp /
+// cost_model.hpp (e.g. when building the reference simulator against the GPU cache,
+// tests/shim_sim/seasim/kv_cache.hpp).
 #pragma once
 
 #include <cstdint>
@@ -27,6 +34,7 @@
 #include <map>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 #include <unordered_map>
 #include <utility>
 #include <vector>
@@ -35,8 +43,7 @@
 
 namespace seasim {
 
-#ifndef SEAKV_SEASIM_ERRORS_DEFINED
-#define SEAKV_SEASIM_ERRORS_DEFINED
+#ifndef SEAKV_USE_REFERENCE_TYPES
 struct ConfigError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
@@ -49,7 +56,6 @@ struct ValidationError : std::runtime_error {
 struct InfeasibleError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
-#endif
 
 inline constexpr double kGiB = 1073741824.0;
 
@@ -66,6 +72,7 @@ struct ModelSpec {
 
   double kv_bytes_per_token() const { return 2.0 * num_layers * num_heads * head_dim * dtype_bytes; }
 };
+#endif  // SEAKV_USE_REFERENCE_TYPES
 
 struct CacheStats {
   std::uint64_t block_table_entries = 0;
@@ -76,16 +83,28 @@ struct CacheStats {
 
 namespace seakv_detail {
 
+template <typename M, typename = void>
+struct q_heads_of {
+  static int get(const M&) { return 0; }  // reference ModelSpec: no GQA field -> MHA
+};
+template <typename M>
+struct q_heads_of<M, std::void_t<decltype(std::declval<const M&>().num_q_heads)>> {
+  static int get(const M& m) { return m.num_q_heads; }
+};
+
 inline skv_model_desc to_desc(const ModelSpec& m) {
   skv_model_desc d;
   d.model_id = m.model_id.c_str();
   d.num_layers = m.num_layers;
   d.num_heads = m.num_heads;
-  d.num_q_heads = m.num_q_heads;
+  d.num_q_heads = q_heads_of<ModelSpec>::get(m);
   d.head_dim = m.head_dim;
   d.dtype_bytes = m.dtype_bytes;
   return d;
 }
+
+// ids cross the ABI shifted by one (0 is the ABI's reserved sentinel)
+inline std::uint64_t abi_id(std::uint64_t id) { return id + 1; }
 
 [[noreturn]] inline void raise(skv_status st, const char* msg) {
   const std::string what = msg ? msg : "seakv error";
@@ -171,33 +190,33 @@ class UnifiedKvCache {
   std::size_t allocated_blocks() const { return skv_allocated_blocks(pool_); }
   int tokens_per_block() const { return skv_tokens_per_block(pool_); }
   std::size_t native_blocks_for(long tokens) const { return skv_native_blocks_for(pool_, tokens); }
-  bool registered(std::uint64_t request_id) const { return skv_registered(pool_, request_id) != 0; }
+  bool registered(std::uint64_t request_id) const { return skv_registered(pool_, seakv_detail::abi_id(request_id)) != 0; }
   std::size_t available_slots(int model_idx) const { return skv_available_slots(pool_, model_idx); }
 
   bool can_grow_to(std::uint64_t request_id, int model_idx, long tokens_needed) const {
     int32_t out = 0;
-    seakv_detail::check(skv_can_grow_to(pool_, request_id, model_idx, tokens_needed, &out), pool_);
+    seakv_detail::check(skv_can_grow_to(pool_, seakv_detail::abi_id(request_id), model_idx, tokens_needed, &out), pool_);
     return out != 0;
   }
 
   bool try_allocate(std::uint64_t request_id, int model_idx, long tokens_needed) {
-    return seakv_detail::check(skv_try_allocate(pool_, request_id, model_idx, tokens_needed), pool_) == SKV_OK;
+    return seakv_detail::check(skv_try_allocate(pool_, seakv_detail::abi_id(request_id), model_idx, tokens_needed), pool_) == SKV_OK;
   }
 
   void free_request(std::uint64_t request_id) {
-    seakv_detail::check(skv_free_request(pool_, request_id), pool_);
+    seakv_detail::check(skv_free_request(pool_, seakv_detail::abi_id(request_id)), pool_);
     tables_.erase(request_id);
   }
 
   void record_context_read(std::uint64_t request_id) {
-    seakv_detail::check(skv_record_context_read(pool_, request_id), pool_);
+    seakv_detail::check(skv_record_context_read(pool_, seakv_detail::abi_id(request_id)), pool_);
   }
 
   const std::vector<std::pair<int, int>>& block_table(std::uint64_t request_id) const {
     size_t n = 0;
-    seakv_detail::check(skv_block_table(pool_, request_id, nullptr, 0, &n), pool_);
+    seakv_detail::check(skv_block_table(pool_, seakv_detail::abi_id(request_id), nullptr, 0, &n), pool_);
     std::vector<int32_t> raw(2 * n);
-    if (n) seakv_detail::check(skv_block_table(pool_, request_id, raw.data(), n, &n), pool_);
+    if (n) seakv_detail::check(skv_block_table(pool_, seakv_detail::abi_id(request_id), raw.data(), n, &n), pool_);
     auto& t = tables_[request_id];
     t.resize(n);
     for (size_t i = 0; i < n; ++i) t[i] = {raw[2 * i], raw[2 * i + 1]};
@@ -207,7 +226,7 @@ class UnifiedKvCache {
   std::uint64_t owner_of(int block, int slot) const {
     uint64_t o = 0;
     seakv_detail::check(skv_owner_of(pool_, block, slot, &o), pool_);
-    return o;
+    return o ? o - 1 : 0;  // 0 = empty, as the reference reports it
   }
 
   std::size_t table_entries() const { return skv_table_entries(pool_); }
@@ -323,6 +342,7 @@ inline std::pair<CacheStats, CacheStats> compare_schemes(const std::vector<Model
   return {merged.stats(), split.stats()};
 }
 
+#ifndef SEAKV_USE_REFERENCE_TYPES
 namespace detail {
 
 // Counter-based SplitMix64 stream with the reference's draw functions
@@ -347,5 +367,6 @@ class Rng {
 };
 
 }  // namespace detail
+#endif  // SEAKV_USE_REFERENCE_TYPES
 
 }  // namespace seasim

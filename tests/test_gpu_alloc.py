@@ -253,3 +253,24 @@ def test_reference_kv_cache_test_against_gpu_dropin():
     fails = re.findall(r"FAILURE (\S+): (.*)", out)
     assert len(fails) == 1 and fails[0][0].endswith("kv_cache_test.cpp:180"), fails
     assert "lhs=34839396352 " in fails[0][1]
+
+
+# --- the reference SIMULATOR driving the GPU cache ----------------------
+SIM_REF = __import__("os").path.join(__import__("os").path.dirname(O.REF_TEST_BIN), "sim_ref")
+SIM_DROPIN = __import__("os").path.join(__import__("os").path.dirname(O.REF_TEST_BIN), "sim_dropin")
+
+
+@pytest.mark.skipif(not (__import__("os").path.exists(SIM_REF) and __import__("os").path.exists(SIM_DROPIN)),
+                    reason="simulator binaries not built")
+@pytest.mark.parametrize("args", [("6", "30", "2.0"), ("12", "20", "1.0")])
+def test_reference_simulator_identical_with_gpu_cache(args):
+    """simulation.hpp (event loop, EngineGate::acquire -> can_grow_to/try_allocate, evictions,
+    free_request) built once with the reference kv_cache.hpp and once with the GPU drop-in:
+    CacheStats of every engine, serving metrics and every request's outcome must match."""
+    import subprocess
+
+    a = subprocess.run([SIM_REF, *args], capture_output=True, text=True, timeout=300)
+    b = subprocess.run([SIM_DROPIN, *args], capture_output=True, text=True, timeout=600)
+    assert a.returncode == 0 and b.returncode == 0, b.stderr
+    assert a.stdout == b.stdout
+    assert "engine 1 kv entries" in b.stdout
