@@ -306,3 +306,60 @@ class ChurnEngine:
             "decode_ms": round(st["decode_ms"], 2), "prefill_ms": round(st["prefill_ms"], 2),
             "append_ms": round(st["append_ms"], 2),
         }
+
+
+# ------------------------------------------------------------------ persisted formats --
+TRACE_HEADER = "arrival_time,service_id,input_len,output_len"  # workload.hpp:214
+OPS_HEADER = "kind,request_id,model_idx,tokens"                 # KvOp, kv_cache.hpp:270-275
+
+
+def save_trace(arrivals: Sequence[Arrival], profiles: Sequence[ServiceProfile], path: str) -> None:
+    """The reference's trace CSV (save_trace, workload.hpp:216-225)."""
+    with open(path, "w") as f:
+        f.write(TRACE_HEADER + "\n")
+        for a in arrivals:
+            f.write(f"{a.t:.6f},{profiles[a.svc].name},{a.in_len},{a.out_len}\n")
+
+
+def load_trace(path: str, profiles: Sequence[ServiceProfile]) -> List[Arrival]:
+    """load_trace (workload.hpp:227-265): header check, 4 fields, lengths >= 1, monotone time."""
+    by_name = {p.name: i for i, p in enumerate(profiles)}
+    out: List[Arrival] = []
+    with open(path) as f:
+        lines = f.read().splitlines()
+    if not lines or lines[0].rstrip("\r") != TRACE_HEADER:
+        raise ValueError(f"{path}:1: bad header, expected '{TRACE_HEADER}'")
+    prev = -1.0
+    for n, line in enumerate(lines[1:], start=2):
+        line = line.rstrip("\r")
+        if not line:
+            continue
+        parts = line.split(",")
+        if len(parts) != 4:
+            raise ValueError(f"{path}:{n}: expected 4 comma-separated fields")
+        t, svc, il, ol = float(parts[0]), parts[1], int(parts[2]), int(parts[3])
+        if il < 1 or ol < 1:
+            raise ValueError(f"{path}:{n}: lengths must be >= 1")
+        if t < prev:
+            raise ValueError(f"{path}:{n}: non-monotone arrival_time")
+        if svc not in by_name:
+            raise ValueError(f"{path}:{n}: unknown service '{svc}'")
+        prev = t
+        out.append(Arrival(t, by_name[svc], il, ol))
+    return out
+
+
+def save_ops(ops: Sequence[tuple], path: str) -> None:
+    """KvOp stream as CSV: kind (0 grow, 1 free), request id, model index, tokens."""
+    with open(path, "w") as f:
+        f.write(OPS_HEADER + "\n")
+        for kind, rid, m, tok in ops:
+            f.write(f"{kind},{rid},{m},{tok}\n")
+
+
+def load_ops(path: str) -> List[tuple]:
+    with open(path) as f:
+        lines = f.read().splitlines()
+    if not lines or lines[0] != OPS_HEADER:
+        raise ValueError(f"{path}:1: bad header, expected '{OPS_HEADER}'")
+    return [tuple(int(x) for x in line.split(",")) for line in lines[1:] if line]
