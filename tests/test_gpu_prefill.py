@@ -85,3 +85,12 @@ def test_prefill_single_token_equals_decode():
     b.decode([q.view(2, 16, 128)], [o2], 1)
     torch.cuda.synchronize()
     assert (o1.view(2, 16, 128).float() - o2.float()).abs().max().item() <= 2e-3
+
+
+def test_prefill_gqa8_llama70b_ratio():
+    """G=8 (Llama-2/3-70B real GQA): 16 tokens x 8 heads per 128-row tile."""
+    run_prefill_check([(2, 2, 16)], [[333, 64]], q_len=48, layer=1)
+
+
+def test_prefill_long_prefix_many_tiles():
+    run_prefill_check([(2, 2, 2)], [[4100]], q_len=300, layer=0)
