@@ -25,6 +25,7 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include <cstdio>
 #include <cstdlib>
 
 #include "skv_internal.h"
@@ -109,9 +110,21 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
+// Build with `make SKV_EXTRA=-DSKV_WATCHDOG` to turn a protocol hang into a trap that names
+// the barrier and phase every stuck warp waits on.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   uint32_t ok = 0;
+#ifdef SKV_WATCHDOG
+  long long spins = 0;
+#endif
   while (!ok) {
+#ifdef SKV_WATCHDOG
+    ++spins;
+    if (spins == (1ll << 22) && (threadIdx.x & 31) == 0)
+      printf("SKV_WATCHDOG block (%d,%d,%d) warp %d bar_off %u parity %u\n", blockIdx.x, blockIdx.y, blockIdx.z,
+             threadIdx.x >> 5, smem_u32(bar) & 0xffff, phase);
+    if (spins == (1ll << 25)) __trap();
+#endif
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
