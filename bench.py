@@ -11,8 +11,8 @@ layer l % 4.  Every per-layer launch reads exactly the config's bytes (23.6 GB p
 layer index, far larger than the 126 MB L2, so no L2 flush is needed).
 
 One step = one decode iteration of all 1024 requests over all 40 layer indices:
-  GPU allocator grow (+1 token each) -> per layer: KV append of the new token +
-  paged decode attention (one launch covering all services).
+  GPU allocator grow (+1 token each) -> per layer ONE launch covering all services that
+  appends the new token's K/V and runs paged decode attention.
 value = decode K/V bytes of the step / device time of the step (GB/s), max over ranks.
 e2e   = the same through the C-ABI with host (pinned) buffers: H2D of q/k/v and D2H of
         the attention output inside the timed region.
@@ -197,23 +197,19 @@ def setup(P, torch, args, device):
     return wl, cache, batch, q, out, k, v, stream
 
 
-def step_device(batch, q, out, k, v, stream, nlayers, ev=None):
-    """One decode step; optional per-layer decode events for the kernel roofline."""
+def step_device(batch, q, out, k, v, stream, nlayers):
+    """One decode step: allocator grow (+1 token per request), then per layer one fused
+    launch that appends the new K/V token and runs paged decode attention."""
     batch.grow(1)
     for layer in range(nlayers):
-        batch.append(k, v, layer, 1, stream)
-        if ev is not None:
-            ev[layer][0].record(stream)
-        batch.decode(q, out, layer, stream=stream)
-        if ev is not None:
-            ev[layer][1].record(stream)
+        batch.decode(q, out, layer, stream=stream, k=k, v=v)
 
 
 def capture_step_graph(torch, cache, batch, q, out, k, v, stream, nlayers):
-    """CUDA graph of one step's device work after the host-side grow: per layer KV append +
-    decode (the decode plan kernel on layer 0, a work-counter reset on the others).  The
-    allocator grow of each step (host admission + GPU placement kernel) stays outside
-    and is flushed before every replay.  Returns None if capture is not possible."""
+    """CUDA graph of one step's device work after the host-side grow: the decode plan
+    kernel, then per layer the fused append + decode launch.  The allocator grow of each
+    step (host admission + GPU placement kernel) stays outside and is flushed before
+    every replay.  Returns None if capture is not possible."""
     try:
         batch.grow(1)
         cache.flush(stream)
@@ -221,8 +217,7 @@ def capture_step_graph(torch, cache, batch, q, out, k, v, stream, nlayers):
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=stream):
             for layer in range(nlayers):
-                batch.append(k, v, layer, 1, stream)
-                batch.decode(q, out, layer, stream=stream)
+                batch.decode(q, out, layer, stream=stream, k=k, v=v)
         g.replay()  # the captured step's attention
         torch.cuda.synchronize()
         return g
@@ -299,10 +294,7 @@ def run_gpu(args):
         step_device(batch, q, out, k, v, stream, NLAYERS)
     barrier()
     graph = None if args.no_graph else capture_step_graph(torch, cache, batch, q, out, k, v, stream, NLAYERS)
-    evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(NLAYERS)]
-           for _ in range(args.steps)]
     kv_total = all_total = 0.0
-    dec_bytes = 0.0
     launches0 = cache.kernel_launches()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
@@ -314,7 +306,7 @@ def run_gpu(args):
                 cache.flush(stream)
                 graph.replay()
             else:
-                step_device(batch, q, out, k, v, stream, NLAYERS, evs[st])
+                step_device(batch, q, out, k, v, stream, NLAYERS)
             kvb, totb = step_bytes(batch, NLAYERS)  # host mirror: exact context of this step
             kv_total += kvb
             all_total += totb
@@ -323,16 +315,26 @@ def run_gpu(args):
     launches_timed = cache.kernel_launches() - launches0
     graph_launches = 0
     if graph is not None:  # the graph's kernels bypass the pool's launch counter
-        graph_launches = args.steps * (2 * NLAYERS + 1)
-        # per-launch decode timing for the roofline: eager steps right after the timed region
-        for st in range(min(args.steps, 2)):
-            step_device(batch, q, out, k, v, stream, NLAYERS, evs[st])
-            dec_bytes += step_bytes(batch, NLAYERS)[1]
-        torch.cuda.synchronize()
-        evs = evs[:min(args.steps, 2)]
-    else:
-        dec_bytes = all_total
-    dec_ms = sum(e[0].elapsed_time(e[1]) for ev in evs for e in ev)
+        graph_launches = args.steps * (NLAYERS + 1)
+    # per-launch decode timing for the roofline: a CUDA graph of the step's NLAYERS fused
+    # append+decode launches (same contexts, no grow; re-appending the same token is
+    # idempotent) replayed back to back on the launching stream, bracketed by events
+    dgraph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(dgraph, stream=stream):
+        for layer in range(NLAYERS):
+            batch.decode(q, out, layer, stream=stream, k=k, v=v)
+    dgraph.replay()
+    torch.cuda.synchronize()
+    d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    nrep = 3
+    d0.record(stream)
+    for _ in range(nrep):
+        dgraph.replay()
+    d1.record(stream)
+    torch.cuda.synchronize()
+    dec_ms = d0.elapsed_time(d1)
+    dec_bytes = step_bytes(batch, NLAYERS)[1] * nrep
+    n_launch = nrep * NLAYERS
     launches = launches_timed + graph_launches
     elapsed_ms = max_over_ranks(t0.elapsed_time(t1))
     kv_all = sum_over_ranks(kv_total)
@@ -342,7 +344,6 @@ def run_gpu(args):
     achieved = dec_bytes / (dec_ms / 1e3) / 1e9  # algorithmic bytes / decode launch time
     traffic, traffic_src = profiled_traffic(wl, args)
     layer0_bytes = batch.decode_bytes(0)[1]
-    n_launch = len(evs) * NLAYERS
 
     # ---- allocator: decode-step growth of the whole batch (host mirror + GPU placement) ---
     torch.cuda.synchronize()
@@ -355,50 +356,56 @@ def run_gpu(args):
     alloc_ns = (time.perf_counter() - a0) / (na * sum(len(c) for c in wl.ctxs)) * 1e9
 
     # ---- e2e through the C-ABI with host buffers -----------------------------------------
-    hq = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in q]
-    ho = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in out]
-    hk = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in k]
-    hv = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in v]
-    for a, b in zip(hq + hk + hv, q + k + v):
-        a.copy_(b)
-    h2d = sum(x.numel() * 2 for x in hq + hk + hv) * NLAYERS
-    d2h = sum(x.numel() * 2 for x in ho) * NLAYERS
+    # Every step copies its inputs (q, k, v of every layer: [NLAYERS, B, H, d] per group)
+    # from pinned host memory and reads every layer's attention output back.  Device
+    # buffers are double-buffered per step: the H2D of step i (h2d stream) overlaps the
+    # attention of step i-1, the D2H of step i (d2h stream) overlaps step i+1, and the
+    # NLAYERS launches of a step run back to back on the compute stream.
+    def pinned_like(x):
+        return torch.empty((NLAYERS,) + tuple(x.shape), dtype=x.dtype, pin_memory=True)
 
-    # double-buffered device inputs; H2D and D2H each on their own stream so the
-    # copies of layer l+1 / l-1 overlap the attention of layer l
+    hq = [pinned_like(x) for x in q]
+    hk = [pinned_like(x) for x in k]
+    hv = [pinned_like(x) for x in v]
+    ho = [pinned_like(x) for x in out]
+    for hs, ds in ((hq, q), (hk, k), (hv, v)):
+        for a, b in zip(hs, ds):
+            a.copy_(b.unsqueeze(0).expand_as(a).cpu())
+    h2d = sum(x.numel() * x.element_size() for x in hq + hk + hv)
+    d2h = sum(x.numel() * x.element_size() for x in ho)
     h2d_stream = torch.cuda.Stream(device=local)
     d2h_stream = torch.cuda.Stream(device=local)
-    dq = [q, [torch.empty_like(x) for x in q]]
-    dk = [k, [torch.empty_like(x) for x in k]]
-    dv = [v, [torch.empty_like(x) for x in v]]
-    do = [out, [torch.empty_like(x) for x in out]]
+    dq = [[torch.empty(x.shape, dtype=x.dtype, device=local) for x in hq] for _ in range(2)]
+    dk = [[torch.empty(x.shape, dtype=x.dtype, device=local) for x in hk] for _ in range(2)]
+    dv = [[torch.empty(x.shape, dtype=x.dtype, device=local) for x in hv] for _ in range(2)]
+    do = [[torch.empty(x.shape, dtype=x.dtype, device=local) for x in ho] for _ in range(2)]
     h2d_ev = [torch.cuda.Event() for _ in range(2)]
     comp_ev = [torch.cuda.Event() for _ in range(2)]
     d2h_ev = [torch.cuda.Event() for _ in range(2)]
     for e in comp_ev + d2h_ev:
         e.record(stream)
+    e2e_step = [0]
 
     def step_e2e():
+        j = e2e_step[0] & 1
+        e2e_step[0] += 1
+        with torch.cuda.stream(h2d_stream):
+            h2d_stream.wait_event(comp_ev[j])  # step i-2 is done with buffer set j
+            for a, b in zip(dq[j] + dk[j] + dv[j], hq + hk + hv):
+                a.copy_(b, non_blocking=True)
+            h2d_ev[j].record(h2d_stream)
         batch.grow(1)
+        stream.wait_event(h2d_ev[j])
+        stream.wait_event(d2h_ev[j])  # output set j drained to host
         for layer in range(NLAYERS):
-            j = layer & 1
-            with torch.cuda.stream(h2d_stream):
-                h2d_stream.wait_event(comp_ev[j])  # compute of layer-2 is done with buffer j
-                for a, b in zip(dq[j] + dk[j] + dv[j], hq + hk + hv):
-                    a.copy_(b, non_blocking=True)
-                h2d_ev[j].record(h2d_stream)
-            stream.wait_event(h2d_ev[j])
-            stream.wait_event(d2h_ev[j])  # out buffer j drained to host
-            batch.append(dk[j], dv[j], layer, 1, stream)
-            batch.decode(dq[j], do[j], layer, stream=stream)
-            comp_ev[j].record(stream)
-            with torch.cuda.stream(d2h_stream):
-                d2h_stream.wait_event(comp_ev[j])
-                for a, b in zip(ho, do[j]):
-                    a.copy_(b, non_blocking=True)
-                d2h_ev[j].record(d2h_stream)
-        stream.wait_stream(d2h_stream)
-        stream.wait_stream(h2d_stream)
+            batch.decode([x[layer] for x in dq[j]], [x[layer] for x in do[j]], layer, stream=stream,
+                         k=[x[layer] for x in dk[j]], v=[x[layer] for x in dv[j]])
+        comp_ev[j].record(stream)
+        with torch.cuda.stream(d2h_stream):
+            d2h_stream.wait_event(comp_ev[j])
+            for a, b in zip(ho, do[j]):
+                a.copy_(b, non_blocking=True)
+            d2h_ev[j].record(d2h_stream)
 
     for _ in range(args.warmup):
         step_e2e()
@@ -409,6 +416,7 @@ def run_gpu(args):
     for _ in range(args.steps):
         step_e2e()
         kv_e2e += step_bytes(batch, NLAYERS)[0]
+    stream.wait_stream(d2h_stream)  # the last step's outputs are on the host
     e1.record(stream)
     barrier()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1))
@@ -441,12 +449,14 @@ def run_gpu(args):
         },
         "e2e": {"value": round(e2e_value, 1), "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e2e_ms / args.steps, 3)},
-        "roofline": {"bound": "hbm", "kernel": "skv decode_kernel (+plan/combine)",
+        "roofline": {"bound": "hbm", "kernel": "skv decode_kernel (KV append + split-KV combine fused)",
                      "achieved": round(achieved, 1), "peak": hbm, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": round(achieved / hbm, 4), "traffic": traffic, "traffic_source": traffic_src,
                      "traffic_note": "4-service layer launch (layers 0-31); algorithmic bytes of that launch "
                                      f"~{layer0_bytes:.4g}",
                      "avg_launch_ms": round(dec_ms / n_launch, 4),
+                     "timing": f"CUDA events around {nrep} replays of a graph of the step's {NLAYERS} decode "
+                               "launches (inter-kernel gaps included)",
                      "bytes_per_launch": round(dec_bytes / n_launch, 1)},
         "allocator": {"ns_per_grow_op": round(alloc_ns, 2),
                       "note": "batch.grow(1) of every request + GPU placement kernel, wall clock incl. sync"},

@@ -161,6 +161,12 @@ typedef struct {
   float softmax_scale;  /* 0 -> 1/sqrt(head_dim) */
   int32_t layer;        /* logical layer index; groups with num_layers <= layer are skipped */
   int32_t split_tokens; /* 0 = automatic split-KV; else tokens per split (multiple of tpb) */
+  /* Optional fused KV append (NULL = none): the step's new token of every request,
+   * [host array of n_groups dev ptrs] each [B_g][1][Hkv/tp][d], is written at position
+   * tokens-1 of `layer` and attended in the same launch (== skv_append_kv with n_new 1
+   * followed by the decode, one kernel instead of two). */
+  const void* const* k;
+  const void* const* v;
 } skv_decode_args;
 /* Paged decode attention over the unified pool: one launch covers every group of
  * the batch (mixed head counts / GQA ratios).  Context of request r = its current

@@ -11,9 +11,13 @@
 // block-table-indirected addresses, and computes softmax(q·Kᵀ)·V for all G query
 // heads of a KV head from each tile (K/V read once per GQA group).  Work items
 // (request, kv head, split) are fetched dynamically; the ring runs ahead across
-// item boundaries.  Split-KV partials are merged by an LSE combine kernel.
+// item boundaries.  Split-KV partials are merged (LSE combine) by the warp whose
+// split of a (request, kv head) finishes last, inside the same launch.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
+
+#include <cstdlib>
+#include <utility>
 
 #include "skv_internal.h"
 
@@ -71,6 +75,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   while (!mbar_try_wait(bar, phase)) {
   }
 }
+
+// Programmatic dependent launch: kernels launched with the PDL attribute may start
+// while the previous kernel on the stream drains; pdl_wait() blocks until that kernel
+// has completed and its memory is visible, pdl_trigger() lets the next one launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 template <typename T>
 struct Cvt;
@@ -292,12 +302,33 @@ __device__ __forceinline__ void process_item(const DataParams& p, Producer& P, c
     mx[gg] = -INFINITY;
     l[gg] = 0.f;
   }
+  // fused append (n_new == 1): the item holding position ctx-1 writes the step's new
+  // K/V token into the pool and patches it into the staged tile before attending
+  int apos = -1;
+  if (p.n_new == 1 && g.k != nullptr) {
+    const int pos = p.req_tokens[p.handles[it.x]] - 1;
+    if (pos >= it.z && pos < it.w) apos = pos;
+  }
   const int b0 = it.z / kTpb, b1 = (it.w + kTpb - 1) / kTpb;
   for (int b = b0; b < b1; ++b) {
     if (P.issued == P.consumed) fill(p, P, w);
     const int stage = P.consumed % kStages;
     const uint32_t phase = (P.consumed / kStages) & 1u;
     mbar_wait(&w.bars[stage], phase);
+    if (apos >= 0 && b == apos / kTpb) {
+      // lanes 0-15 move the K row, 16-31 the V row (16 B each), as append_kernel
+      const int kv = lane >> 4;
+      const int2 e = p.req_table[(size_t)p.handles[it.x] * p.cap + b];
+      const uint4 val = *reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(kv ? g.v : g.k) +
+                                                        ((size_t)rl * g.Hkv + head) * (kD * 2) + c * 16);
+      const int off = kv * (kTpb * kD * 2) + (apos % kTpb) * (kD * 2) + c * 16;
+      *reinterpret_cast<uint4*>(p.pool + g.layer_off + (long long)head * g.head_stride +
+                                (long long)e.x * p.merged_stride + (long long)e.y * g.native_stride + off) = val;
+      *reinterpret_cast<uint4*>(w.tiles + stage * kTile + off) = val;
+      // the slot is refilled by TMA (async proxy) later: order this generic write first
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+    }
     const int valid = min(kTpb, it.w - b * kTpb);
     if (valid == kTpb) consume_tile<T, G, false>(w.tiles + stage * kTile, lane, valid, q, o, mx, l);
     else consume_tile<T, G, true>(w.tiles + stage * kTile, lane, valid, q, o, mx, l);
@@ -331,16 +362,67 @@ __device__ __forceinline__ void process_item(const DataParams& p, Producer& P, c
       }
     }
   } else {
-    const int split = it.z / p.split_tokens;
+    // split-KV: publish this split's (m, l, o) partials; the split that arrives last
+    // for this (request, kv head) merges all of them (LSE combine) and writes out.
+    const int pb = p.pbase[it.x];
+    const int split = it.z / p.rsplit[it.x];
 #pragma unroll
     for (int gg = 0; gg < G; ++gg) {
-      const size_t slot = (size_t)p.pbase[it.x] + (size_t)split * g.Hq + head * G + gg;
+      const size_t slot = (size_t)pb + (size_t)split * g.Hq + head * G + gg;
       if (hf == 0) {
         float4* dst = reinterpret_cast<float4*>(p.ws_o + slot * kD + c * 8);
-        dst[0] = make_float4(o[gg][0], o[gg][1], o[gg][2], o[gg][3]);
-        dst[1] = make_float4(o[gg][4], o[gg][5], o[gg][6], o[gg][7]);
+        __stcg(dst, make_float4(o[gg][0], o[gg][1], o[gg][2], o[gg][3]));
+        __stcg(dst + 1, make_float4(o[gg][4], o[gg][5], o[gg][6], o[gg][7]));
       }
-      if (lane == 0) p.ws_ml[slot] = make_float2(mx[gg], l[gg]);
+      if (lane == 0) __stcg(p.ws_ml + slot, make_float2(mx[gg], l[gg]));
+    }
+    __syncwarp();
+    int last = 0;
+    if (lane == 0) {
+      __threadfence();
+      last = atomicAdd(p.arrive + pb + head, 1) == ns - 1;
+      if (last) __threadfence();
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (last) {
+      // lane (c, hf): dims [8c, 8c+8) over splits hf, hf+2, ...
+#pragma unroll
+      for (int gg = 0; gg < G; ++gg) {
+        const int hq = head * G + gg;
+        float M = -INFINITY;
+        for (int s = hf; s < ns; s += 2) M = fmaxf(M, __ldcg(p.ws_ml + pb + (size_t)s * g.Hq + hq).x);
+        M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 16));
+        float L = 0.f, acc[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+        for (int s = hf; s < ns; s += 2) {
+          const size_t slot = (size_t)pb + (size_t)s * g.Hq + hq;
+          const float2 ml = __ldcg(p.ws_ml + slot);
+          const float wgt = ml.y > 0.f ? exp2f(ml.x - M) : 0.f;
+          L += ml.y * wgt;
+          const float4* src = reinterpret_cast<const float4*>(p.ws_o + slot * kD + c * 8);
+          const float4 a = __ldcg(src), b = __ldcg(src + 1);
+          acc[0] += a.x * wgt;
+          acc[1] += a.y * wgt;
+          acc[2] += a.z * wgt;
+          acc[3] += a.w * wgt;
+          acc[4] += b.x * wgt;
+          acc[5] += b.y * wgt;
+          acc[6] += b.z * wgt;
+          acc[7] += b.w * wgt;
+        }
+        L += __shfl_xor_sync(0xffffffffu, L, 16);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], 16);
+        if (hf == 0) {
+          const float inv = L > 0.f ? 1.f / L : 0.f;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[j] *= inv;
+          T* op = reinterpret_cast<T*>(g.out) + ((size_t)rl * g.Hq + hq) * kD + c * 8;
+          *reinterpret_cast<uint4*>(op) = Cvt<T>::from_f32(acc);
+        }
+      }
+      if (lane == 0) p.arrive[pb + head] = 0;  // ready for the next launch
     }
   }
 }
@@ -354,7 +436,6 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const __grid_con
   w.bars = reinterpret_cast<uint64_t*>(smem + kWarps * kStages * kTile) + wid * kStages;
   w.ring = reinterpret_cast<int*>(smem + kWarps * kStages * kTile + kWarps * kStages * 8) + wid * kRing;
   w.lane = lane;
-  w.n_items = *p.n_items;
   w.policy = evict_first_policy();
   if (lane == 0) {
 #pragma unroll
@@ -373,6 +454,17 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const __grid_con
   P.done = 0;
   P.pushed = P.popped = 0;
   P.issued = P.consumed = 0;
+  // Everything before pdl_wait() overlaps the previous launch's tail.  With prefetch the
+  // first kStages K/V tiles of this warp are already in flight: the cache bytes of this
+  // layer do not depend on the previous launch (see DataParams::prefetch).
+  if (p.prefetch) {
+    w.n_items = *p.n_items;
+    fill(p, P, w);
+  }
+  pdl_wait();
+  // the next launch may queue its CTAs now (they become resident as this grid's CTAs exit)
+  pdl_trigger();
+  if (!p.prefetch) w.n_items = *p.n_items;
   for (;;) {
     fill(p, P, w);
     if (P.pushed == P.popped) {
@@ -389,6 +481,16 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const __grid_con
     else if (MAXG >= 4 && G == 4) process_item<T, (MAXG >= 4 ? 4 : 1)>(p, P, w, it);
     else if (MAXG >= 8 && G == 8) process_item<T, (MAXG >= 8 ? 8 : 1)>(p, P, w, it);
   }
+  // the last CTA to finish resets the work counter for the next launch (no memset node)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(p.counter + 1, 1) == (int)gridDim.x - 1) {
+      p.counter[0] = 0;
+      p.counter[1] = 0;
+      __threadfence();
+    }
+  }
 }
 
 // Work list: one item per (request, split, kv head); partial slots for split requests.
@@ -396,6 +498,8 @@ __global__ void __launch_bounds__(1024) plan_kernel(DataParams p) {
   __shared__ int sm_warp[33];
   __shared__ int carry_items, carry_slots;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  pdl_wait();  // the previous decode may still be reading the work list
+  pdl_trigger();
   if (tid == 0) carry_items = carry_slots = 0;
   __syncthreads();
   auto scan = [&](int v, int* total) {
@@ -439,11 +543,15 @@ __global__ void __launch_bounds__(1024) plan_kernel(DataParams p) {
     const int ex_i = scan(valid ? ns * hkv : 0, &ti);
     const int ex_s = scan(valid && ns > 1 ? ns * hq : 0, &ts);
     if (valid) {
+      // balanced splits: ns = ceil(ctx / split_tokens) pieces of round_up(ceil(ctx / ns), tpb)
+      // tokens (<= split_tokens, and every piece non-empty)
+      const int rs = ns > 1 ? ((ctx + ns - 1) / ns + kTpb - 1) / kTpb * kTpb : max(ctx, 1);
       p.nsplit[r] = ns;
+      p.rsplit[r] = rs;
       p.pbase[r] = carry_slots + ex_s;
       int4* dst = p.items + carry_items + ex_i;
       for (int s = 0; s < ns; ++s) {
-        const int tb = s * p.split_tokens, te = min(ctx, tb + p.split_tokens);
+        const int tb = s * rs, te = min(ctx, tb + rs);
         for (int h = 0; h < hkv; ++h) dst[s * hkv + h] = make_int4(r, (grp << 16) | h, tb, te);
       }
     }
@@ -456,49 +564,16 @@ __global__ void __launch_bounds__(1024) plan_kernel(DataParams p) {
   }
   if (tid == 0) {
     *p.n_items = carry_items;
-    *p.counter = 0;
-  }
-}
-
-// LSE merge of split partials: one warp per (request, q head); lane owns 4 dims.
-template <typename T>
-__global__ void combine_kernel(const __grid_constant__ DataParams p) {
-  const int r = blockIdx.y;
-  if (p.nsplit[r] <= 1) return;
-  const int grp = p.req_group[r];
-  const DataGroup& g = p.g[grp];
-  if (!g.active) return;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int ns = p.nsplit[r];
-  for (int hq = blockIdx.x * (blockDim.x >> 5) + wid; hq < g.Hq; hq += gridDim.x * (blockDim.x >> 5)) {
-    float M = -INFINITY;
-    for (int s = 0; s < ns; ++s) M = fmaxf(M, p.ws_ml[(size_t)p.pbase[r] + (size_t)s * g.Hq + hq].x);
-    float L = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int s = 0; s < ns; ++s) {
-      const size_t slot = (size_t)p.pbase[r] + (size_t)s * g.Hq + hq;
-      const float2 ml = p.ws_ml[slot];
-      const float wgt = ml.y > 0.f ? exp2f(ml.x - M) : 0.f;
-      L += ml.y * wgt;
-      const float4 v = *reinterpret_cast<const float4*>(p.ws_o + slot * kD + lane * 4);
-      acc[0] += v.x * wgt;
-      acc[1] += v.y * wgt;
-      acc[2] += v.z * wgt;
-      acc[3] += v.w * wgt;
-    }
-    const float inv = L > 0.f ? 1.f / L : 0.f;
-    uint16_t* op = reinterpret_cast<uint16_t*>(g.out) + ((size_t)(r - g.req_begin) * g.Hq + hq) * kD + lane * 4;
-    ushort4 out;
-    out.x = Cvt<T>::one(acc[0] * inv);
-    out.y = Cvt<T>::one(acc[1] * inv);
-    out.z = Cvt<T>::one(acc[2] * inv);
-    out.w = Cvt<T>::one(acc[3] * inv);
-    *reinterpret_cast<ushort4*>(op) = out;
+    p.counter[0] = 0;  // this launch's counter set (each decode launch also self-resets its set)
+    p.counter[1] = 0;
   }
 }
 
 // KV append: one warp per (request, new token, kv head); lanes 0-15 move the K row
 // (256 B), lanes 16-31 the V row, 16 B each.
 __global__ void append_kernel(const __grid_constant__ DataParams p) {
+  pdl_wait();
+  pdl_trigger();
   const int r = blockIdx.y;
   const DataGroup& g = p.g[p.req_group[r]];
   if (!g.active) return;
@@ -538,6 +613,32 @@ __global__ void synth_kernel(uint4* pool, size_t n16, unsigned long long seed, f
   }
 }
 
+bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("SKV_NO_PDL");
+    on = (e && e[0] == '1') ? 0 : 1;
+  }
+  return on == 1;
+}
+
+// Launch with the programmatic-stream-serialization attribute (see pdl_wait).
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 int g_num_sms = 0;
 int num_sms() {
   if (!g_num_sms) {
@@ -557,14 +658,16 @@ void launch_decode_t(const DataParams& p, int grid, cudaStream_t s) {
     cudaFuncSetAttribute(decode_kernel<T, MAXG>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
-  decode_kernel<T, MAXG><<<grid, kWarps * 32, smem, s>>>(p);
+  launch_pdl(decode_kernel<T, MAXG>, dim3(grid), dim3(kWarps * 32), smem, s, p);
 }
 
 }  // namespace
 
 int decode_ctas_per_sm() { return 1; }
 
-void launch_decode_plan(const DataParams& p, cudaStream_t s) { plan_kernel<<<1, 1024, 0, s>>>(p); }
+void launch_decode_plan(const DataParams& p, cudaStream_t s) {
+  launch_pdl(plan_kernel, dim3(1), dim3(1024), 0, s, p);
+}
 
 void launch_decode(const DataParams& p, int max_g, int grid, cudaStream_t s) {
   if (grid <= 0) grid = num_sms() * decode_ctas_per_sm();
@@ -581,18 +684,12 @@ void launch_decode(const DataParams& p, int max_g, int grid, cudaStream_t s) {
   }
 }
 
-void launch_decode_combine(const DataParams& p, cudaStream_t s) {
-  dim3 grid(1, p.nreq);
-  if (p.dtype == 0) combine_kernel<__half><<<grid, 256, 0, s>>>(p);
-  else combine_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(p);
-}
-
 void launch_append(const DataParams& p, cudaStream_t s) {
   int maxh = 1;
   for (int i = 0; i < p.ngroups; ++i) maxh = max(maxh, p.g[i].Hkv);
   const int warps = p.n_new * maxh;
   dim3 grid((warps + 7) / 8, p.nreq);
-  append_kernel<<<grid, 256, 0, s>>>(p);
+  launch_pdl(append_kernel, grid, dim3(256), 0, s, p);
 }
 
 void launch_synth_fill(void* pool, size_t bytes, int dtype, unsigned long long seed, float amp,

@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <unordered_map>
@@ -140,10 +141,13 @@ struct skv_batch {
   int* d_counter = nullptr;
   int* d_pbase = nullptr;
   int* d_nsplit = nullptr;
+  int* d_rsplit = nullptr;
+  int* d_arrive = nullptr;     // [slots_cap] split arrivals per (request, kv head)
   float* d_ws_o = nullptr;
   float2* d_ws_ml = nullptr;
   size_t slots_cap = 0;
   uint64_t plan_epoch = ~0ull;
+  uint64_t launch_seq = 0;
   int plan_split = 0;
   bool plan_has_split = false;
 };
@@ -874,19 +878,21 @@ static skv_status batch_fill(skv_pool* p, skv_batch* b, const int32_t* group_mod
   DeviceGuard guard(p->device);
   if ((size_t)total > b->req_cap) {
     SKV_CUDA(p, cudaStreamSynchronize(p->stream));
-    for (void* q : {(void*)b->d_handles, (void*)b->d_group, (void*)b->d_pbase, (void*)b->d_nsplit})
+    for (void* q : {(void*)b->d_handles, (void*)b->d_group, (void*)b->d_pbase, (void*)b->d_nsplit,
+                    (void*)b->d_rsplit})
       if (q) cudaFree(q);
     b->req_cap = std::max<size_t>((size_t)total * 2, 64);
     skv_status st;
     if ((st = dev_alloc(p, &b->d_handles, b->req_cap, false)) || (st = dev_alloc(p, &b->d_group, b->req_cap, false)) ||
-        (st = dev_alloc(p, &b->d_pbase, b->req_cap)) || (st = dev_alloc(p, &b->d_nsplit, b->req_cap)))
+        (st = dev_alloc(p, &b->d_pbase, b->req_cap)) || (st = dev_alloc(p, &b->d_nsplit, b->req_cap)) ||
+        (st = dev_alloc(p, &b->d_rsplit, b->req_cap)))
       return st;
     if (b->h_stage) cudaFreeHost(b->h_stage);
     SKV_CUDA(p, cudaMallocHost(&b->h_stage, b->req_cap * 2 * sizeof(int32_t)));
   }
   if (!b->d_nitems) {
     skv_status st;
-    if ((st = dev_alloc(p, &b->d_nitems, 1)) || (st = dev_alloc(p, &b->d_counter, 1))) return st;
+    if ((st = dev_alloc(p, &b->d_nitems, 1)) || (st = dev_alloc(p, &b->d_counter, 4))) return st;
   }
   if (total) {
     // stage through pinned memory on the pool stream (wait for the previous upload first)
@@ -928,8 +934,8 @@ void skv_batch_destroy(skv_batch* b) {
   DeviceGuard g(b->pool->device);
   cudaStreamSynchronize(b->pool->stream);
   for (void* q : {(void*)b->d_handles, (void*)b->d_group, (void*)b->d_items, (void*)b->d_nitems,
-                  (void*)b->d_counter, (void*)b->d_pbase, (void*)b->d_nsplit, (void*)b->d_ws_o,
-                  (void*)b->d_ws_ml})
+                  (void*)b->d_counter, (void*)b->d_pbase, (void*)b->d_nsplit, (void*)b->d_rsplit,
+                  (void*)b->d_arrive, (void*)b->d_ws_o, (void*)b->d_ws_ml})
     if (q) cudaFree(q);
   if (b->h_stage) cudaFreeHost(b->h_stage);
   if (b->stage_ev) cudaEventDestroy(b->stage_ev);
@@ -1048,9 +1054,16 @@ skv_status skv_decode_attention(skv_pool* p, skv_batch* b, const skv_decode_args
   if ((st = make_params(p, b, a->layer, &dp))) return st;
   int maxg = 1;
   long long sum_hkv = 0, work = 0, max_ctx = 0;
+  if ((a->k == nullptr) != (a->v == nullptr))
+    return fail(p, SKV_ERR_ARG, "decode: fused append needs both k and v");
+  dp.n_new = a->k ? 1 : 0;  // 1 = fused append of the step's token
   for (int g = 0; g < b->ngroups; ++g) {
     dp.g[g].q = a->q[g];
     dp.g[g].out = a->out[g];
+    if (a->k) {
+      dp.g[g].k = a->k[g];
+      dp.g[g].v = a->v[g];
+    }
     maxg = std::max(maxg, dp.g[g].G);
     for (int i = 0; i < b->gsize[g]; ++i) {
       const long long ctx = p->req[b->handles[b->gbegin[g] + i]].tokens;
@@ -1061,13 +1074,16 @@ skv_status skv_decode_attention(skv_pool* p, skv_batch* b, const skv_decode_args
   }
   const float scale = a->softmax_scale > 0.f ? a->softmax_scale : 1.0f / std::sqrt(128.0f);
   dp.scale_log2 = scale * 1.4426950408889634f;
-  // split-KV: enough work items to cover every warp slot several times
+  // split-KV only when the unsplit (request, kv head) items cannot keep every warp slot
+  // busy for ~1.5 rounds (measured: at config 1, 1.95 rounds unsplit beats any split);
+  // then enough balanced splits to cover the slots ~4 times
   int split = a->split_tokens;
   if (split <= 0) {
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p->device);
-    const long long target = 4LL * nsm * 8;
-    if (sum_hkv >= target || max_ctx <= 256) split = (int)std::max<long long>(round_up(std::max(max_ctx, 1LL), 16), 16);
+    const long long slots8 = (long long)nsm * 8, target = 4LL * slots8;
+    if (2 * sum_hkv >= 3 * slots8 || max_ctx <= 256)
+      split = (int)std::max<long long>(round_up(std::max(max_ctx, 1LL), 16), 16);
     else split = (int)std::max<long long>(256, round_up(ceil_div_ll(work, target), 16));
   }
   split = (int)round_up(split, 16);
@@ -1098,34 +1114,48 @@ skv_status skv_decode_attention(skv_pool* p, skv_batch* b, const skv_decode_args
     SKV_CUDA(p, cudaStreamSynchronize(s));
     if (b->d_ws_o) cudaFree(b->d_ws_o);
     if (b->d_ws_ml) cudaFree(b->d_ws_ml);
+    if (b->d_arrive) cudaFree(b->d_arrive);
     b->slots_cap = (size_t)slots * 2;
+    if ((st = dev_alloc(p, &b->d_arrive, 2 * b->slots_cap))) return st;
     SKV_CUDA(p, cudaMalloc(&b->d_ws_o, b->slots_cap * 128 * sizeof(float)));
     SKV_CUDA(p, cudaMalloc(&b->d_ws_ml, b->slots_cap * sizeof(float2)));
     b->plan_epoch = ~0ull;
   }
   dp.items = b->d_items;
   dp.n_items = b->d_nitems;
-  dp.counter = b->d_counter;
+  // Consecutive decode launches alternate between two (work counter, arrival counter)
+  // sets: under programmatic dependent launch the next launch starts fetching work
+  // while this one drains, and each launch's last CTA / last split resets its own set.
+  const int parity = (int)(b->launch_seq++ & 1);
+  dp.counter = b->d_counter + 2 * parity;
   dp.pbase = b->d_pbase;
   dp.nsplit = b->d_nsplit;
+  dp.rsplit = b->d_rsplit;
+  dp.arrive = b->d_arrive + parity * b->slots_cap;
   dp.ws_o = b->d_ws_o;
   dp.ws_ml = b->d_ws_ml;
   if ((st = order_streams(p, s))) return st;
+  bool planned = false;
   if (b->plan_epoch != p->token_epoch || b->plan_split != split) {
     skv::launch_decode_plan(dp, s);
     p->launches++;
     b->plan_epoch = p->token_epoch;
     b->plan_split = split;
     b->plan_has_split = any_split;
-  } else {
-    SKV_CUDA(p, cudaMemsetAsync(b->d_counter, 0, sizeof(int), s));
+    planned = true;
   }
+  // K/V tiles may be prefetched before the previous launch completes only when nothing
+  // that launch may still write is read early: the work list comes from an earlier
+  // plan, and the new token (the only pool bytes written by a fused decode) is patched
+  // in after the wait by this launch's own fused append.
+  static const bool no_prefetch = [] {
+    const char* e = getenv("SKV_NO_PREFETCH");
+    return e && e[0] == '1';
+  }();
+  dp.prefetch = (!planned && dp.n_new == 1 && !no_prefetch) ? 1 : 0;
+  // split partials are merged inside the decode kernel; its work counter self-resets
   skv::launch_decode(dp, maxg, 0, s);
   p->launches++;
-  if (any_split) {
-    skv::launch_decode_combine(dp, s);
-    p->launches++;
-  }
   return after_data(p, s);
 }
 

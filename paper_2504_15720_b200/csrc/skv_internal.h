@@ -104,16 +104,18 @@ struct DataParams {
   // decode plan
   int4* items;               // [max_items] {req, (group<<16)|kv_head, tok_begin, tok_end}
   int* n_items;
-  int* counter;              // dynamic work counter
+  int* counter;              // [2] dynamic work counter, finished-CTA count (both self-resetting)
+  int prefetch;              // 1: K/V loads may be issued before the PDL wait (see skv_capi.cpp)
   int* pbase;                // [nreq] partial-slot base (split requests)
   int* nsplit;               // [nreq]
+  int* rsplit;               // [nreq] tokens per split of the request (balanced, multiple of tpb)
+  int* arrive;               // [slots] per (request, kv head) split arrivals (self-resetting)
   float* ws_o;               // [slots][D] unnormalised partial outputs
   float2* ws_ml;             // [slots] (running max (log2 domain), sum)
 };
 
 void launch_decode_plan(const DataParams& p, cudaStream_t s);
 void launch_decode(const DataParams& p, int max_g, int grid, cudaStream_t s);
-void launch_decode_combine(const DataParams& p, cudaStream_t s);
 void launch_append(const DataParams& p, cudaStream_t s);
 void launch_prefill(const DataParams& p, cudaStream_t s);
 void launch_synth_fill(void* pool, size_t bytes, int dtype, unsigned long long seed, float amp,

@@ -109,7 +109,8 @@ class Layout(C.Structure):
 
 class _DecodeArgs(C.Structure):
     _fields_ = [("q", C.POINTER(C.c_void_p)), ("out", C.POINTER(C.c_void_p)), ("softmax_scale", C.c_float),
-                ("layer", C.c_int32), ("split_tokens", C.c_int32)]
+                ("layer", C.c_int32), ("split_tokens", C.c_int32), ("k", C.POINTER(C.c_void_p)),
+                ("v", C.POINTER(C.c_void_p))]
 
 
 class _AppendArgs(C.Structure):
@@ -481,12 +482,22 @@ class Batch:
         return kv.value, tot.value
 
     def decode(self, q: Sequence, out: Sequence, layer: int, softmax_scale: float = 0.0, split_tokens: int = 0,
-               stream=None):
+               stream=None, k: Sequence | None = None, v: Sequence | None = None):
+        """Paged decode attention of every group for ``layer``.  With ``k``/``v`` (each
+        [B_g, 1, Hkv, d]) the step's new token is appended at position tokens-1 inside the
+        same launch (fused ``append(k, v, layer, 1)``)."""
         n = len(self.groups)
         qa = (C.c_void_p * n)(*[_ptr(t) for t in q])
         oa = (C.c_void_p * n)(*[_ptr(t) for t in out])
         a = _DecodeArgs(C.cast(qa, C.POINTER(C.c_void_p)), C.cast(oa, C.POINTER(C.c_void_p)), softmax_scale,
                         layer, split_tokens)
+        if (k is None) != (v is None):
+            raise ValueError("decode: pass both k and v for the fused append, or neither")
+        if k is not None:
+            ka = (C.c_void_p * n)(*[_ptr(t) for t in k])
+            va = (C.c_void_p * n)(*[_ptr(t) for t in v])
+            a.k = C.cast(ka, C.POINTER(C.c_void_p))
+            a.v = C.cast(va, C.POINTER(C.c_void_p))
         self.cache._chk(self.cache._lib.skv_decode_attention(self.cache._h, self._h, C.byref(a),
                                                              _stream_ptr(stream)))
 

@@ -217,3 +217,101 @@ def test_unwritten_tail_slots_with_nan_are_ignored():
         s = (kk[:, h // 2] @ q[0, h].float()) / np.sqrt(128.0)
         ref = torch.softmax(s, 0) @ vv[:, h // 2]
         assert (out[0, h].float() - ref).abs().max().item() <= 2e-3
+
+
+@pytest.mark.parametrize("split", [0, 32])
+def test_fused_append_decode_equals_append_then_decode(split):
+    """decode(k=, v=) appends the step's token inside the decode launch: pool bytes and
+    outputs identical to append(n_new=1) followed by decode (incl. split-KV, where only
+    the item holding position ctx-1 writes), and within tolerance of the oracle."""
+    shapes = [(3, 8, 32), (3, 4, 4), (4, 2, 16)]
+    ctxs = [[40, 7, 300], [16, 1], [129, 64]]
+    res = []
+    for fused in (False, True):
+        cache, groups = build_pool(shapes, ctxs, seed=77)
+        b = cache.batch(groups)
+        assert b.grow(1) == 7
+        gen = torch.Generator(device="cuda").manual_seed(5)
+        ks = [(torch.rand((len(ids), 1, H, 128), generator=gen, device="cuda") - 0.5).half()
+              for (mi, ids), (L, H, Hq) in zip(groups, shapes)]
+        vs = [(torch.rand((len(ids), 1, H, 128), generator=gen, device="cuda") - 0.5).half()
+              for (mi, ids), (L, H, Hq) in zip(groups, shapes)]
+        qs = [torch.randn((len(ids), Hq, 128), generator=gen, device="cuda").half()
+              for (mi, ids), (L, H, Hq) in zip(groups, shapes)]
+        outs = [torch.empty_like(q) for q in qs]
+        n0 = cache.kernel_launches()
+        if fused:
+            b.decode(qs, outs, 2, split_tokens=split, k=ks, v=vs)
+        else:
+            b.append(ks, vs, 2, n_new=1)
+            b.decode(qs, outs, 2, split_tokens=split)
+        torch.cuda.synchronize()
+        res.append((host_image(cache), [o.clone() for o in outs], cache.kernel_launches() - n0, cache, groups, qs))
+    (img0, out0, n_sep, _, _, _), (img1, out1, n_fused, cache, groups, qs) = res
+    assert np.array_equal(img0, img1)
+    assert all(torch.equal(a, c) for a, c in zip(out0, out1))
+    assert n_fused == n_sep - 1
+    for (mi, ids), q, o in zip(groups, qs, out1):
+        ctx = np.array([ctxs[mi][j] + 1 for j in range(len(ids))], dtype=np.int64)
+        ref = O.decode_attention(oracle_layout(cache, mi), img1, 2, tables_of(cache, ids), ctx,
+                                 q.view(torch.int16).cpu().numpy().view(np.uint16), 1.0 / np.sqrt(128.0))
+        assert np.abs(o.float().cpu().numpy() - ref).max() <= 2e-3
+
+
+@pytest.mark.parametrize("split", [0, 32])
+def test_back_to_back_fused_launches_match_serialised(split):
+    """Layer after layer of fused append+decode launched back to back (programmatic
+    dependent launch lets launch l+1 prefetch K/V while l drains; counters alternate
+    between two sets) gives the same pool and outputs as the same launches each followed
+    by a device synchronisation, over two decode steps, eager and as a CUDA graph."""
+    shapes = [(4, 8, 32), (3, 4, 4)]
+    ctxs = [[40, 300, 17], [64, 1]]
+
+    def run(mode):
+        cache, groups = build_pool(shapes, ctxs, seed=5, phys_layers=1)
+        torch.cuda.synchronize()
+        s = torch.cuda.Stream()
+        torch.cuda.set_stream(s)
+        cache.set_stream(s)
+        b = cache.batch(groups)
+        gen = torch.Generator(device="cuda").manual_seed(11)
+        outs_all = []
+        graph = None
+        for step in range(2):
+            b.grow(1)
+            cache.flush()
+            ks = [[(torch.rand((len(ids), 1, H, 128), generator=gen, device="cuda") - 0.5).half()
+                   for (mi, ids), (L, H, Hq) in zip(groups, shapes)] for _ in range(4)]
+            vs = [[(torch.rand((len(ids), 1, H, 128), generator=gen, device="cuda") - 0.5).half()
+                   for (mi, ids), (L, H, Hq) in zip(groups, shapes)] for _ in range(4)]
+            qs = [[torch.randn((len(ids), Hq, 128), generator=gen, device="cuda").half()
+                   for (mi, ids), (L, H, Hq) in zip(groups, shapes)] for _ in range(4)]
+            outs = [[torch.empty_like(q) for q in ql] for ql in qs]
+            if mode == "graph":
+                b.decode(qs[0], outs[0], 0, split_tokens=split, k=ks[0], v=vs[0])  # plan outside
+                torch.cuda.synchronize()
+                graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(graph, stream=s):
+                    for layer in range(4):
+                        b.decode(qs[layer], outs[layer], layer, split_tokens=split, k=ks[layer], v=vs[layer],
+                                 stream=s)
+                graph.replay()
+            else:
+                for layer in range(4):
+                    b.decode(qs[layer], outs[layer], layer, split_tokens=split, k=ks[layer], v=vs[layer])
+                    if mode == "sync":
+                        torch.cuda.synchronize()
+            torch.cuda.synchronize()
+            outs_all.append([[o.clone() for o in ol] for ol in outs])
+        torch.cuda.synchronize()
+        torch.cuda.set_stream(torch.cuda.default_stream())
+        return host_image(cache), outs_all
+
+    img_s, out_s = run("sync")
+    for mode in ("eager", "graph"):
+        img, out = run(mode)
+        assert np.array_equal(img, img_s), mode
+        for a_step, b_step in zip(out, out_s):
+            for layer, (a_l, b_l) in enumerate(zip(a_step, b_step)):
+                # groups whose model has <= layer layers are skipped (output untouched)
+                assert all(torch.equal(x, y) for x, y, (L, _, _) in zip(a_l, b_l, shapes) if layer < L), mode
