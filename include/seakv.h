@@ -160,7 +160,9 @@ typedef struct {
   void* const* out;     /* [host array of n_groups dev ptrs] each [B_g][Hq/tp][d] */
   float softmax_scale;  /* 0 -> 1/sqrt(head_dim) */
   int32_t layer;        /* logical layer index; groups with num_layers <= layer are skipped */
-  int32_t split_tokens; /* 0 = automatic split-KV; else tokens per split (multiple of tpb) */
+  int32_t split_tokens; /* split-KV: max tokens of a (request, kv head)'s first piece (the
+                           work list also cuts ~1/4 of every context into two trailing
+                           pieces, see plan_kernel); 0 = automatic */
   /* Optional fused KV append (NULL = none): the step's new token of every request,
    * [host array of n_groups dev ptrs] each [B_g][1][Hkv/tp][d], is written at position
    * tokens-1 of `layer` and attended in the same launch (== skv_append_kv with n_new 1
@@ -207,6 +209,11 @@ skv_status skv_synth_fill(skv_pool* p, uint64_t seed, float amp, void* stream);
 /* Copies merged blocks ids[0..n) to host dst (n * merged_stride bytes). Syncs. */
 skv_status skv_read_blocks(skv_pool* p, const int32_t* ids, size_t n, void* dst);
 /* Number of GPU kernels this pool has launched (instrumentation for bench.py). */
+/* Debug: with SKV_TRACE=1 in the environment every decode launch of `b` records, per
+ * warp, {start, after the dependent-launch wait, end} (globaltimer ns) and
+ * tiles<<32 | items; this copies the last launch's records (4 u64 each) to `host`
+ * (*n = records).  *n = 0 when tracing is off. */
+skv_status skv_debug_decode_trace(skv_pool* p, skv_batch* b, uint64_t* host, size_t cap, size_t* n);
 uint64_t skv_kernel_launches(const skv_pool* p);
 
 #ifdef __cplusplus

@@ -17,6 +17,8 @@
 // each model — all computed by one 1024-thread CTA with warp-aggregated scans.
 // Frees are order-independent (set inserts): one warp per request with
 // warp-aggregated atomics on the occupancy masks, then an idempotent fix-up pass.
+#include <algorithm>
+
 #include "skv_internal.h"
 
 namespace skv {
@@ -329,6 +331,25 @@ __global__ void free_fixup_kernel(DevAlloc st, AllocParams pr, const FreeOp* __r
 }
 
 }  // namespace
+
+// Host (pinned, mapped) -> device copy done by SMs instead of a copy engine: the small
+// per-step op uploads must not queue behind a caller's bulk H2D/D2H copies in the copy
+// engines' FIFOs (measured: a 200 MB input copy on another stream delayed the step's
+// allocator upload by its full duration).
+__global__ void stage_copy_kernel(uint32_t* __restrict__ dst, const uint32_t* __restrict__ src, size_t n4) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
+// bytes: a multiple of 4 (ops and index arrays)
+void launch_stage_copy(void* dst, const void* src_host_mapped, size_t bytes, cudaStream_t s) {
+  const size_t n4 = bytes / 4;
+  if (!n4) return;
+  const int threads = 256;
+  const int blocks = (int)std::min<size_t>((n4 + threads - 1) / threads, 64);
+  stage_copy_kernel<<<blocks, threads, 0, s>>>(static_cast<uint32_t*>(dst), static_cast<const uint32_t*>(src_host_mapped),
+                                               n4);
+}
 
 void launch_grow(const DevAlloc& st, const AllocParams& pr, const GrowOp* ops, int n,
                  const GrowScratch& sc, cudaStream_t s) {

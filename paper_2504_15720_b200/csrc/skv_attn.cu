@@ -11,8 +11,9 @@
 // block-table-indirected addresses, and computes softmax(q·Kᵀ)·V for all G query
 // heads of a KV head from each tile (K/V read once per GQA group).  Work items
 // (request, kv head, split) are fetched dynamically; the ring runs ahead across
-// item boundaries.  Split-KV partials are merged (LSE combine) by the warp whose
-// split of a (request, kv head) finishes last, inside the same launch.
+// item boundaries; the work list is ordered by decreasing piece size (plan_kernel).
+// Pieces of a cut (request, kv head) are merged (LSE combine) by the piece that
+// finishes last, inside the same launch.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -79,6 +80,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 // Programmatic dependent launch: kernels launched with the PDL attribute may start
 // while the previous kernel on the stream drains; pdl_wait() blocks until that kernel
 // has completed and its memory is visible, pdl_trigger() lets the next one launch.
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
@@ -283,7 +289,7 @@ __device__ __forceinline__ void fill(const DataParams& p, Producer& P, const War
 
 template <typename T, int G>
 __device__ __forceinline__ void process_item(const DataParams& p, Producer& P, const WarpCtx& w,
-                                             const int4 it) {
+                                             const int4 it, int idx) {
   const int lane = w.lane, c = lane & 15, hf = lane >> 4;
   const int grp = it.y >> 16, head = it.y & 0xffff;
   const DataGroup& g = p.g[grp];
@@ -348,7 +354,8 @@ __device__ __forceinline__ void process_item(const DataParams& p, Producer& P, c
 #pragma unroll
     for (int j = 0; j < 8; ++j) o[gg][j] += __shfl_xor_sync(0xffffffffu, o[gg][j], 16);
   }
-  const int ns = p.nsplit[it.x];
+  const int4 x = p.itemx[idx];  // {pieces, partial-slot base, piece, arrival index}
+  const int ns = x.x;
   if (ns <= 1) {
 #pragma unroll
     for (int gg = 0; gg < G; ++gg) {
@@ -361,76 +368,77 @@ __device__ __forceinline__ void process_item(const DataParams& p, Producer& P, c
         *reinterpret_cast<uint4*>(op) = Cvt<T>::from_f32(r);
       }
     }
-  } else {
-    // split-KV: publish this split's (m, l, o) partials; the split that arrives last
-    // for this (request, kv head) merges all of them (LSE combine) and writes out.
-    const int pb = p.pbase[it.x];
-    const int split = it.z / p.rsplit[it.x];
+    return;
+  }
+  // piece of a cut (request, kv head): publish (m, l, o); the piece that finishes last
+  // merges all of them (LSE combine) and writes the output, inside this launch
 #pragma unroll
-    for (int gg = 0; gg < G; ++gg) {
-      const size_t slot = (size_t)pb + (size_t)split * g.Hq + head * G + gg;
-      if (hf == 0) {
-        float4* dst = reinterpret_cast<float4*>(p.ws_o + slot * kD + c * 8);
-        __stcg(dst, make_float4(o[gg][0], o[gg][1], o[gg][2], o[gg][3]));
-        __stcg(dst + 1, make_float4(o[gg][4], o[gg][5], o[gg][6], o[gg][7]));
-      }
-      if (lane == 0) __stcg(p.ws_ml + slot, make_float2(mx[gg], l[gg]));
+  for (int gg = 0; gg < G; ++gg) {
+    const size_t slot = (size_t)x.y + (size_t)x.z * G + gg;
+    if (hf == 0) {
+      float4* dst = reinterpret_cast<float4*>(p.ws_o + slot * kD + c * 8);
+      __stcg(dst, make_float4(o[gg][0], o[gg][1], o[gg][2], o[gg][3]));
+      __stcg(dst + 1, make_float4(o[gg][4], o[gg][5], o[gg][6], o[gg][7]));
     }
-    __syncwarp();
-    int last = 0;
-    if (lane == 0) {
-      __threadfence();
-      last = atomicAdd(p.arrive + pb + head, 1) == ns - 1;
-      if (last) __threadfence();
+    if (lane == 0) __stcg(p.ws_ml + slot, make_float2(mx[gg], l[gg]));
+  }
+  __syncwarp();
+  int last = 0;
+  if (lane == 0) {
+    __threadfence();
+    last = atomicAdd(p.arrive + x.w, 1) == ns - 1;
+    if (last) __threadfence();
+  }
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (!last) return;
+#pragma unroll
+  for (int gg = 0; gg < G; ++gg) {
+    float M = -INFINITY;
+    for (int s = lane; s < ns; s += 32) M = fmaxf(M, __ldcg(p.ws_ml + x.y + (size_t)s * G + gg).x);
+#pragma unroll
+    for (int o2 = 16; o2 >= 1; o2 >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o2));
+    // lane (c, hf): dims [8c, 8c+8) over pieces hf, hf+2, ...
+    float L = 0.f, acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+#pragma unroll 2
+    for (int s = hf; s < ns; s += 2) {
+      const size_t slot = (size_t)x.y + (size_t)s * G + gg;
+      const float2 ml = __ldcg(p.ws_ml + slot);
+      const float4* src = reinterpret_cast<const float4*>(p.ws_o + slot * kD + c * 8);
+      const float4 a = __ldcg(src), b = __ldcg(src + 1);
+      const float wgt = ml.y > 0.f ? exp2f(ml.x - M) : 0.f;
+      L += ml.y * wgt;
+      acc[0] += a.x * wgt;
+      acc[1] += a.y * wgt;
+      acc[2] += a.z * wgt;
+      acc[3] += a.w * wgt;
+      acc[4] += b.x * wgt;
+      acc[5] += b.y * wgt;
+      acc[6] += b.z * wgt;
+      acc[7] += b.w * wgt;
     }
-    last = __shfl_sync(0xffffffffu, last, 0);
-    if (last) {
-      // lane (c, hf): dims [8c, 8c+8) over splits hf, hf+2, ...
+    L += __shfl_xor_sync(0xffffffffu, L, 16);
 #pragma unroll
-      for (int gg = 0; gg < G; ++gg) {
-        const int hq = head * G + gg;
-        float M = -INFINITY;
-        for (int s = hf; s < ns; s += 2) M = fmaxf(M, __ldcg(p.ws_ml + pb + (size_t)s * g.Hq + hq).x);
-        M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, 16));
-        float L = 0.f, acc[8];
+    for (int j = 0; j < 8; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], 16);
+    if (hf == 0) {
+      const float inv = L > 0.f ? 1.f / L : 0.f;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] = 0.f;
-        for (int s = hf; s < ns; s += 2) {
-          const size_t slot = (size_t)pb + (size_t)s * g.Hq + hq;
-          const float2 ml = __ldcg(p.ws_ml + slot);
-          const float wgt = ml.y > 0.f ? exp2f(ml.x - M) : 0.f;
-          L += ml.y * wgt;
-          const float4* src = reinterpret_cast<const float4*>(p.ws_o + slot * kD + c * 8);
-          const float4 a = __ldcg(src), b = __ldcg(src + 1);
-          acc[0] += a.x * wgt;
-          acc[1] += a.y * wgt;
-          acc[2] += a.z * wgt;
-          acc[3] += a.w * wgt;
-          acc[4] += b.x * wgt;
-          acc[5] += b.y * wgt;
-          acc[6] += b.z * wgt;
-          acc[7] += b.w * wgt;
-        }
-        L += __shfl_xor_sync(0xffffffffu, L, 16);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], 16);
-        if (hf == 0) {
-          const float inv = L > 0.f ? 1.f / L : 0.f;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) acc[j] *= inv;
-          T* op = reinterpret_cast<T*>(g.out) + ((size_t)rl * g.Hq + hq) * kD + c * 8;
-          *reinterpret_cast<uint4*>(op) = Cvt<T>::from_f32(acc);
-        }
-      }
-      if (lane == 0) p.arrive[pb + head] = 0;  // ready for the next launch
+      for (int j = 0; j < 8; ++j) acc[j] *= inv;
+      T* op = reinterpret_cast<T*>(g.out) + ((size_t)rl * g.Hq + head * G + gg) * kD + c * 8;
+      *reinterpret_cast<uint4*>(op) = Cvt<T>::from_f32(acc);
     }
   }
+  if (lane == 0) p.arrive[x.w] = 0;  // ready for the launch after next (same counter set)
 }
 
 template <typename T, int MAXG>
 __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const __grid_constant__ DataParams p) {
   extern __shared__ __align__(128) char smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const unsigned long long t_start = p.trace ? global_ns() : 0ull;
+  unsigned long long t_wait = 0ull;
+  int n_done = 0;
   WarpCtx w;
   w.tiles = smem + wid * kStages * kTile;
   w.bars = reinterpret_cast<uint64_t*>(smem + kWarps * kStages * kTile) + wid * kStages;
@@ -462,6 +470,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const __grid_con
     fill(p, P, w);
   }
   pdl_wait();
+  if (p.trace) t_wait = global_ns();
   // the next launch may queue its CTAs now (they become resident as this grid's CTAs exit)
   pdl_trigger();
   if (!p.prefetch) w.n_items = *p.n_items;
@@ -474,12 +483,20 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const __grid_con
     }
     const int idx = w.ring[P.popped % kRing];
     P.popped++;
+    ++n_done;
     const int4 it = p.items[idx];
     const int G = p.g[it.y >> 16].G;
-    if (G == 1) process_item<T, 1>(p, P, w, it);
-    else if (MAXG >= 2 && G == 2) process_item<T, (MAXG >= 2 ? 2 : 1)>(p, P, w, it);
-    else if (MAXG >= 4 && G == 4) process_item<T, (MAXG >= 4 ? 4 : 1)>(p, P, w, it);
-    else if (MAXG >= 8 && G == 8) process_item<T, (MAXG >= 8 ? 8 : 1)>(p, P, w, it);
+    if (G == 1) process_item<T, 1>(p, P, w, it, idx);
+    else if (MAXG >= 2 && G == 2) process_item<T, (MAXG >= 2 ? 2 : 1)>(p, P, w, it, idx);
+    else if (MAXG >= 4 && G == 4) process_item<T, (MAXG >= 4 ? 4 : 1)>(p, P, w, it, idx);
+    else if (MAXG >= 8 && G == 8) process_item<T, (MAXG >= 8 ? 8 : 1)>(p, P, w, it, idx);
+  }
+  if (p.trace && lane == 0) {
+    unsigned long long* t = p.trace + ((size_t)blockIdx.x * kWarps + wid) * 4;
+    t[0] = t_start;
+    t[1] = t_wait;
+    t[2] = global_ns();
+    t[3] = ((unsigned long long)P.consumed << 32) | (unsigned)n_done;
   }
   // the last CTA to finish resets the work counter for the next launch (no memset node)
   __syncthreads();
@@ -493,14 +510,43 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const __grid_con
   }
 }
 
-// Work list: one item per (request, split, kv head); partial slots for split requests.
+// Work list for the dynamically scheduled decode.  A (request, kv head) of nt K/V
+// tiles is one piece, or — for the last n_cut (request, kv head)s of the batch — a
+// leading part plus two trailing pieces of ~3/16 and ~1/16 of a base piece.  The list
+// holds all leading pieces, then all middle ones, then all small ones; warps fetch in
+// list order, so the launch ends on small pieces: its tail (warps idling while others
+// finish) stays short even though per-warp HBM bandwidth is uneven, while the piece
+// count (per-piece q loads, partial writes, merges) grows only by ~2*n_cut.  Leading
+// parts longer than split_tokens are cut further into balanced chunks.  Pieces of a cut
+// (request, kv head) are merged in-kernel by the piece that finishes last.
+struct PieceShape {
+  int s1, s2, s3;  // leading / middle / small tiles
+  int k1, c1;      // leading chunks and their size
+  int ns;          // pieces
+};
+__device__ __forceinline__ PieceShape piece_shape(int nt, int maxt, bool cut) {
+  PieceShape q;
+  const int base = min(nt, maxt);
+  if (cut && nt >= 4) {
+    q.s3 = max(1, base / 16);
+    q.s2 = max(1, (3 * base) / 16);
+  } else {
+    q.s2 = q.s3 = 0;
+  }
+  q.s1 = nt - q.s2 - q.s3;
+  q.k1 = q.s1 > 0 ? (q.s1 + maxt - 1) / maxt : 1;  // empty context: one (empty) piece -> zeros
+  q.c1 = q.s1 > 0 ? (q.s1 + q.k1 - 1) / q.k1 : 0;
+  q.ns = q.k1 + (q.s2 > 0) + (q.s3 > 0);
+  return q;
+}
+
 __global__ void __launch_bounds__(1024) plan_kernel(DataParams p) {
   __shared__ int sm_warp[33];
-  __shared__ int carry_items, carry_slots;
+  __shared__ int carry[5];  // (request, kv head)s, leading, middle, small pieces, partial slots
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   pdl_wait();  // the previous decode may still be reading the work list
   pdl_trigger();
-  if (tid == 0) carry_items = carry_slots = 0;
+  if (tid < 5) carry[tid] = 0;
   __syncthreads();
   auto scan = [&](int v, int* total) {
     int incl = v;
@@ -528,42 +574,92 @@ __global__ void __launch_bounds__(1024) plan_kernel(DataParams p) {
     __syncthreads();
     return ex;
   };
-  for (int r0 = 0; r0 < p.nreq; r0 += 1024) {
+  // Every group is planned (the plan is reused across layers); pieces of groups inactive
+  // at a layer are skipped when fetched.
+  const int n = p.nreq, maxt = max(1, p.split_tokens / kTpb);
+  int* rh_off = p.rscr;           // (request, kv head) offset of request r
+  int* o1 = p.rscr + n;           // leading-piece offset
+  int* o2 = p.rscr + 2 * n;       // middle-piece offset
+  int* o3 = p.rscr + 3 * n;       // small-piece offset
+  int* os = p.rscr + 4 * n;       // partial-slot offset
+  // pass 0: (request, kv head) offsets
+  for (int r0 = 0; r0 < n; r0 += 1024) {
     const int r = r0 + tid;
-    const bool valid = r < p.nreq;
-    int ctx = 0, ns = 1, hkv = 0, hq = 0, grp = 0;
-    if (valid) {
-      grp = p.req_group[r];
-      ctx = p.req_tokens[p.handles[r]];
-      ns = ctx <= 0 ? 1 : (ctx + p.split_tokens - 1) / p.split_tokens;
-      hkv = p.g[grp].Hkv;
-      hq = p.g[grp].Hq;
+    int t;
+    const int e = scan(r < n ? p.g[p.req_group[r]].Hkv : 0, &t);
+    if (r < n) rh_off[r] = carry[0] + e;
+    __syncthreads();
+    if (tid == 0) carry[0] += t;
+    __syncthreads();
+  }
+  const int NRH = carry[0];
+  const int first_cut = NRH - min(NRH, p.n_cut);
+  // pass A: piece and slot offsets per request
+  for (int r0 = 0; r0 < n; r0 += 1024) {
+    const int r = r0 + tid;
+    int v1 = 0, v2 = 0, v3 = 0, vs = 0;
+    if (r < n) {
+      const DataGroup& g = p.g[p.req_group[r]];
+      const int nt = (p.req_tokens[p.handles[r]] + kTpb - 1) / kTpb;
+      const int nc = min(g.Hkv, max(0, rh_off[r] + g.Hkv - first_cut));  // its last nc heads are cut
+      const PieceShape u = piece_shape(nt, maxt, false), c = piece_shape(nt, maxt, true);
+      v1 = (g.Hkv - nc) * u.k1 + nc * c.k1;
+      v2 = c.s2 > 0 ? nc : 0;
+      v3 = c.s3 > 0 ? nc : 0;
+      vs = (u.ns > 1 ? (g.Hkv - nc) * u.ns : 0) * g.G + (c.ns > 1 ? nc * c.ns : 0) * g.G;
     }
-    int ti, ts;
-    const int ex_i = scan(valid ? ns * hkv : 0, &ti);
-    const int ex_s = scan(valid && ns > 1 ? ns * hq : 0, &ts);
-    if (valid) {
-      // balanced splits: ns = ceil(ctx / split_tokens) pieces of round_up(ceil(ctx / ns), tpb)
-      // tokens (<= split_tokens, and every piece non-empty)
-      const int rs = ns > 1 ? ((ctx + ns - 1) / ns + kTpb - 1) / kTpb * kTpb : max(ctx, 1);
-      p.nsplit[r] = ns;
-      p.rsplit[r] = rs;
-      p.pbase[r] = carry_slots + ex_s;
-      int4* dst = p.items + carry_items + ex_i;
-      for (int s = 0; s < ns; ++s) {
-        const int tb = s * rs, te = min(ctx, tb + rs);
-        for (int h = 0; h < hkv; ++h) dst[s * hkv + h] = make_int4(r, (grp << 16) | h, tb, te);
-      }
+    int t1, t2, t3, ts;
+    const int e1 = scan(v1, &t1), e2 = scan(v2, &t2), e3 = scan(v3, &t3), es = scan(vs, &ts);
+    if (r < n) {
+      o1[r] = carry[1] + e1;
+      o2[r] = carry[2] + e2;
+      o3[r] = carry[3] + e3;
+      os[r] = carry[4] + es;
     }
     __syncthreads();
     if (tid == 0) {
-      carry_items += ti;
-      carry_slots += ts;
+      carry[1] += t1;
+      carry[2] += t2;
+      carry[3] += t3;
+      carry[4] += ts;
     }
     __syncthreads();
   }
+  const int N1 = carry[1], N2 = carry[2];
+  // pass B: one warp per request, lanes over its kv heads
+  for (int r = wid; r < n; r += 32) {
+    const int grp = p.req_group[r];
+    const DataGroup& g = p.g[grp];
+    const int ctx = p.req_tokens[p.handles[r]];
+    const int nt = (ctx + kTpb - 1) / kTpb;
+    const int nc = min(g.Hkv, max(0, rh_off[r] + g.Hkv - first_cut));
+    const int hcut = g.Hkv - nc;  // heads >= hcut are cut
+    const PieceShape u = piece_shape(nt, maxt, false), c = piece_shape(nt, maxt, true);
+    for (int h = lane; h < g.Hkv; h += 32) {
+      const bool cut = h >= hcut;
+      const PieceShape& q = cut ? c : u;
+      const int i1 = o1[r] + (cut ? hcut * u.k1 + (h - hcut) * c.k1 : h * u.k1);  // also the arrival index
+      const int sb = os[r] + (cut ? (u.ns > 1 ? hcut * u.ns : 0) + (h - hcut) * c.ns : h * u.ns) * g.G;
+      const int hy = (grp << 16) | h;
+      for (int j = 0; j < q.k1; ++j) {
+        const int tb = j * q.c1, te = min(q.s1, tb + q.c1);
+        p.items[i1 + j] = make_int4(r, hy, tb * kTpb, min(ctx, te * kTpb));
+        p.itemx[i1 + j] = make_int4(q.ns, sb, j, i1);
+      }
+      if (q.s2 > 0) {
+        const int i = N1 + o2[r] + (h - hcut);
+        p.items[i] = make_int4(r, hy, q.s1 * kTpb, min(ctx, (q.s1 + q.s2) * kTpb));
+        p.itemx[i] = make_int4(q.ns, sb, q.k1, i1);
+      }
+      if (q.s3 > 0) {
+        const int i = N1 + N2 + o3[r] + (h - hcut);
+        p.items[i] = make_int4(r, hy, (q.s1 + q.s2) * kTpb, ctx);
+        p.itemx[i] = make_int4(q.ns, sb, q.k1 + (q.s2 > 0), i1);
+      }
+    }
+  }
   if (tid == 0) {
-    *p.n_items = carry_items;
+    *p.n_items = N1 + N2 + carry[3];
     p.counter[0] = 0;  // this launch's counter set (each decode launch also self-resets its set)
     p.counter[1] = 0;
   }

@@ -136,20 +136,20 @@ struct skv_batch {
   int nreq = 0;
   // decode plan workspace
   int4* d_items = nullptr;
+  int4* d_itemx = nullptr;
+  int* d_arrive = nullptr;      // [2][items_cap] arrival counters, two alternating sets
   size_t items_cap = 0;
   int* d_nitems = nullptr;
-  int* d_counter = nullptr;
-  int* d_pbase = nullptr;
-  int* d_nsplit = nullptr;
-  int* d_rsplit = nullptr;
-  int* d_arrive = nullptr;     // [slots_cap] split arrivals per (request, kv head)
+  int* d_counter = nullptr;     // [2][2] work counter + finished CTAs, two alternating sets
+  int* d_rscr = nullptr;        // [5 * req_cap] plan scratch
   float* d_ws_o = nullptr;
   float2* d_ws_ml = nullptr;
   size_t slots_cap = 0;
   uint64_t plan_epoch = ~0ull;
   uint64_t launch_seq = 0;
   int plan_split = 0;
-  bool plan_has_split = false;
+  unsigned long long* d_trace = nullptr;  // SKV_TRACE=1: per-warp timing of the last decode
+  size_t trace_n = 0;
 };
 
 namespace {
@@ -249,7 +249,7 @@ skv_status flush(skv_pool* p) {
   if (bytes > p->h_stage_cap) {
     if (p->h_stage) cudaFreeHost(p->h_stage);
     p->h_stage_cap = std::max(bytes * 2, (size_t)1 << 16);
-    SKV_CUDA(p, cudaMallocHost(&p->h_stage, p->h_stage_cap));
+    SKV_CUDA(p, cudaHostAlloc(&p->h_stage, p->h_stage_cap, cudaHostAllocMapped));
   }
   if (bytes > p->d_ops_cap) {
     SKV_CUDA(p, cudaStreamSynchronize(p->stream));
@@ -271,7 +271,8 @@ skv_status flush(skv_pool* p) {
   }
   std::memcpy(p->h_stage, p->grow_ops.data(), gbytes);
   std::memcpy(static_cast<char*>(p->h_stage) + gbytes, p->free_ops.data(), fbytes);
-  SKV_CUDA(p, cudaMemcpyAsync(p->d_ops, p->h_stage, bytes, cudaMemcpyHostToDevice, p->stream));
+  skv::launch_stage_copy(p->d_ops, p->h_stage, bytes, p->stream);  // SM copy, not a copy engine
+  p->launches++;
   const skv::GrowOp* dg = static_cast<const skv::GrowOp*>(p->d_ops);
   const skv::FreeOp* df = reinterpret_cast<const skv::FreeOp*>(static_cast<char*>(p->d_ops) + gbytes);
   size_t kf = 0;
@@ -284,10 +285,10 @@ skv_status flush(skv_pool* p) {
       p->launches += 1;
     } else {
       FreeResult& fresult = p->pending[fr++];
-      skv::launch_free(p->dev, p->prm, df + r.begin, n, p->d_outE + fresult.slot * p->M, p->stream);
+      // emptied-block counts are written by the kernel straight into pinned host memory
+      // (no copy-engine D2H that could queue behind a caller's bulk copies)
+      skv::launch_free(p->dev, p->prm, df + r.begin, n, p->h_outE + fresult.slot * p->M, p->stream);
       p->launches += 2;
-      SKV_CUDA(p, cudaMemcpyAsync(p->h_outE + fresult.slot * p->M, p->d_outE + fresult.slot * p->M,
-                                  sizeof(int32_t) * p->M, cudaMemcpyDeviceToHost, p->stream));
       if (!fresult.ev) SKV_CUDA(p, cudaEventCreateWithFlags(&fresult.ev, cudaEventDisableTiming));
       SKV_CUDA(p, cudaEventRecord(fresult.ev, p->stream));
     }
@@ -638,7 +639,7 @@ skv_status skv_pool_create(const skv_model_desc* models, int32_t n, int32_t tpb,
         cudaStreamSynchronize(p->stream) != cudaSuccess)
       return bail(fail(p, SKV_ERR_CUDA, "init copy failed"));
   }
-  if (cudaMallocHost(reinterpret_cast<void**>(&p->h_outE), sizeof(int32_t) * kResultSlots * n) != cudaSuccess)
+  if (cudaHostAlloc(reinterpret_cast<void**>(&p->h_outE), sizeof(int32_t) * kResultSlots * n, cudaHostAllocMapped) != cudaSuccess)
     return bail(fail(p, SKV_ERR_CUDA, "cudaMallocHost failed"));
   if (p->allocate_storage && (st = ensure_storage(p))) return bail(st);
   if (cudaStreamSynchronize(p->stream) != cudaSuccess) return bail(fail(p, SKV_ERR_CUDA, "init sync failed"));
@@ -878,17 +879,15 @@ static skv_status batch_fill(skv_pool* p, skv_batch* b, const int32_t* group_mod
   DeviceGuard guard(p->device);
   if ((size_t)total > b->req_cap) {
     SKV_CUDA(p, cudaStreamSynchronize(p->stream));
-    for (void* q : {(void*)b->d_handles, (void*)b->d_group, (void*)b->d_pbase, (void*)b->d_nsplit,
-                    (void*)b->d_rsplit})
+    for (void* q : {(void*)b->d_handles, (void*)b->d_group, (void*)b->d_rscr})
       if (q) cudaFree(q);
     b->req_cap = std::max<size_t>((size_t)total * 2, 64);
     skv_status st;
     if ((st = dev_alloc(p, &b->d_handles, b->req_cap, false)) || (st = dev_alloc(p, &b->d_group, b->req_cap, false)) ||
-        (st = dev_alloc(p, &b->d_pbase, b->req_cap)) || (st = dev_alloc(p, &b->d_nsplit, b->req_cap)) ||
-        (st = dev_alloc(p, &b->d_rsplit, b->req_cap)))
+        (st = dev_alloc(p, &b->d_rscr, 5 * b->req_cap)))
       return st;
     if (b->h_stage) cudaFreeHost(b->h_stage);
-    SKV_CUDA(p, cudaMallocHost(&b->h_stage, b->req_cap * 2 * sizeof(int32_t)));
+    SKV_CUDA(p, cudaHostAlloc(&b->h_stage, b->req_cap * 2 * sizeof(int32_t), cudaHostAllocMapped));
   }
   if (!b->d_nitems) {
     skv_status st;
@@ -900,8 +899,8 @@ static skv_status batch_fill(skv_pool* p, skv_batch* b, const int32_t* group_mod
     int32_t* hs = static_cast<int32_t*>(b->h_stage);
     std::memcpy(hs, b->handles.data(), total * 4);
     std::memcpy(hs + b->req_cap, b->h_group.data(), total * 4);
-    SKV_CUDA(p, cudaMemcpyAsync(b->d_handles, hs, total * 4, cudaMemcpyHostToDevice, p->stream));
-    SKV_CUDA(p, cudaMemcpyAsync(b->d_group, hs + b->req_cap, total * 4, cudaMemcpyHostToDevice, p->stream));
+    skv::launch_stage_copy(b->d_handles, hs, total * 4, p->stream);  // SM copies (see flush)
+    skv::launch_stage_copy(b->d_group, hs + b->req_cap, total * 4, p->stream);
     if (!b->stage_ev) SKV_CUDA(p, cudaEventCreateWithFlags(&b->stage_ev, cudaEventDisableTiming));
     SKV_CUDA(p, cudaEventRecord(b->stage_ev, p->stream));
   }
@@ -933,9 +932,9 @@ void skv_batch_destroy(skv_batch* b) {
   if (!b) return;
   DeviceGuard g(b->pool->device);
   cudaStreamSynchronize(b->pool->stream);
-  for (void* q : {(void*)b->d_handles, (void*)b->d_group, (void*)b->d_items, (void*)b->d_nitems,
-                  (void*)b->d_counter, (void*)b->d_pbase, (void*)b->d_nsplit, (void*)b->d_rsplit,
-                  (void*)b->d_arrive, (void*)b->d_ws_o, (void*)b->d_ws_ml})
+  for (void* q : {(void*)b->d_handles, (void*)b->d_group, (void*)b->d_items, (void*)b->d_itemx,
+                  (void*)b->d_nitems, (void*)b->d_counter, (void*)b->d_rscr, (void*)b->d_arrive,
+                  (void*)b->d_ws_o, (void*)b->d_ws_ml, (void*)b->d_trace})
     if (q) cudaFree(q);
   if (b->h_stage) cudaFreeHost(b->h_stage);
   if (b->stage_ev) cudaEventDestroy(b->stage_ev);
@@ -1074,52 +1073,64 @@ skv_status skv_decode_attention(skv_pool* p, skv_batch* b, const skv_decode_args
   }
   const float scale = a->softmax_scale > 0.f ? a->softmax_scale : 1.0f / std::sqrt(128.0f);
   dp.scale_log2 = scale * 1.4426950408889634f;
-  // split-KV only when the unsplit (request, kv head) items cannot keep every warp slot
-  // busy for ~1.5 rounds (measured: at config 1, 1.95 rounds unsplit beats any split);
-  // then enough balanced splits to cover the slots ~4 times
+  // Work list (plan_kernel): the last n_cut (request, kv head)s get two small trailing
+  // pieces (4 per warp slot: enough small work to even out the launch's tail); leading
+  // parts are cut to <= split tokens only when there are too few (request, kv head)s to
+  // keep every warp slot busy (~4 pieces per slot).
+  int nsm = 148;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p->device);
+  const long long slots8 = (long long)nsm * 8 * skv::decode_ctas_per_sm();
   int split = a->split_tokens;
-  if (split <= 0) {
-    int nsm = 148;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p->device);
-    const long long slots8 = (long long)nsm * 8, target = 4LL * slots8;
-    if (2 * sum_hkv >= 3 * slots8 || max_ctx <= 256)
-      split = (int)std::max<long long>(round_up(std::max(max_ctx, 1LL), 16), 16);
-    else split = (int)std::max<long long>(256, round_up(ceil_div_ll(work, target), 16));
+  if (split < 0) return fail(p, SKV_ERR_ARG, "decode: split_tokens must be >= 0");
+  // Measured on B200 (scripts/sweep_sched.sh, profiles/r01_sweep_sched.txt): chunk when
+  // there are fewer than 1.5 (request, kv head)s per warp slot; give trailing pieces to
+  // W/2 (request, kv head)s when pieces are short (< 64 tiles: per-piece overhead
+  // dominates), else to 2W.  SKV_CHUNK_X4 / SKV_NCUT_X4 override both (in quarters of W).
+  static const long long chunk_x4 = [] {
+    const char* e = getenv("SKV_CHUNK_X4");
+    return e ? atoll(e) : 6LL;
+  }();
+  static const long long ncut_x4 = [] {
+    const char* e = getenv("SKV_NCUT_X4");
+    return e ? atoll(e) : -1LL;
+  }();
+  if (split == 0) {
+    if (4 * sum_hkv >= chunk_x4 * slots8 || max_ctx <= 256) split = 1 << 30;
+    else split = (int)std::max<long long>(256, round_up(ceil_div_ll(work, 4 * slots8), 16));
   }
-  split = (int)round_up(split, 16);
+  split = (int)std::min<long long>(round_up(split, 16), 1 << 30);
   dp.split_tokens = split;
-  // capacities
+  const long long piece_tiles = std::min<long long>(ceil_div_ll(work, std::max(1LL, sum_hkv) * 16), split / 16);
+  const long long ncut = ncut_x4 >= 0 ? ncut_x4 * slots8 / 4 : (piece_tiles < 64 ? slots8 / 2 : 2 * slots8);
+  dp.n_cut = (int)std::min<long long>(ncut, sum_hkv);
+  // capacities: an upper bound on pieces and partial slots (every head cut)
   long long items = 0, slots = 0;
-  bool any_split = false;
+  const long long maxt = std::max(1, split / 16);
   for (int g = 0; g < b->ngroups; ++g)
     for (int i = 0; i < b->gsize[g]; ++i) {
-      const long long ctx = p->req[b->handles[b->gbegin[g] + i]].tokens;
-      const long long ns = ctx <= 0 ? 1 : ceil_div_ll(ctx, split);
+      const long long nt = ceil_div_ll(std::max<long long>(p->req[b->handles[b->gbegin[g] + i]].tokens, 0), 16);
+      const long long k1 = nt > 0 ? ceil_div_ll(nt, maxt) : 1;
+      const long long ns = k1 + 2;
       items += ns * dp.g[g].Hkv;
-      if (ns > 1) {
-        slots += ns * dp.g[g].Hq;
-        any_split = true;
-      }
+      slots += ns * dp.g[g].G * dp.g[g].Hkv;
     }
   if ((size_t)items > b->items_cap) {
-    if (b->d_items) {
-      SKV_CUDA(p, cudaStreamSynchronize(s));
-      cudaFree(b->d_items);
-    }
+    SKV_CUDA(p, cudaStreamSynchronize(s));
+    for (void* q : {(void*)b->d_items, (void*)b->d_itemx, (void*)b->d_arrive})
+      if (q) cudaFree(q);
     b->items_cap = (size_t)items * 2;
     SKV_CUDA(p, cudaMalloc(&b->d_items, b->items_cap * sizeof(int4)));
+    SKV_CUDA(p, cudaMalloc(&b->d_itemx, b->items_cap * sizeof(int4)));
+    if ((st = dev_alloc(p, &b->d_arrive, 2 * b->items_cap))) return st;
     b->plan_epoch = ~0ull;
   }
   if ((size_t)slots > b->slots_cap) {
     SKV_CUDA(p, cudaStreamSynchronize(s));
     if (b->d_ws_o) cudaFree(b->d_ws_o);
     if (b->d_ws_ml) cudaFree(b->d_ws_ml);
-    if (b->d_arrive) cudaFree(b->d_arrive);
     b->slots_cap = (size_t)slots * 2;
-    if ((st = dev_alloc(p, &b->d_arrive, 2 * b->slots_cap))) return st;
     SKV_CUDA(p, cudaMalloc(&b->d_ws_o, b->slots_cap * 128 * sizeof(float)));
     SKV_CUDA(p, cudaMalloc(&b->d_ws_ml, b->slots_cap * sizeof(float2)));
-    b->plan_epoch = ~0ull;
   }
   dp.items = b->d_items;
   dp.n_items = b->d_nitems;
@@ -1128,10 +1139,9 @@ skv_status skv_decode_attention(skv_pool* p, skv_batch* b, const skv_decode_args
   // while this one drains, and each launch's last CTA / last split resets its own set.
   const int parity = (int)(b->launch_seq++ & 1);
   dp.counter = b->d_counter + 2 * parity;
-  dp.pbase = b->d_pbase;
-  dp.nsplit = b->d_nsplit;
-  dp.rsplit = b->d_rsplit;
-  dp.arrive = b->d_arrive + parity * b->slots_cap;
+  dp.itemx = b->d_itemx;
+  dp.rscr = b->d_rscr;
+  dp.arrive = b->d_arrive + parity * b->items_cap;
   dp.ws_o = b->d_ws_o;
   dp.ws_ml = b->d_ws_ml;
   if ((st = order_streams(p, s))) return st;
@@ -1141,7 +1151,6 @@ skv_status skv_decode_attention(skv_pool* p, skv_batch* b, const skv_decode_args
     p->launches++;
     b->plan_epoch = p->token_epoch;
     b->plan_split = split;
-    b->plan_has_split = any_split;
     planned = true;
   }
   // K/V tiles may be prefetched before the previous launch completes only when nothing
@@ -1153,6 +1162,18 @@ skv_status skv_decode_attention(skv_pool* p, skv_batch* b, const skv_decode_args
     return e && e[0] == '1';
   }();
   dp.prefetch = (!planned && dp.n_new == 1 && !no_prefetch) ? 1 : 0;
+  static const bool trace_on = [] {
+    const char* e = getenv("SKV_TRACE");
+    return e && e[0] == '1';
+  }();
+  if (trace_on) {
+    const size_t n = (size_t)slots8;
+    if (!b->d_trace) {
+      SKV_CUDA(p, cudaMalloc(&b->d_trace, n * 4 * sizeof(unsigned long long)));
+      b->trace_n = n;
+    }
+    dp.trace = b->d_trace;
+  }
   // split partials are merged inside the decode kernel; its work counter self-resets
   skv::launch_decode(dp, maxg, 0, s);
   p->launches++;
@@ -1257,3 +1278,15 @@ skv_status skv_read_blocks(skv_pool* p, const int32_t* ids, size_t n, void* dst)
 uint64_t skv_kernel_launches(const skv_pool* p) { return p->launches; }
 
 }  // extern "C"
+
+skv_status skv_debug_decode_trace(skv_pool* p, skv_batch* b, uint64_t* host, size_t cap, size_t* n) {
+  *n = 0;
+  if (!b || b->pool != p) return fail(p, SKV_ERR_ARG, "batch belongs to another pool");
+  if (!b->d_trace) return SKV_OK;
+  DeviceGuard guard(p->device);
+  SKV_CUDA(p, cudaDeviceSynchronize());
+  const size_t m = std::min(cap / 4, b->trace_n);
+  SKV_CUDA(p, cudaMemcpy(host, b->d_trace, m * 4 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  *n = m;
+  return SKV_OK;
+}

@@ -63,6 +63,7 @@ struct GrowScratch {
   long long* out_E;  // [M] (free runs) host-visible copy of emptied-block counts
 };
 
+void launch_stage_copy(void* dst, const void* src_host_mapped, size_t bytes, cudaStream_t s);
 void launch_grow(const DevAlloc& st, const AllocParams& pr, const GrowOp* ops, int n,
                  const GrowScratch& sc, cudaStream_t s);
 void launch_free(const DevAlloc& st, const AllocParams& pr, const FreeOp* ops, int n,
@@ -99,17 +100,19 @@ struct DataParams {
   long long merged_stride;
   int head_dim, tpb, dtype;
   float scale_log2;          // softmax scale * log2(e)
-  int split_tokens;          // tokens per split (multiple of tpb)
+  int split_tokens;          // decode: max tokens of a phase-1 piece (multiple of tpb)
+  int n_cut;                 // decode: (request, kv head)s given trailing pieces (the last ones)
   int n_new;                 // append / prefill tokens per request
   // decode plan
-  int4* items;               // [max_items] {req, (group<<16)|kv_head, tok_begin, tok_end}
+  int4* items;               // [max_items] {req, (group<<16)|kv_head, tok_begin, tok_end}, by phase
   int* n_items;
   int* counter;              // [2] dynamic work counter, finished-CTA count (both self-resetting)
   int prefetch;              // 1: K/V loads may be issued before the PDL wait (see skv_capi.cpp)
-  int* pbase;                // [nreq] partial-slot base (split requests)
-  int* nsplit;               // [nreq]
-  int* rsplit;               // [nreq] tokens per split of the request (balanced, multiple of tpb)
-  int* arrive;               // [slots] per (request, kv head) split arrivals (self-resetting)
+  int4* itemx;               // [max_items] {pieces of the (request, kv head), partial-slot base,
+                             //  piece index, arrival counter index}
+  int* rscr;                 // [5*nreq] plan scratch
+  int* arrive;               // [items] pieces finished per (request, kv head) (self-resetting)
+  unsigned long long* trace; // debug (SKV_TRACE=1): per warp {start, after wait, end, tiles<<32|items} ns
   float* ws_o;               // [slots][D] unnormalised partial outputs
   float2* ws_ml;             // [slots] (running max (log2 domain), sum)
 };

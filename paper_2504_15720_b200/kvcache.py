@@ -190,6 +190,7 @@ def lib() -> C.CDLL:
         "skv_synth_fill": (S, [P, C.c_uint64, C.c_float, P]),
         "skv_read_blocks": (S, [P, P, C.c_size_t, P]),
         "skv_kernel_launches": (C.c_uint64, [P]),
+        "skv_debug_decode_trace": (S, [P, P, P, C.c_size_t, C.POINTER(C.c_size_t)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -500,6 +501,15 @@ class Batch:
             a.v = C.cast(va, C.POINTER(C.c_void_p))
         self.cache._chk(self.cache._lib.skv_decode_attention(self.cache._h, self._h, C.byref(a),
                                                              _stream_ptr(stream)))
+
+    def decode_trace(self) -> np.ndarray:
+        """Debug (SKV_TRACE=1): per-warp [start_ns, after_wait_ns, end_ns, tiles<<32|items]
+        of the last decode launch; empty when tracing is off."""
+        buf = np.zeros((4096, 4), dtype=np.uint64)
+        n = C.c_size_t()
+        self.cache._chk(self.cache._lib.skv_debug_decode_trace(self.cache._h, self._h, buf.ctypes.data,
+                                                               buf.size, C.byref(n)))
+        return buf[: n.value]
 
     def append(self, k: Sequence, v: Sequence, layer: int, n_new: int = 1, stream=None):
         n = len(self.groups)
