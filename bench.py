@@ -583,6 +583,157 @@ def run_churn(args):
     print(json.dumps(res), flush=True)
 
 
+SHAPES_C5 = {  # reference model id -> (layers, kv heads, q heads); 70B keeps the reference's 64 KV heads (Q7)
+    "llama2-70b": (80, 64, 64), "llama2-7b": (32, 32, 32), "llama2-13b": (40, 40, 40),
+    "opt-6.7b": (32, 32, 32), "llama3-8b": (32, 8, 32),
+}
+
+
+def run_config5(args):
+    """Config 5: 16 services (one 70B shape + 15 mixed) placed on N GPUs by the reference
+    placement (placement.dedicated_plan with the SURVEY §8e overrides).  Each process (one
+    GPU) owns one sharing group's unified pool at the group's TP size; per layer ONE decode
+    launch covers every service of the group.  A head-sharded (tp > 1) group also projects
+    the 70B service's partial attention output through its W_o row slice and sums it over
+    the group with NCCL AllReduce -- the only collective of the data path.  Total work is
+    fixed as N grows (strong scaling)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2504_15720_b200 as P
+    from paper_2504_15720_b200 import placement as PL
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # SKV_BENCH_SHARE_GPU=1: every rank on GPU 0 (functional test of the N-rank path on a
+    # 1-GPU box; use SKV_BENCH_BACKEND=gloo then)
+    dev = 0 if os.environ.get("SKV_BENCH_SHARE_GPU") == "1" else local
+    torch.cuda.set_device(dev)
+    backend = os.environ.get("SKV_BENCH_BACKEND", "nccl")
+    if world > 1:
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
+    services = PL.config5_services()
+    plan = PL.dedicated_plan(services, PL.config5_overrides(world))
+    assert plan.feasible, f"config5 placement infeasible on {world} GPUs: unplaced {plan.unplaced}"
+    tp_groups = {}
+    for gi, g in enumerate(plan.groups):  # every rank creates every subgroup, same order
+        if world > 1 and g.tp_size > 1:
+            tp_groups[gi] = dist.new_group(g.gpu_ids)
+    role = PL.rank_role(plan, rank)
+    nreq = args.requests or 16
+    ctx = args.ctx or 2048
+    grow = args.warmup * 2 + args.steps * 2 + 8
+    kv_total = 0.0
+    elapsed_ms = 0.0
+    ar_ms = 0.0
+    n_ar = 0
+    launches = 0
+    if role is not None:
+        g = role.group
+        tp = g.tp_size
+        names = [services[s] for s in role.services]
+        models = [P.ModelSpec(f"{n}#{s}", SHAPES_C5[n][0], SHAPES_C5[n][1], 128, 2, SHAPES_C5[n][2])
+                  for n, s in zip(names, role.services)]
+        merged = P.plan_merged_shape(models, 16, tp)
+        subs = [int(merged // P.native_block_bytes(m, 16, tp)) for m in models]
+        pool = sum(-(-nreq * ((ctx + grow + 15) // 16) // sb) for sb in subs) + 64
+        cache = P.UnifiedKvCache(models, 16, tp, pool, device=dev, dtype=P.FP16, phys_layers=args.phys_layers,
+                                 max_requests=nreq * len(models) + 16,
+                                 max_blocks_per_request=(ctx + grow + 15) // 16 + 1, allocate_storage=True)
+        groups = [(m, []) for m in range(len(models))]
+        ops, rid = [], 1
+        for r in range(nreq):
+            for m in range(len(models)):
+                ops.append((0, rid, m, ctx))
+                groups[m][1].append(rid)
+                rid += 1
+        assert cache.replay(ops).all(), "pool too small"
+        stream = torch.cuda.Stream(device=dev)
+        torch.cuda.set_stream(stream)
+        cache.set_stream(stream)
+        cache.synth_fill(5 + role.group_index, 1.0, stream)
+        batch = cache.batch(groups)
+        gen = torch.Generator(device=dev).manual_seed(1)
+        shp = [SHAPES_C5[n] for n in names]
+        q = [torch.randn((nreq, Hq // tp, 128), generator=gen, device=dev).half() for _, _, Hq in shp]
+        out = [torch.empty_like(x) for x in q]
+        k = [torch.randn((nreq, 1, H // tp, 128), generator=gen, device=dev).half() * 0.5 for _, H, _ in shp]
+        v = [torch.randn((nreq, 1, H // tp, 128), generator=gen, device=dev).half() * 0.5 for _, H, _ in shp]
+        big = [i for i, n in enumerate(names) if n == "llama2-70b"]
+        hidden = 8192
+        w_o = (torch.randn((64 // tp * 128, hidden), generator=gen, device=dev) / 90).half() if big else None
+        y = torch.empty((nreq, hidden), device=dev, dtype=torch.float16) if big else None
+        pg = tp_groups.get(role.group_index)
+        nl = max(L for L, _, _ in shp)
+        ev_ar = []
+
+        def step(timed):
+            batch.grow(1)
+            for layer in range(nl):
+                batch.decode(q, out, layer, stream=stream, k=k, v=v)
+                if big and layer < shp[big[0]][0]:
+                    torch.matmul(out[big[0]].view(nreq, -1), w_o, out=y)  # partial row-parallel output
+                    if pg is not None:
+                        e = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                        e[0].record(stream)
+                        dist.all_reduce(y, op=dist.ReduceOp.SUM, group=pg)
+                        e[1].record(stream)
+                        if timed:
+                            ev_ar.append(e)
+
+        for _ in range(args.warmup):
+            step(False)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        l0 = cache.kernel_launches()
+        t0.record(stream)
+        for _ in range(args.steps):
+            step(True)
+            kv_total += step_bytes(batch, nl)[0]
+        t1.record(stream)
+        torch.cuda.synchronize()
+        launches = cache.kernel_launches() - l0
+        elapsed_ms = t0.elapsed_time(t1)
+        ar_ms = sum(a.elapsed_time(b) for a, b in ev_ar)
+        n_ar = len(ev_ar)
+    if world > 1:
+        dist.barrier()
+        t = torch.tensor([elapsed_ms, kv_total, float(launches)], dtype=torch.float64,
+                         device=dev if backend == "nccl" else "cpu")
+        mx = t.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        elapsed_ms, kv_all, launches = float(mx[0]), float(t[1]), int(t[2])
+    else:
+        kv_all = kv_total
+    if rank == 0:
+        hbm, peak_kind = peaks()
+        value = kv_all / (elapsed_ms / 1e3) / 1e9
+        desc = "; ".join(f"group {gi}: gpus {g.gpu_ids} tp{g.tp_size} services "
+                         f"{[services[s] for s in g.services]}" for gi, g in enumerate(plan.groups))
+        print(json.dumps({
+            "metric": "unified-KV paged decode attention HBM GB/s (mixed services)", "value": round(value, 1),
+            "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(elapsed_ms / args.steps, 3), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "fp16", "data": "synthetic",
+            "config": {"workload": f"config5: 16 services (llama2-70b shape head-sharded + 15 mixed), reference "
+                                   f"dedicated_plan with SURVEY 8e overrides; {nreq} decode requests per service at "
+                                   f"ctx {ctx}+; layer-sliced pools ({args.phys_layers} physical layers)",
+                       "placement": desc, "backend": backend},
+            "frac_of_hbm_x_n": round(value / (hbm * world), 4), "peak": hbm, "peak_kind": peak_kind,
+            "allreduce": {"per_layer_ms_rank0": round(ar_ms / max(1, n_ar), 4), "count_rank0": n_ar},
+            "gpu_launches": launches,
+        }), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def run_reference(args):
     """Reference arm: the reference's own CPU path for this workload on the host cores —
     the reference has no attention, so the fp32 oracle port stands in for decode and the
@@ -685,7 +836,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="config2", choices=["config1", "config2", "config3", "config4"])
+    ap.add_argument("--workload", default="config2", choices=["config1", "config2", "config3", "config4", "config5"])
     ap.add_argument("--rate", type=float, default=20.0, help="config3 arrival rate (requests/s)")
     ap.add_argument("--pool-gb", dest="pool_gb", type=float, default=100.0, help="config3 pool size")
     ap.add_argument("--requests", type=int, default=0, help="decode requests per service (0 = workload default)")
@@ -701,6 +852,8 @@ def main():
         run_reference(args)
     elif args.workload == "config3":
         run_churn(args)
+    elif args.workload == "config5":
+        run_config5(args)
     else:
         run_gpu(args)
 

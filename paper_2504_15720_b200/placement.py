@@ -191,5 +191,7 @@ def config5_overrides(n_gpus: int) -> PlacementConfig:
     if n_gpus == 2:
         return PlacementConfig(share_cap=16, gpus_per_node=2, min_tp_override={"llama2-70b": 2},
                                extra_tp_entries={"llama2-70b": {2: (2.0, 0.08)}})
+    # one GPU cannot hold the 16 services' weights (~370 GiB): the 1-GPU point of the
+    # scaling curve is a KV-path-only run (weights not resident), so the memory check is off
     return PlacementConfig(share_cap=16, gpus_per_node=1, min_tp_override={"llama2-70b": 1},
-                           extra_tp_entries={"llama2-70b": {1: (2.8, 0.11)}})
+                           extra_tp_entries={"llama2-70b": {1: (2.8, 0.11)}}, gpu_mem_gib=1e9)

@@ -27,7 +27,7 @@ def test_placement_reproduces_reference_default_outcomes():
     assert (len(p8.groups), len(p8.unplaced)) == (5, 6)
 
 
-@pytest.mark.parametrize("n", [2, 4, 8])
+@pytest.mark.parametrize("n", [1, 2, 4, 8])
 def test_config5_overrides_place_everything(n):
     plan = PL.dedicated_plan(PL.config5_services(), PL.config5_overrides(n))
     assert plan.feasible and not plan.unplaced
