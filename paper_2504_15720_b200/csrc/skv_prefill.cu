@@ -104,6 +104,16 @@ __device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
+// A operand from TMEM (kind::f16, K-major): D[tmem_d] (+)= A[tmem_a] . B[desc_b]
+__device__ __forceinline__ void mma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(bar))
@@ -174,6 +184,18 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float (&v)[32]) 
       "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]),
       "f"(v[17]), "f"(v[18]), "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]),
       "f"(v[25]), "f"(v[26]), "f"(v[27]), "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31]));
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_st32u(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]),
+      "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]),
+      "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31]));
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
@@ -446,13 +468,13 @@ __global__ void __launch_bounds__(kThreads, 2) prefill_kernel(const __grid_const
 // all tcgen05.mma, warps 9-10 stream Q and a 3-stage K/V ring with cp.async signalled
 // through mbarriers.  Tensor-core order: QK_A QK_B | PV_A QK_A' | PV_B QK_B' | ... so the
 // tensor core works on one tile while the other tile's softmax runs on the CUDA cores.
-constexpr int kStagesV3 = 4;
+constexpr int kStagesV3 = 5;  // K/V ring depth (P lives in TMEM, so smem holds only Q and K/V)
 constexpr int kSoftmaxWarps = 8;             // 4 per query tile, one thread per query row
 constexpr int kMmaWarp = kSoftmaxWarps;      // warp 16
 constexpr int kLoadWarp = kSoftmaxWarps + 1; // warp 17
 constexpr int kThreadsV3 = (kSoftmaxWarps + 2) * 32;
 constexpr int kLoadThreads = 32;
-constexpr int kSmemV3 = 2 * kTileBytes + kStagesV3 * 2 * kKVBytes + 2 * kPBytes + 256;
+constexpr int kSmemV3 = 2 * kTileBytes + kStagesV3 * 2 * kKVBytes + 256;
 
 __device__ __forceinline__ void mbar_init_n(uint64_t* b, uint32_t n) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(n));
@@ -480,15 +502,19 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v3(const __grid_
   if (smem_u32(smem) & 1023) __trap();
   char* sQ[2] = {smem, smem + kTileBytes};
   char* kvbase = smem + 2 * kTileBytes;
-  char* sP[2] = {kvbase + kStagesV3 * 2 * kKVBytes, kvbase + kStagesV3 * 2 * kKVBytes + kPBytes};
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP[1] + kPBytes);
-  uint64_t* kv_full = bars;                 // [stages] count 1 (TMA arrive.expect_tx)
-  uint64_t* kv_empty = bars + 4;            // [stages] count 1 (tcgen05.commit after PV_B)
-  uint64_t* q_full = bars + 8;              // count 32 (cp.async arrive.noinc per loader lane)
-  uint64_t* s_full = bars + 9;              // [tile][S buffer] count 1
-  uint64_t* p_full = bars + 13;             // [2] count 128
-  uint64_t* pv_done = bars + 15;            // [2] count 1
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
+  // P(j) is written by the softmax into TMEM over S(j) (fp16/bf16 pairs in the first 32
+  // columns of the S buffer) and read from there by the P.V MMA (A operand in TMEM), so the
+  // softmax never waits for a P buffer: it may run a key tile ahead of the tensor core.
+  uint64_t* bars = reinterpret_cast<uint64_t*>(kvbase + kStagesV3 * 2 * kKVBytes);
+  uint64_t* kv_full = bars;                       // [stages] count 1 (TMA arrive.expect_tx)
+  uint64_t* kv_empty = bars + kStagesV3;          // [stages] count 1 (tcgen05.commit after PV_B)
+  uint64_t* q_full = bars + 2 * kStagesV3;        // count 32 (cp.async arrive.noinc per loader lane)
+  uint64_t* s_full = bars + 2 * kStagesV3 + 1;    // [tile][S buffer] count 1
+  // per (tile, S/P buffer): each completes once per two key tiles and is waited on in
+  // order, so no waiter can fall two phases behind
+  uint64_t* p_full = bars + 2 * kStagesV3 + 5;    // [tile][buffer] count 128
+  uint64_t* pv_done = bars + 2 * kStagesV3 + 9;   // [tile][buffer] count 1
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStagesV3 + 13);
 
   const int r = blockIdx.z, h = blockIdx.y;
   const int grp = p.req_group[r];
@@ -518,7 +544,7 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v3(const __grid_
     }
     mbar_init_n(q_full, kLoadThreads);
     for (int i = 0; i < 4; ++i) mbar_init_n(&s_full[i], 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 4; ++i) {
       mbar_init_n(&p_full[i], 128);
       mbar_init_n(&pv_done[i], 1);
     }
@@ -590,14 +616,15 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v3(const __grid_
         }
         mma_commit(&s_full[x * 2 + (j & 1)]);
       };
-      auto pv = [&](int x, int j) {  // O[x] += P_x . V_j
+      auto pv = [&](int x, int j) {  // O[x] += P_x(j) . V_j, P from TMEM (16 keys = 8 columns)
         const int st = j % kStagesV3;
         const uint32_t sV = smem_u32(kvbase + st * 2 * kKVBytes + kKVBytes);
+        const uint32_t tP = tmem + x * 128 + (j & 1) * 64;
 #pragma unroll
         for (int k = 0; k < kKT / 16; ++k)
-          mma_f16(tmem + 256 + x * 128, make_desc(smem_u32(sP[x]) + k * 32, 16, 1024),
-                  make_desc(sV + k * 2048, kKVHalf, 1024), idesc_pv, (j > 0 || k > 0) ? 1u : 0u);
-        mma_commit(&pv_done[x]);
+          mma_f16_ts(tmem + 256 + x * 128, tP + k * 8, make_desc(sV + k * 2048, kKVHalf, 1024), idesc_pv,
+                     (j > 0 || k > 0) ? 1u : 0u);
+        mma_commit(&pv_done[2 * x + (j & 1)]);
       };
       auto wait_kv = [&](int j) {
         mbar_wait(&kv_full[j % kStagesV3], (j / kStagesV3) & 1);
@@ -616,14 +643,14 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v3(const __grid_
         qk(1, 1);
       }
       for (int j = 0; j < n_kt; ++j) {
-        mbar_wait(&p_full[0], j & 1);
+        mbar_wait(&p_full[j & 1], (j >> 1) & 1);
         tc_fence_after();
         pv(0, j);
         if (j + 2 < n_kt) {
           wait_kv(j + 2);
           qk(0, j + 2);
         }
-        mbar_wait(&p_full[1], j & 1);
+        mbar_wait(&p_full[2 + (j & 1)], (j >> 1) & 1);
         tc_fence_after();
         pv(1, j);
         mma_commit(&kv_empty[j % kStagesV3]);
@@ -643,7 +670,6 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v3(const __grid_
     const bool tail_rows = t0 + tpt > q_len;
     const float c2 = p.scale_log2;
     float m = -INFINITY, l = 0.f;
-    char* sPx = sP[x];
     for (int j = 0; j < n_kt; ++j) {
       mbar_wait(&s_full[x * 2 + (j & 1)], (j >> 1) & 1);
       tc_fence_after();
@@ -683,40 +709,36 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v3(const __grid_
         l *= alpha;
         m = mt;
       }
-      if (j > 0) {
-        mbar_wait(&pv_done[x], (j - 1) & 1);  // PV(j-1) finished: O stable, P buffer free
+      // the O correction needs PV(j-1) done (it cannot have run further: PV(j) needs P(j))
+      if (j > 0 && __any_sync(0xffffffffu, need)) {
+        mbar_wait(&pv_done[2 * x + ((j - 1) & 1)], ((j - 1) >> 1) & 1);
         tc_fence_after();
-        if (__any_sync(0xffffffffu, need)) {
 #pragma unroll
-          for (int cc = 0; cc < 4; ++cc) {
-            float o[32];
-            tmem_ld32(tO + cc * 32, o);
+        for (int cc = 0; cc < 4; ++cc) {
+          float o[32];
+          tmem_ld32(tO + cc * 32, o);
 #pragma unroll
-            for (int k = 0; k < 32; ++k) o[k] *= alpha;
-            tmem_st32(tO + cc * 32, o);
-          }
+          for (int k = 0; k < 32; ++k) o[k] *= alpha;
+          tmem_st32(tO + cc * 32, o);
         }
       }
       const float mu = (m == -INFINITY) ? 0.f : m;
       float ls[4] = {0.f, 0.f, 0.f, 0.f};
+      uint32_t pk[32];
 #pragma unroll
-      for (int cc = 0; cc < 8; ++cc) {
-        uint32_t pk[4];
-#pragma unroll
-        for (int k = 0; k < 8; k += 2) {
-          const float v0 = ex2(fmaf(s[cc * 8 + k], c2, -mu));
-          const float v1 = ex2(fmaf(s[cc * 8 + k + 1], c2, -mu));
-          ls[k >> 1] += v0 + v1;
-          pk[k >> 1] = pack2<T>(v0, v1);
-        }
-        *reinterpret_cast<uint4*>(sPx + sw_p(row, cc)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      for (int k = 0; k < 64; k += 2) {
+        const float v0 = ex2(fmaf(s[k], c2, -mu));
+        const float v1 = ex2(fmaf(s[k + 1], c2, -mu));
+        ls[(k >> 1) & 3] += v0 + v1;
+        pk[k >> 1] = pack2<T>(v0, v1);
       }
+      tmem_st32u(tS, pk);  // P(j) over S(j): row = lane, keys (2c, 2c+1) in column c
       l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
-      fence_async_smem();
+      fence_async_smem();  // the last tile's V-row zeroing (generic stores) -> tensor core
       tc_fence_before();
-      mbar_arrive(&p_full[x]);
+      mbar_arrive(&p_full[2 * x + (j & 1)]);
     }
-    mbar_wait(&pv_done[x], (n_kt - 1) & 1);
+    mbar_wait(&pv_done[2 * x + ((n_kt - 1) & 1)], ((n_kt - 1) >> 1) & 1);
     tc_fence_after();
     const float inv = l > 0.f ? 1.f / l : 0.f;
     char* dst = reinterpret_cast<char*>(g.out) +
