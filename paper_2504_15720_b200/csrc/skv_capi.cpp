@@ -1221,6 +1221,11 @@ skv_status skv_prefill_attention(skv_pool* p, skv_batch* b, const skv_prefill_ar
   const float scale = a->softmax_scale > 0.f ? a->softmax_scale : 1.0f / std::sqrt(128.0f);
   dp.scale_log2 = scale * 1.4426950408889634f;
   dp.n_new = a->q_len;
+  static const int dbg = [] {
+    const char* e = getenv("SKV_PREFILL_DBG");
+    return e ? atoi(e) : 0;
+  }();
+  dp.dbg = dbg;
   if ((st = order_streams(p, s))) return st;
   skv::launch_prefill(dp, s);
   p->launches++;

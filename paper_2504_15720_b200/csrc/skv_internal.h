@@ -112,6 +112,7 @@ struct DataParams {
                              //  piece index, arrival counter index}
   int* rscr;                 // [5*nreq] plan scratch
   int* arrive;               // [items] pieces finished per (request, kv head) (self-resetting)
+  int dbg;                   // debug knobs (prefill v5: bit1 = polynomial exp2 for 1/4)
   unsigned long long* trace; // debug (SKV_TRACE=1): per warp {start, after wait, end, tiles<<32|items} ns
   float* ws_o;               // [slots][D] unnormalised partial outputs
   float2* ws_ml;             // [slots] (running max (log2 domain), sum)
