@@ -209,6 +209,42 @@ skv_status skv_synth_fill(skv_pool* p, uint64_t seed, float amp, void* stream);
 /* Copies merged blocks ids[0..n) to host dst (n * merged_stride bytes). Syncs. */
 skv_status skv_read_blocks(skv_pool* p, const int32_t* ids, size_t n, void* dst);
 /* Number of GPU kernels this pool has launched (instrumentation for bench.py). */
+/* ---- split scheme (reference: SplitCacheCounter, kv_cache.hpp:277-348) ----
+ * The alternative the paper compares against: every native
+ * block of a request is split into per-(layer, kv head) blocks of 8 KiB, each with its
+ * own table entry (L*H entries per native block instead of one).  The GPU pool below
+ * stores those blocks and runs the SAME decode kernel through per-(request, layer,
+ * head) tables, so merged and split are measured on one data path.  Accounting
+ * (skv_split_stats) is SplitCacheCounter's.  Batches for the split data path are
+ * created on the registry pool (skv_split_registry) from registered request ids; grow
+ * and free go through skv_split_grow / skv_split_free only. */
+typedef struct skv_split skv_split;
+skv_status skv_split_create(const skv_model_desc* models, int32_t n, int32_t tokens_per_block,
+                            int32_t tp_size, size_t split_blocks, const skv_pool_opts* opts,
+                            skv_split** out);
+void skv_split_destroy(skv_split* s);
+const char* skv_split_last_error(const skv_split* s);
+skv_pool* skv_split_registry(skv_split* s);
+size_t skv_split_free_blocks(const skv_split* s);
+size_t skv_split_pool_size(const skv_split* s);
+uint64_t skv_split_kernel_launches(const skv_split* s);
+/* SplitCacheCounter::grow for each (id, model, total tokens) (:286-302), all-or-nothing per
+ * op against the split-block pool (granted[i] = 0: pool exhausted, nothing changed), plus
+ * one GPU launch assigning the new split blocks and writing their table entries. */
+skv_status skv_split_grow(skv_split* s, const uint64_t* ids, const int32_t* models,
+                          const int64_t* tokens, int32_t n, int32_t* granted);
+skv_status skv_split_free(skv_split* s, const uint64_t* ids, int32_t n); /* :304-309 */
+skv_status skv_split_stats(const skv_split* s, skv_cache_stats* out);    /* :311-318 */
+uint64_t skv_split_table_entries(const skv_split* s); /* live entries (current_entries_) */
+skv_status skv_split_synth_fill(skv_split* s, uint64_t seed, float amp, void* stream);
+skv_status skv_split_decode(skv_split* s, skv_batch* b, const skv_decode_args* args, void* stream);
+skv_status skv_split_append(skv_split* s, skv_batch* b, const skv_append_args* args, void* stream);
+/* split block ids of one (request, layer, kv head) row, in token order (tests) */
+skv_status skv_split_block_ids(skv_split* s, uint64_t id, int32_t layer, int32_t head, int32_t* out,
+                               size_t cap, size_t* n);
+/* copies 8 KiB blocks (K then V, [16 tokens][128]) to host memory (tests) */
+skv_status skv_split_read_blocks(skv_split* s, const int32_t* ids, size_t n, void* dst);
+
 /* Debug: with SKV_TRACE=1 in the environment every decode launch of `b` records, per
  * warp, {start, after the dependent-launch wait, end} (globaltimer ns) and
  * tiles<<32 | items; this copies the last launch's records (4 u64 each) to `host`

@@ -6,5 +6,5 @@ paged decode attention as hand-written sm_100a kernels behind the C-ABI in
 include/seakv.h.  See DESIGN.md.
 """
 from .kvcache import (  # noqa: F401
-    BF16, FP16, ArgError, Batch, CacheStats, ConfigError, CudaError, LogicError, ModelSpec, UnifiedKvCache,
-    ValidationError, build, lib, native_block_bytes, plan_merged_shape)
+    BF16, FP16, ArgError, Batch, CacheStats, ConfigError, CudaError, LogicError, ModelSpec, SplitBatch, SplitKvCache,
+    UnifiedKvCache, ValidationError, build, lib, native_block_bytes, plan_merged_shape)

@@ -351,6 +351,56 @@ void launch_stage_copy(void* dst, const void* src_host_mapped, size_t bytes, cud
                                                n4);
 }
 
+// Split scheme: claim c of op i (c in [0, nblk*L*H)) is native block blk0 + c/(L*H),
+// layer (c/H)%L, head c%H; it takes stack[base + c] (the host moved the stack top).
+__device__ __forceinline__ int split_op_of(const SplitOp* ops, int n, long long c) {
+  int lo = 0, hi = n - 1;  // last op with cbeg <= c
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (ops[mid].cbeg <= c) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+__global__ void split_claim_kernel(const SplitOp* __restrict__ ops, int n, long long total,
+                                   const int32_t* __restrict__ stack, int2* __restrict__ table, int Lmax, int Hmax,
+                                   int cap) {
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < total; c += (long long)gridDim.x * blockDim.x) {
+    const SplitOp op = ops[split_op_of(ops, n, c)];
+    const long long k = c - op.cbeg;
+    const int lh = op.L * op.H;
+    const int blk = op.blk0 + (int)(k / lh), l = (int)(k / op.H) % op.L, h = (int)(k % op.H);
+    table[(((size_t)op.handle * Lmax + l) * Hmax + h) * cap + blk] = make_int2(stack[op.base + k], 0);
+  }
+}
+
+__global__ void split_release_kernel(const SplitOp* __restrict__ ops, int n, long long total,
+                                     int32_t* __restrict__ stack, const int2* __restrict__ table, int Lmax, int Hmax,
+                                     int cap) {
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < total; c += (long long)gridDim.x * blockDim.x) {
+    const SplitOp op = ops[split_op_of(ops, n, c)];
+    const long long k = c - op.cbeg;
+    const int lh = op.L * op.H;
+    const int blk = op.blk0 + (int)(k / lh), l = (int)(k / op.H) % op.L, h = (int)(k % op.H);
+    stack[op.base + k] = table[(((size_t)op.handle * Lmax + l) * Hmax + h) * cap + blk].x;
+  }
+}
+
+void launch_split_claim(const SplitOp* ops, int n, long long total, const int32_t* stack, int2* table, int Lmax,
+                        int Hmax, int cap, cudaStream_t s) {
+  if (total <= 0) return;
+  const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 8);
+  split_claim_kernel<<<blocks, 256, 0, s>>>(ops, n, total, stack, table, Lmax, Hmax, cap);
+}
+
+void launch_split_release(const SplitOp* ops, int n, long long total, int32_t* stack, const int2* table, int Lmax,
+                          int Hmax, int cap, cudaStream_t s) {
+  if (total <= 0) return;
+  const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 8);
+  split_release_kernel<<<blocks, 256, 0, s>>>(ops, n, total, stack, table, Lmax, Hmax, cap);
+}
+
 void launch_grow(const DevAlloc& st, const AllocParams& pr, const GrowOp* ops, int n,
                  const GrowScratch& sc, cudaStream_t s) {
   if (n <= 0) return;

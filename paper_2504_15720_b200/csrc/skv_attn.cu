@@ -214,6 +214,13 @@ __device__ __forceinline__ void consume_tile(const char* tile, int lane, int val
   }
 }
 
+// Block-table row of (request handle, kv head) at the launch's layer: one row per request
+// in the merged scheme, one per (request, layer, kv head) in the split scheme.
+__device__ __forceinline__ const int2* table_row(const DataParams& p, int handle, int head) {
+  return p.split_L ? p.req_table + (((size_t)handle * p.split_L + p.layer) * p.split_H + head) * p.cap
+                   : p.req_table + (size_t)handle * p.cap;
+}
+
 // Per-warp producer: walks the same item sequence as the consumer, kStages tiles ahead.
 struct Producer {
   int idx;         // current item, -1 before the first
@@ -256,7 +263,7 @@ __device__ __forceinline__ bool produce_one(const DataParams& p, Producer& P, co
     P.idx = idx;
     P.blk = it.z / kTpb;
     P.bend = (it.w + kTpb - 1) / kTpb;
-    P.row = p.req_table + (size_t)p.handles[it.x] * p.cap;
+    P.row = table_row(p, p.handles[it.x], it.y & 0xffff);
     P.base = p.pool + g.layer_off + (long long)(it.y & 0xffff) * g.head_stride;
     P.nstride = g.native_stride;
     P.cbase = -1;
@@ -324,7 +331,7 @@ __device__ __forceinline__ void process_item(const DataParams& p, Producer& P, c
     if (apos >= 0 && b == apos / kTpb) {
       // lanes 0-15 move the K row, 16-31 the V row (16 B each), as append_kernel
       const int kv = lane >> 4;
-      const int2 e = p.req_table[(size_t)p.handles[it.x] * p.cap + b];
+      const int2 e = table_row(p, p.handles[it.x], head)[b];
       const uint4 val = *reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(kv ? g.v : g.k) +
                                                         ((size_t)rl * g.Hkv + head) * (kD * 2) + c * 16);
       const int off = kv * (kTpb * kD * 2) + (apos % kTpb) * (kD * 2) + c * 16;
@@ -681,7 +688,7 @@ __global__ void append_kernel(const __grid_constant__ DataParams p) {
   const int handle = p.handles[r];
   const int pos = p.req_tokens[handle] - p.n_new + i;
   if (pos < 0) return;
-  const int2 e = p.req_table[(size_t)handle * p.cap + pos / kTpb];
+  const int2 e = table_row(p, handle, h)[pos / kTpb];
   const int kv = lane >> 4, c = lane & 15;
   char* dst = p.pool + (long long)e.x * p.merged_stride + (long long)e.y * g.native_stride + g.layer_off +
               (long long)h * g.head_stride + kv * (kTpb * kD * 2) + (pos % kTpb) * (kD * 2) + c * 16;

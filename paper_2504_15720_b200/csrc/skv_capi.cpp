@@ -118,6 +118,7 @@ struct skv_pool {
   alignas(64) CUtensorMap kv_tmap;
   bool has_tmap = false;
   uint64_t launches = 0;
+  const skv::SplitView* split = nullptr;  // data path addresses a split-scheme pool (skv_split.cpp)
   std::string err;
 };
 
@@ -1003,14 +1004,24 @@ static skv_status make_params(skv_pool* p, skv_batch* b, int layer, skv::DataPar
   dp->tpb = p->tpb;
   dp->dtype = p->dtype;
   dp->head_dim = 128;
+  dp->layer = layer;
+  if (p->split) {  // split scheme: per (request, layer, head) rows of 8 KiB block ids
+    dp->req_table = p->split->table;
+    dp->cap = p->split->cap;
+    dp->pool = p->split->storage;
+    dp->merged_stride = 2 * 16 * 128 * 2;
+    dp->split_L = p->split->L;
+    dp->split_H = p->split->H;
+    dp->has_tmap = 0;
+  }
   for (int g = 0; g < b->ngroups; ++g) {
     const ModelInfo& mi = p->models[b->gmodel[g]];
     if (mi.d != 128 || mi.e != 2 || p->tpb != 16)
       return fail(p, SKV_ERR_ARG, "data path kernels need head_dim 128, 2-byte dtype, tokens_per_block 16");
     skv::DataGroup& dg = dp->g[g];
-    dg.native_stride = mi.native_stride;
-    dg.layer_off = (long long)(layer % mi.phys_L) * mi.layer_stride;
-    dg.head_stride = mi.head_stride;
+    dg.native_stride = p->split ? 0 : mi.native_stride;
+    dg.layer_off = p->split ? 0 : (long long)(layer % mi.phys_L) * mi.layer_stride;
+    dg.head_stride = p->split ? 0 : mi.head_stride;
     dg.Hq = mi.Hq;
     dg.Hkv = mi.Hkv;
     dg.G = mi.Hq / mi.Hkv;
@@ -1046,7 +1057,7 @@ static skv_status after_data(skv_pool* p, cudaStream_t s) {
 skv_status skv_decode_attention(skv_pool* p, skv_batch* b, const skv_decode_args* a, void* stream) {
   skv_status st = check_batch(p, b);
   if (st) return st;
-  if ((st = ensure_storage(p))) return st;
+  if (!p->split && (st = ensure_storage(p))) return st;
   DeviceGuard guard(p->device);
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : p->stream;
   skv::DataParams dp;
@@ -1183,7 +1194,7 @@ skv_status skv_decode_attention(skv_pool* p, skv_batch* b, const skv_decode_args
 skv_status skv_append_kv(skv_pool* p, skv_batch* b, const skv_append_args* a, void* stream) {
   skv_status st = check_batch(p, b);
   if (st) return st;
-  if ((st = ensure_storage(p))) return st;
+  if (!p->split && (st = ensure_storage(p))) return st;
   if (a->n_new < 1) return fail(p, SKV_ERR_ARG, "append: n_new must be >= 1");
   DeviceGuard guard(p->device);
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : p->stream;
@@ -1294,4 +1305,10 @@ skv_status skv_debug_decode_trace(skv_pool* p, skv_batch* b, uint64_t* host, siz
   SKV_CUDA(p, cudaMemcpy(host, b->d_trace, m * 4 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
   *n = m;
   return SKV_OK;
+}
+
+void skv_internal_set_split(skv_pool* p, const skv::SplitView* view) { p->split = view; }
+int skv_internal_handle(const skv_pool* p, uint64_t id) {
+  auto it = p->id2h.find(id);
+  return it == p->id2h.end() ? -1 : it->second;
 }

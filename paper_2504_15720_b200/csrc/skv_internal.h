@@ -113,12 +113,44 @@ struct DataParams {
   int* rscr;                 // [5*nreq] plan scratch
   int* arrive;               // [items] pieces finished per (request, kv head) (self-resetting)
   int dbg;                   // debug knobs (prefill v5: bit1 = polynomial exp2 for 1/4)
+  // split scheme (skv_split.cpp): split_L > 0 -> req_table rows are per (request, layer,
+  // kv head): row (handle*split_L + layer)*split_H + head, entry .x = split block id,
+  // address = pool + id * merged_stride (8 KiB), every per-group offset/stride is 0
+  int split_L, split_H, layer;
   unsigned long long* trace; // debug (SKV_TRACE=1): per warp {start, after wait, end, tiles<<32|items} ns
   float* ws_o;               // [slots][D] unnormalised partial outputs
   float2* ws_ml;             // [slots] (running max (log2 domain), sum)
 };
 
+// Split-scheme view installed on an allocator-only registry pool while a split pool
+// runs its data path through the shared decode machinery (skv_split.cpp).
+struct SplitView {
+  int2* table;     // [R][L][H][cap] (split block id, 0)
+  char* storage;   // [blocks][8 KiB]
+  int L, H, cap;
+};
+
+// split-scheme block claims / releases (skv_alloc.cu): op i covers claims
+// [cbeg[i], cbeg[i+1]) of the batch, native blocks [blk0, blk0 + nblk) of request
+// `handle` for all (layer, head) of its model; ids come from / return to stack[base..]
+struct SplitOp {
+  int32_t handle, L, H, blk0, nblk, base, cbeg, pad;
+};
+void launch_split_claim(const SplitOp* ops, int n, long long total, const int32_t* stack, int2* table, int Lmax,
+                        int Hmax, int cap, cudaStream_t s);
+void launch_split_release(const SplitOp* ops, int n, long long total, int32_t* stack, const int2* table, int Lmax,
+                          int Hmax, int cap, cudaStream_t s);
+
 void launch_decode_plan(const DataParams& p, cudaStream_t s);
+
+}  // namespace skv
+
+struct skv_pool;
+// hooks of the registry pool used by skv_split.cpp (skv_capi.cpp)
+void skv_internal_set_split(skv_pool* p, const skv::SplitView* view);
+int skv_internal_handle(const skv_pool* p, uint64_t id);  // -1 if unknown
+
+namespace skv {
 void launch_decode(const DataParams& p, int max_g, int grid, cudaStream_t s);
 void launch_append(const DataParams& p, cudaStream_t s);
 void launch_prefill(const DataParams& p, cudaStream_t s);

@@ -191,6 +191,23 @@ def lib() -> C.CDLL:
         "skv_read_blocks": (S, [P, P, C.c_size_t, P]),
         "skv_kernel_launches": (C.c_uint64, [P]),
         "skv_debug_decode_trace": (S, [P, P, P, C.c_size_t, C.POINTER(C.c_size_t)]),
+        "skv_split_create": (S, [C.POINTER(_ModelDesc), C.c_int32, C.c_int32, C.c_int32, C.c_size_t,
+                                 C.POINTER(_Opts), C.POINTER(P)]),
+        "skv_split_destroy": (V, [P]),
+        "skv_split_last_error": (C.c_char_p, [P]),
+        "skv_split_registry": (P, [P]),
+        "skv_split_free_blocks": (C.c_size_t, [P]),
+        "skv_split_pool_size": (C.c_size_t, [P]),
+        "skv_split_kernel_launches": (C.c_uint64, [P]),
+        "skv_split_grow": (S, [P, P, P, P, C.c_int32, P]),
+        "skv_split_free": (S, [P, P, C.c_int32]),
+        "skv_split_stats": (S, [P, C.POINTER(_Stats)]),
+        "skv_split_table_entries": (C.c_uint64, [P]),
+        "skv_split_synth_fill": (S, [P, C.c_uint64, C.c_float, P]),
+        "skv_split_decode": (S, [P, P, C.POINTER(_DecodeArgs), P]),
+        "skv_split_append": (S, [P, P, C.POINTER(_AppendArgs), P]),
+        "skv_split_block_ids": (S, [P, C.c_uint64, C.c_int32, C.c_int32, P, C.c_size_t, C.POINTER(C.c_size_t)]),
+        "skv_split_read_blocks": (S, [P, P, C.c_size_t, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -527,3 +544,143 @@ class Batch:
                          layer, q_len)
         self.cache._chk(self.cache._lib.skv_prefill_attention(self.cache._h, self._h, C.byref(a),
                                                               _stream_ptr(stream)))
+
+
+class SplitKvCache:
+    """The split scheme on the GPU (reference SplitCacheCounter,
+    kv_cache.hpp:277-348): per-(layer, kv head) 8 KiB blocks with one table entry each,
+    same decode kernel as the merged pool.  ``grow``/``free`` are batched
+    SplitCacheCounter calls; ``stats()`` is SplitCacheCounter::stats."""
+
+    def __init__(self, models: Sequence[ModelSpec], tokens_per_block: int = 16, tp_size: int = 1,
+                 split_blocks: int = 0, *, device: int = 0, dtype: int = FP16, max_requests: int = 4096,
+                 max_blocks_per_request: int = 0):
+        L = lib()
+        self._lib = L
+        self.models = list(models)
+        arr, self._keep = _desc(self.models)
+        opts = _Opts()
+        L.skv_default_opts(C.byref(opts))
+        opts.device, opts.dtype = device, dtype
+        opts.max_requests, opts.max_blocks_per_request = max_requests, max_blocks_per_request
+        h = C.c_void_p()
+        _raise(L.skv_split_create(arr, len(self.models), tokens_per_block, tp_size, split_blocks, C.byref(opts),
+                                  C.byref(h)), None)
+        self._s = h.value
+        reg = UnifiedKvCache.__new__(UnifiedKvCache)  # the registry pool is owned by the split pool
+        reg._lib, reg._h, reg.models, reg.device, reg.dtype = L, L.skv_split_registry(self._s), self.models, device, dtype
+        reg.close = lambda: None
+        self.registry = reg
+        self.device, self.dtype = device, dtype
+
+    def close(self):
+        if getattr(self, "_s", None):
+            self.registry._h = None
+            self._lib.skv_split_destroy(self._s)
+            self._s = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _chk(self, st):
+        if st not in (SKV_OK, SKV_CACHE_FULL):
+            msg = self._lib.skv_split_last_error(self._s)
+            raise _ERRS.get(st, RuntimeError)(msg.decode() if msg else f"status {st}")
+        return st
+
+    def grow(self, ids: Sequence[int], models: Sequence[int], tokens: Sequence[int]) -> np.ndarray:
+        n = len(ids)
+        ia = np.asarray(ids, dtype=np.uint64)
+        ma = np.asarray(models, dtype=np.int32)
+        ta = np.asarray(tokens, dtype=np.int64)
+        g = np.zeros(n, dtype=np.int32)
+        self._chk(self._lib.skv_split_grow(self._s, ia.ctypes.data, ma.ctypes.data, ta.ctypes.data, n, g.ctypes.data))
+        return g.astype(bool)
+
+    def free(self, ids: Sequence[int]):
+        ia = np.asarray(ids, dtype=np.uint64)
+        self._chk(self._lib.skv_split_free(self._s, ia.ctypes.data, len(ia)))
+
+    def stats(self) -> dict:
+        st = _Stats()
+        self._chk(self._lib.skv_split_stats(self._s, C.byref(st)))
+        return {"block_table_entries": st.block_table_entries, "native_reads_writes": st.native_reads_writes,
+                "internal_fragmentation_bytes": st.internal_fragmentation_bytes,
+                "peak_utilization": st.peak_utilization}
+
+    def table_entries(self) -> int:
+        return self._lib.skv_split_table_entries(self._s)
+
+    def free_blocks(self) -> int:
+        return self._lib.skv_split_free_blocks(self._s)
+
+    def pool_size(self) -> int:
+        return self._lib.skv_split_pool_size(self._s)
+
+    def kernel_launches(self) -> int:
+        return self._lib.skv_split_kernel_launches(self._s) + self.registry.kernel_launches()
+
+    def request_tokens(self, request_id: int) -> int:
+        return self.registry.request_tokens(request_id)
+
+    def synth_fill(self, seed: int, amp: float = 1.0, stream=None):
+        self._chk(self._lib.skv_split_synth_fill(self._s, seed, amp, _stream_ptr(stream)))
+
+    def set_stream(self, stream):
+        self.registry.set_stream(stream)
+
+    def block_ids(self, request_id: int, layer: int, head: int) -> np.ndarray:
+        out = np.zeros(1 << 16, dtype=np.int32)
+        n = C.c_size_t()
+        self._chk(self._lib.skv_split_block_ids(self._s, request_id, layer, head, out.ctypes.data, out.size,
+                                                C.byref(n)))
+        return out[: n.value].copy()
+
+    def read_blocks(self, ids) -> np.ndarray:
+        ids = np.ascontiguousarray(ids, dtype=np.int32)
+        out = np.empty(len(ids) * 8192, dtype=np.uint8)
+        self._chk(self._lib.skv_split_read_blocks(self._s, ids.ctypes.data, len(ids), out.ctypes.data))
+        return out
+
+    def batch(self, groups: Sequence[tuple[int, Sequence[int]]]) -> "SplitBatch":
+        return SplitBatch(self, groups)
+
+
+class SplitBatch(Batch):
+    """A batch of a SplitKvCache: decode / append address the split tables."""
+
+    def __init__(self, split: SplitKvCache, groups):
+        self.split = split
+        super().__init__(split.registry, groups)
+
+    def grow(self, delta: int = 1) -> int:
+        ids = [i for _, g in self.groups for i in g]
+        models = [m for m, g in self.groups for _ in g]
+        toks = [self.split.request_tokens(i) + delta for i in ids]
+        return int(self.split.grow(ids, models, toks).sum())
+
+    def decode(self, q, out, layer, softmax_scale=0.0, split_tokens=0, stream=None, k=None, v=None):
+        n = len(self.groups)
+        qa = (C.c_void_p * n)(*[_ptr(t) for t in q])
+        oa = (C.c_void_p * n)(*[_ptr(t) for t in out])
+        a = _DecodeArgs(C.cast(qa, C.POINTER(C.c_void_p)), C.cast(oa, C.POINTER(C.c_void_p)), softmax_scale,
+                        layer, split_tokens)
+        if k is not None:
+            ka = (C.c_void_p * n)(*[_ptr(t) for t in k])
+            va = (C.c_void_p * n)(*[_ptr(t) for t in v])
+            a.k = C.cast(ka, C.POINTER(C.c_void_p))
+            a.v = C.cast(va, C.POINTER(C.c_void_p))
+        self.split._chk(self.split._lib.skv_split_decode(self.split._s, self._h, C.byref(a), _stream_ptr(stream)))
+
+    def append(self, k, v, layer, n_new=1, stream=None):
+        n = len(self.groups)
+        ka = (C.c_void_p * n)(*[_ptr(t) for t in k])
+        va = (C.c_void_p * n)(*[_ptr(t) for t in v])
+        a = _AppendArgs(C.cast(ka, C.POINTER(C.c_void_p)), C.cast(va, C.POINTER(C.c_void_p)), layer, n_new)
+        self.split._chk(self.split._lib.skv_split_append(self.split._s, self._h, C.byref(a), _stream_ptr(stream)))
+
+    def prefill(self, *a, **k):
+        raise NotImplementedError("the split-scheme pool implements the decode path (SURVEY §8(f) row 2)")
