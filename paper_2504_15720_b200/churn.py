@@ -146,7 +146,8 @@ class ChurnEngine:
         self._dec_batch: Optional[Batch] = None
         self._pre_batches: Dict[int, Batch] = {}
         self.stats = dict(iterations=0, grow_ops=0, free_ops=0, preemptions=0, alloc_s=0.0, append_ms=0.0,
-                          decode_ms=0.0, prefill_ms=0.0, decode_bytes=0.0, append_bytes=0.0, prefill_flops=0.0,
+                          decode_ms=0.0, prefill_ms=0.0, decode_bytes=0.0, append_bytes=0.0, data_path_ms=0.0,
+                          prefill_flops=0.0,
                           occupancy_sum=0.0, finished=0, admitted=0, cache_full=0)
         self.M = M
 
@@ -221,6 +222,8 @@ class ChurnEngine:
         # data path over every layer index
         ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
         marks = []
+        span = [ev(), ev()]  # GPU time of the whole data path of this step
+        span[0].record(self.stream)
         if dec_ok:
             groups = [(m, [r.rid for r in dec_ok if r.model == m]) for m in range(self.M)]
             groups = [g for g in groups if g[1]]
@@ -228,6 +231,10 @@ class ChurnEngine:
             q = [self.q_dec[m][: len(ids)] for m, ids in groups]
             o = [self.o_dec[m][: len(ids)] for m, ids in groups]
             kv = [self.kv_dec[m][: len(ids)] for m, ids in groups]
+            # separate append and decode launches, each bracketed by events (per-kernel
+            # accounting; the benchmark's decode step uses the fused launch instead).
+            # This driver is host-bound: the intervals include host submission gaps, and
+            # data_path_ms is the GPU span of the whole step.
             for layer in range(self.nlayers):
                 e = [ev(), ev(), ev()]
                 e[0].record(self.stream)
@@ -265,7 +272,9 @@ class ChurnEngine:
                 p0 = r.done
                 st["prefill_flops"] += 4.0 * 128 * Hq * L * (c * p0 + c * (c + 1) / 2)
                 st["append_bytes"] += c * L * 2 * H * 128 * 2 * 2
+        span[1].record(self.stream)
         torch.cuda.synchronize()
+        st["data_path_ms"] += span[0].elapsed_time(span[1])
         for kind, e in marks:
             st["append_ms"] += e[0].elapsed_time(e[1])
             st["decode_ms" if kind == "dec" else "prefill_ms"] += e[1].elapsed_time(e[2])
@@ -304,7 +313,7 @@ class ChurnEngine:
             "append_GBps": round(st["append_bytes"] / max(st["append_ms"], 1e-9) / 1e6, 1),
             "prefill_TFLOPs": round(st["prefill_flops"] / max(st["prefill_ms"], 1e-9) / 1e9, 1),
             "decode_ms": round(st["decode_ms"], 2), "prefill_ms": round(st["prefill_ms"], 2),
-            "append_ms": round(st["append_ms"], 2),
+            "append_ms": round(st["append_ms"], 2), "data_path_ms": round(st["data_path_ms"], 2),
         }
 
 
