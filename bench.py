@@ -262,13 +262,22 @@ def run_gpu(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # SKV_BENCH_SHARE_GPU=1 + SKV_BENCH_BACKEND=gloo: every rank on GPU 0 (functional test
+    # of the N-rank path on a 1-GPU box; the numbers are then meaningless)
+    if os.environ.get("SKV_BENCH_SHARE_GPU") == "1":
+        local = 0
+    backend = os.environ.get("SKV_BENCH_BACKEND", "nccl")
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     wl, cache, batch, q, out, k, v, stream = setup(P, torch, args, local)
     NLAYERS = wl.nlayers
+    red_dev = "cuda" if backend == "nccl" else "cpu"
 
     def barrier():
         torch.cuda.synchronize()
@@ -278,14 +287,14 @@ def run_gpu(args):
     def max_over_ranks(x):
         if not dist:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     def sum_over_ranks(x):
         if not dist:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t.item())
 
