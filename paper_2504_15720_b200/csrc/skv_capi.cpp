@@ -1237,6 +1237,25 @@ skv_status skv_prefill_attention(skv_pool* p, skv_batch* b, const skv_prefill_ar
     return e ? atoi(e) : 0;
   }();
   dp.dbg = dbg;
+  static const bool trace_on = [] {
+    const char* e = getenv("SKV_TRACE");
+    return e && e[0] == '1';
+  }();
+  if (trace_on) {  // prefill_kernel_v3 built with -DSKV_PF_TRACE: 16 u64 per CTA (4 records)
+    int tiles = 1, heads = 1;
+    for (int g = 0; g < b->ngroups; ++g) {
+      tiles = std::max(tiles, (a->q_len * dp.g[g].G + 127) / 128);
+      heads = std::max(heads, dp.g[g].Hkv);
+    }
+    const size_t n = (size_t)((tiles + 1) / 2) * heads * b->nreq * 4;
+    if (b->trace_n < n) {
+      if (b->d_trace) cudaFree(b->d_trace);
+      SKV_CUDA(p, cudaMalloc(&b->d_trace, n * 4 * sizeof(unsigned long long)));
+      b->trace_n = n;
+    }
+    SKV_CUDA(p, cudaMemsetAsync(b->d_trace, 0, n * 4 * sizeof(unsigned long long), s));
+    dp.trace = b->d_trace;
+  }
   if ((st = order_streams(p, s))) return st;
   skv::launch_prefill(dp, s);
   p->launches++;

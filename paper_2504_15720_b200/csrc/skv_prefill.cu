@@ -524,8 +524,25 @@ __device__ __forceinline__ void cp_async_arrive(uint64_t* b) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(b)) : "memory");
 }
 
+// Build with SKV_EXTRA=-DSKV_PF_TRACE to record, per CTA, clock64 cycles spent in each
+// role's waits (16 u64 per CTA in p.trace; see scripts/prefill_trace.py).
+#ifdef SKV_PF_TRACE
+#define PF_T(slot, stmt)                      \
+  do {                                        \
+    const long long t0_ = clock64();          \
+    stmt;                                     \
+    pf_acc[slot] += clock64() - t0_;          \
+  } while (0)
+#else
+#define PF_T(slot, stmt) stmt
+#endif
+
 template <typename T>
 __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v3(const __grid_constant__ DataParams p) {
+#ifdef SKV_PF_TRACE
+  long long pf_acc[4] = {0, 0, 0, 0};
+  const long long pf_start = clock64();
+#endif
   extern __shared__ __align__(1024) char smem[];
   if (smem_u32(smem) & 1023) __trap();
   char* sQ[2] = {smem, smem + kTileBytes};
@@ -603,7 +620,7 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v3(const __grid_
       const int n_blk = (n_keys + kTpb - 1) / kTpb;
       for (int j = 0; j < n_kt; ++j) {
         const int st = j % kStagesV3;
-        if (j >= kStagesV3) mbar_wait(&kv_empty[st], ((j / kStagesV3) - 1) & 1);
+        if (j >= kStagesV3) PF_T(0, mbar_wait(&kv_empty[st], ((j / kStagesV3) - 1) & 1));
         int2 e[4];
         int nb = 0;
 #pragma unroll
@@ -655,13 +672,13 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v3(const __grid_
         mma_commit(&pv_done[2 * x + (j & 1)]);
       };
       auto wait_kv = [&](int j) {
-        mbar_wait(&kv_full[j % kStagesV3], (j / kStagesV3) & 1);
+        PF_T(1, mbar_wait(&kv_full[j % kStagesV3], (j / kStagesV3) & 1));
         fence_async_smem();  // cp.async / TMA data -> tensor-core reads
         tc_fence_after();
       };
       // QK runs two tiles ahead of PV (S double-buffered in TMEM), so the softmax of
       // tile j+1 never waits for PV(j): order QK_A0 QK_B0 QK_A1 QK_B1 | PV_A0 QK_A2 PV_B0 QK_B2 | ...
-      mbar_wait(q_full, 0);
+      PF_T(0, mbar_wait(q_full, 0));
       wait_kv(0);
       qk(0, 0);
       qk(1, 0);
@@ -671,14 +688,14 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v3(const __grid_
         qk(1, 1);
       }
       for (int j = 0; j < n_kt; ++j) {
-        mbar_wait(&p_full[j & 1], (j >> 1) & 1);
+        PF_T(2, mbar_wait(&p_full[j & 1], (j >> 1) & 1));
         tc_fence_after();
         pv(0, j);
         if (j + 2 < n_kt) {
           wait_kv(j + 2);
           qk(0, j + 2);
         }
-        mbar_wait(&p_full[2 + (j & 1)], (j >> 1) & 1);
+        PF_T(3, mbar_wait(&p_full[2 + (j & 1)], (j >> 1) & 1));
         tc_fence_after();
         pv(1, j);
         mma_commit(&kv_empty[j % kStagesV3]);
@@ -699,7 +716,7 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v3(const __grid_
     const float c2 = p.scale_log2;
     float m = -INFINITY, l = 0.f;
     for (int j = 0; j < n_kt; ++j) {
-      mbar_wait(&s_full[x * 2 + (j & 1)], (j >> 1) & 1);
+      PF_T(0, mbar_wait(&s_full[x * 2 + (j & 1)], (j >> 1) & 1));
       tc_fence_after();
       const uint32_t tS = tS0 + (j & 1) * 64;
       if (x == 0 && j == n_kt - 1 && (j + 1) * kKT > ctx) {
@@ -730,7 +747,7 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v3(const __grid_
       }
       // the O correction needs PV(j-1) done (it cannot have run further: PV(j) needs P(j))
       if (j > 0 && __any_sync(0xffffffffu, need)) {
-        mbar_wait(&pv_done[2 * x + ((j - 1) & 1)], ((j - 1) >> 1) & 1);
+        PF_T(1, mbar_wait(&pv_done[2 * x + ((j - 1) & 1)], ((j - 1) >> 1) & 1));
         tc_fence_after();
 #pragma unroll
         for (int cc = 0; cc < 4; ++cc) {
@@ -757,7 +774,7 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v3(const __grid_
       tc_fence_before();
       mbar_arrive(&p_full[2 * x + (j & 1)]);
     }
-    mbar_wait(&pv_done[2 * x + ((n_kt - 1) & 1)], ((n_kt - 1) >> 1) & 1);
+    PF_T(2, mbar_wait(&pv_done[2 * x + ((n_kt - 1) & 1)], ((n_kt - 1) >> 1) & 1));
     tc_fence_after();
     const float inv = l > 0.f ? 1.f / l : 0.f;
     char* dst = reinterpret_cast<char*>(g.out) +
@@ -779,6 +796,300 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v3(const __grid_
       }
     }
   }
+#ifdef SKV_PF_TRACE
+  if (p.trace) {  // [cta][16]: loader 0, mma 1-4, softmax A 5-8, softmax B 9-12, cta 13, n_kt 14
+    unsigned long long* t = p.trace + ((size_t)(blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 16;
+    if (warp == kLoadWarp && lane == 0) t[0] = pf_acc[0];
+    if (warp == kMmaWarp && lane == 0)
+      for (int i = 0; i < 4; ++i) t[1 + i] = pf_acc[i];
+    if (warp < kSoftmaxWarps && (tid & 127) == 0)
+      for (int i = 0; i < 3; ++i) t[5 + 4 * (warp >> 2) + i] = pf_acc[i];
+    if (tid == 0) {
+      t[13] = clock64() - pf_start;
+      t[14] = n_kt;
+    }
+  }
+#endif
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kMmaWarp) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// v7: Q in TMEM.  With Q and K both read from shared memory, a 128x64x16 QK^T MMA moves
+// 6 KiB of operands per 32 tensor-core cycles, above the 128 B/clk shared-memory read
+// rate: it issues at 48 clk instead of 32 (scripts/umma_bench).  Here the softmax warps
+// write their Q rows into TMEM once per CTA (one thread per row, tcgen05.st) and QK^T is
+// the TS form (A = Q from TMEM, B = K from smem): shared memory then feeds only K and V
+// (64 B/clk), the tensor core runs both MMAs at full rate, and the Q buffers' 64 KiB of
+// smem become two more K/V stages (7).  TMEM: Q_A | Q_B (64 cols each) | S_A | S_B (64) |
+// O_A | O_B (128); S is single-buffered per tile (P written over it), so per tile the
+// chain is softmax(j) -> P.V(j) -> QK(j+1) -> softmax(j+1), the other tile's softmax
+// running meanwhile.
+constexpr int kStagesV7 = 7;
+constexpr int kSmemV7 = kStagesV7 * 2 * kKVBytes + 256;
+
+template <typename T>
+__global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v7(const __grid_constant__ DataParams p) {
+  extern __shared__ __align__(1024) char smem[];
+  if (smem_u32(smem) & 1023) __trap();
+#ifdef SKV_PF_TRACE
+  long long pf_acc[4] = {0, 0, 0, 0};
+  const long long pf_start = clock64();
+#endif
+  char* kvbase = smem;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(kvbase + kStagesV7 * 2 * kKVBytes);
+  uint64_t* kv_full = bars;                      // [stages]
+  uint64_t* kv_empty = bars + kStagesV7;         // [stages]
+  uint64_t* q_full = bars + 2 * kStagesV7;       // count 256: every softmax thread stored its Q row
+  uint64_t* s_full = bars + 2 * kStagesV7 + 1;   // [tile]
+  uint64_t* p_full = bars + 2 * kStagesV7 + 3;   // [tile] count 128
+  uint64_t* pv_done = bars + 2 * kStagesV7 + 5;  // [tile]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStagesV7 + 7);
+
+  const int r = blockIdx.z, h = blockIdx.y;
+  const int grp = p.req_group[r];
+  const DataGroup& g = p.g[grp];
+  const int G = g.G;
+  const int q_len = p.n_new;
+  const int tileA = 2 * blockIdx.x;
+  if (!g.active || h >= g.Hkv || tileA * kRows >= q_len * G) return;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int handle = p.handles[r];
+  const int ctx = p.req_tokens[handle];
+  const int start = ctx - q_len;
+  const int tpt = kRows / G;
+  const int t0A = tileA * tpt;
+  const int n_keys = min(ctx, start + t0A + 2 * tpt);
+  const int n_kt = (n_keys + kKT - 1) / kKT;
+  const int rl = r - g.req_begin;
+
+  if (warp == kMmaWarp) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < kStagesV7; ++i) {
+      mbar_init_n(&kv_full[i], 1);
+      mbar_init_n(&kv_empty[i], 1);
+    }
+    mbar_init_n(q_full, 2 * 128);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init_n(&s_full[i], 1);
+      mbar_init_n(&p_full[i], 128);
+      mbar_init_n(&pv_done[i], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == kLoadWarp) {  // ----------------------------------------------- K/V streaming
+    if (lane == 0) {
+      const int2* row_tab = p.req_table + (size_t)handle * p.cap;
+      const long long base_off = g.layer_off + (long long)h * g.head_stride;
+      const int n_blk = (n_keys + kTpb - 1) / kTpb;
+      for (int j = 0; j < n_kt; ++j) {
+        const int st = j % kStagesV7;
+        if (j >= kStagesV7) PF_T(0, mbar_wait(&kv_empty[st], ((j / kStagesV7) - 1) & 1));
+        int2 e[4];
+        int nb = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int bi = j * 4 + b;
+          e[b] = bi < n_blk ? row_tab[bi] : make_int2(-1, 0);
+          nb += bi < n_blk;
+        }
+        mbar_expect_tx_v3(&kv_full[st], nb * 4 * 2048);
+        const uint32_t sK = smem_u32(kvbase + st * 2 * kKVBytes), sV = sK + kKVBytes;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          if (e[b].x < 0) continue;
+          const int row0 = (int)(((long long)e[b].x * p.merged_stride + (long long)e[b].y * g.native_stride +
+                                  base_off) >> 8);
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            tma_load_2d(sK + hh * kKVHalf + b * 2048, &p.kv_tmap, hh * 64, row0, &kv_full[st]);
+            tma_load_2d(sV + hh * kKVHalf + b * 2048, &p.kv_tmap, hh * 64, row0 + kTpb, &kv_full[st]);
+          }
+        }
+      }
+    }
+  } else if (warp == kMmaWarp) {  // -------------------------------------------- MMA issue
+    if (lane == 0) {
+      const uint32_t idesc_qk = make_idesc_n(p.dtype, 0, kKT);
+      const uint32_t idesc_pv = make_idesc_n(p.dtype, 1, kD);
+      auto qk = [&](int x, int j) {  // S_x = Q_x (TMEM, 8 columns per 16 dims) . K_j^T
+        const uint32_t sK = smem_u32(kvbase + (j % kStagesV7) * 2 * kKVBytes);
+#pragma unroll
+        for (int k = 0; k < kD / 16; ++k) {
+          const uint32_t koff = (k >> 2) * kKVHalf + (k & 3) * 32;
+          mma_f16_ts(tmem + 128 + x * 64, tmem + x * 64 + k * 8, make_desc(sK + koff, 16, 1024), idesc_qk, k > 0);
+        }
+        mma_commit(&s_full[x]);
+      };
+      auto pv = [&](int x, int j) {  // O_x += P_x(j) (TMEM, over S_x) . V_j
+        const uint32_t sV = smem_u32(kvbase + (j % kStagesV7) * 2 * kKVBytes + kKVBytes);
+#pragma unroll
+        for (int k = 0; k < kKT / 16; ++k)
+          mma_f16_ts(tmem + 256 + x * 128, tmem + 128 + x * 64 + k * 8, make_desc(sV + k * 2048, kKVHalf, 1024),
+                     idesc_pv, (j > 0 || k > 0) ? 1u : 0u);
+        mma_commit(&pv_done[x]);
+      };
+      auto wait_kv = [&](int j) {
+        PF_T(1, mbar_wait(&kv_full[j % kStagesV7], (j / kStagesV7) & 1));
+        tc_fence_after();
+      };
+      PF_T(0, mbar_wait(q_full, 0));
+      tc_fence_after();
+      wait_kv(0);
+      qk(0, 0);
+      qk(1, 0);
+      for (int j = 0; j < n_kt; ++j) {
+        PF_T(2, mbar_wait(&p_full[0], j & 1));
+        tc_fence_after();
+        pv(0, j);
+        if (j + 1 < n_kt) {
+          wait_kv(j + 1);
+          qk(0, j + 1);  // overwrites S_A / P_A(j) after P.V_A(j) in issue order
+        }
+        PF_T(3, mbar_wait(&p_full[1], j & 1));
+        tc_fence_after();
+        pv(1, j);
+        mma_commit(&kv_empty[j % kStagesV7]);
+        if (j + 1 < n_kt) qk(1, j + 1);
+      }
+    }
+    __syncwarp();
+  } else {  // ------------------------------------------------------------- softmax warps
+    const int x = warp >> 2;
+    const int row = tid & 127;
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const uint32_t tQ = tmem + x * 64 + lane_off, tS = tmem + 128 + x * 64 + lane_off;
+    const uint32_t tO = tmem + 256 + x * 128 + lane_off;
+    const int t0 = t0A + x * tpt;
+    const int my_tok = t0 + row / G;
+    const bool row_ok = my_tok < q_len;
+    const int my_pos = start + my_tok;
+    const bool tail_rows = t0 + tpt > q_len;
+    const float c2 = p.scale_log2;
+    {  // this thread's Q row -> TMEM lane `row`, 64 columns of packed pairs
+      const uint4* src = reinterpret_cast<const uint4*>(
+          reinterpret_cast<const char*>(g.q) +
+          (((size_t)rl * q_len + (row_ok ? my_tok : 0)) * g.Hq + h * G + row % G) * (kD * 2));
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        uint32_t qv[32];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const uint4 v = row_ok ? src[hh * 8 + i] : make_uint4(0u, 0u, 0u, 0u);
+          qv[4 * i] = v.x;
+          qv[4 * i + 1] = v.y;
+          qv[4 * i + 2] = v.z;
+          qv[4 * i + 3] = v.w;
+        }
+        tmem_st32u(tQ + hh * 32, qv);
+      }
+      tc_fence_before();
+      mbar_arrive(q_full);
+    }
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < n_kt; ++j) {
+      PF_T(0, mbar_wait(&s_full[x], j & 1));
+      tc_fence_after();
+      if (x == 0 && j == n_kt - 1 && (j + 1) * kKT > n_keys) {
+        char* sV = kvbase + (j % kStagesV7) * 2 * kKVBytes + kKVBytes;
+        const int c = row & 15;
+        for (int key = row >> 4; key < kKT; key += 8)
+          if (j * kKT + key >= n_keys) *reinterpret_cast<uint4*>(sV + sw_kv(key, c)) = make_uint4(0, 0, 0, 0);
+      }
+      float s[64];
+      tmem_ld64(tS, s);
+      const bool masked = (j * kKT + kKT - 1 > start + t0) || tail_rows;
+      if (masked) {
+#pragma unroll
+        for (int k = 0; k < 64; ++k)
+          if (!(row_ok && j * kKT + k <= my_pos)) s[k] = -INFINITY;
+      }
+      float mx4[4] = {s[0], s[1], s[2], s[3]};
+#pragma unroll
+      for (int k = 4; k < 64; ++k) mx4[k & 3] = fmaxf(mx4[k & 3], s[k]);
+      const float mt = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * c2;
+      const bool need = mt > m + kRescale;
+      float alpha = 1.f;
+      if (need) {
+        alpha = ex2(m - mt);
+        l *= alpha;
+        m = mt;
+      }
+      // S(j) ready implies P.V(j-1) retired (issued before QK(j)); P.V(j) waits for P(j)
+      if (j > 0 && __any_sync(0xffffffffu, need)) {
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+          float o[32];
+          tmem_ld32(tO + cc * 32, o);
+#pragma unroll
+          for (int k = 0; k < 32; ++k) o[k] *= alpha;
+          tmem_st32(tO + cc * 32, o);
+        }
+      }
+      const float mu = (m == -INFINITY) ? 0.f : m;
+      float ls[4] = {0.f, 0.f, 0.f, 0.f};
+      uint32_t pk[32];
+#pragma unroll
+      for (int k = 0; k < 64; k += 2) {
+        const float v0 = ex2(fmaf(s[k], c2, -mu));
+        const float v1 = ex2(fmaf(s[k + 1], c2, -mu));
+        ls[(k >> 1) & 3] += v0 + v1;
+        pk[k >> 1] = pack2<T>(v0, v1);
+      }
+      tmem_st32u(tS, pk);
+      l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+      fence_async_smem();
+      tc_fence_before();
+      mbar_arrive(&p_full[x]);
+    }
+    PF_T(2, mbar_wait(&pv_done[x], (n_kt - 1) & 1));
+    tc_fence_after();
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    char* dst = reinterpret_cast<char*>(g.out) +
+                (((size_t)rl * q_len + (row_ok ? my_tok : 0)) * g.Hq + h * G + row % G) * (kD * 2);
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) {
+      float o[32];
+      tmem_ld32(tO + cc * 32, o);
+      if (row_ok) {
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          uint4 v;
+          v.x = pack2<T>(o[8 * q4] * inv, o[8 * q4 + 1] * inv);
+          v.y = pack2<T>(o[8 * q4 + 2] * inv, o[8 * q4 + 3] * inv);
+          v.z = pack2<T>(o[8 * q4 + 4] * inv, o[8 * q4 + 5] * inv);
+          v.w = pack2<T>(o[8 * q4 + 6] * inv, o[8 * q4 + 7] * inv);
+          *reinterpret_cast<uint4*>(dst + cc * 64 + q4 * 16) = v;
+        }
+      }
+    }
+  }
+#ifdef SKV_PF_TRACE
+  if (p.trace) {  // same record layout as v3
+    unsigned long long* t = p.trace + ((size_t)(blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 16;
+    if (warp == kLoadWarp && lane == 0) t[0] = pf_acc[0];
+    if (warp == kMmaWarp && lane == 0)
+      for (int i = 0; i < 4; ++i) t[1 + i] = pf_acc[i];
+    if (warp < kSoftmaxWarps && (tid & 127) == 0)
+      for (int i = 0; i < 3; ++i) t[5 + 4 * (warp >> 2) + i] = pf_acc[i];
+    if (tid == 0) {
+      t[13] = clock64() - pf_start;
+      t[14] = n_kt;
+    }
+  }
+#endif
   tc_fence_before();
   __syncthreads();
   if (warp == kMmaWarp) {
@@ -1111,6 +1422,7 @@ void launch_prefill_t(const DataParams& p, cudaStream_t s) {
     cudaFuncSetAttribute(prefill_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2);
     cudaFuncSetAttribute(prefill_kernel_v3<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemV3);
     cudaFuncSetAttribute(prefill_kernel_v5<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemV5);
+    cudaFuncSetAttribute(prefill_kernel_v7<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemV7);
     attr = true;
   }
   int tiles = 1, heads = 1;
@@ -1120,7 +1432,7 @@ void launch_prefill_t(const DataParams& p, cudaStream_t s) {
   }
   static const int version = [] {
     const char* e = getenv("SEAKV_PREFILL_V");
-    return e ? atoi(e) : 3;  // v5 measured slower (824 vs 867 TFLOP/s at 16K), kept selectable
+    return e ? atoi(e) : 7;  // v7 measured fastest (profiles/r01_prefill_probe_v7.txt); 3 and 5 selectable
   }();
   if (version == 2 || !p.has_tmap) {
     dim3 grid(tiles, heads, p.nreq);
@@ -1128,6 +1440,9 @@ void launch_prefill_t(const DataParams& p, cudaStream_t s) {
   } else if (version == 3) {
     dim3 grid((tiles + 1) / 2, heads, p.nreq);
     prefill_kernel_v3<T><<<grid, kThreadsV3, kSmemV3, s>>>(p);
+  } else if (version == 7) {
+    dim3 grid((tiles + 1) / 2, heads, p.nreq);
+    prefill_kernel_v7<T><<<grid, kThreadsV3, kSmemV7, s>>>(p);
   } else {
     dim3 grid((tiles + 1) / 2, heads, p.nreq);
     prefill_kernel_v5<T><<<grid, kThreadsV3, kSmemV5, s>>>(p);

@@ -519,10 +519,11 @@ class Batch:
         self.cache._chk(self.cache._lib.skv_decode_attention(self.cache._h, self._h, C.byref(a),
                                                              _stream_ptr(stream)))
 
-    def decode_trace(self) -> np.ndarray:
+    def decode_trace(self, max_records: int = 4096) -> np.ndarray:
         """Debug (SKV_TRACE=1): per-warp [start_ns, after_wait_ns, end_ns, tiles<<32|items]
-        of the last decode launch; empty when tracing is off."""
-        buf = np.zeros((4096, 4), dtype=np.uint64)
+        of the last decode launch (or, for a prefill built with -DSKV_PF_TRACE, 16 u64 of
+        per-role wait cycles per CTA); empty when tracing is off."""
+        buf = np.zeros((max_records, 4), dtype=np.uint64)
         n = C.c_size_t()
         self.cache._chk(self.cache._lib.skv_debug_decode_trace(self.cache._h, self._h, buf.ctypes.data,
                                                                buf.size, C.byref(n)))

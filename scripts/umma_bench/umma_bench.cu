@@ -15,7 +15,7 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint
   d |= (uint64_t)2 << 61;
   return d;
 }
-__global__ void __launch_bounds__(128, 1) bench(int n, int iters, long long* out) {
+__global__ void __launch_bounds__(128, 1) bench(int n, int iters, int ts, long long* out) {
   extern __shared__ __align__(1024) char smem[];
   __shared__ uint32_t slot;
   __shared__ __align__(8) uint64_t bar;
@@ -38,11 +38,20 @@ __global__ void __launch_bounds__(128, 1) bench(int n, int iters, long long* out
     uint32_t idesc = (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
     const uint64_t a = make_desc(smem_u32(smem), 16, 1024), b = make_desc(smem_u32(smem + 32768), 16, 1024);
     long long t0 = clock64();
-    for (int i = 0; i < iters; ++i) {
-      asm volatile(
-          "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-          "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + (i & 1) * 256),
-          "l"(a), "l"(b), "r"(idesc), "r"(1));
+    if (ts) {  // A from TMEM columns [384, 392) (one K=16 step of a 128-row operand)
+      for (int i = 0; i < iters; ++i) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem + (i & 1) * 128),
+            "r"(tmem + 384 + (i & 7) * 8), "l"(b), "r"(idesc), "r"(1));
+      }
+    } else {
+      for (int i = 0; i < iters; ++i) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + (i & 1) * 256),
+            "l"(a), "l"(b), "r"(idesc), "r"(1));
+      }
     }
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar))
                  : "memory");
@@ -66,14 +75,16 @@ int main() {
   cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
   int clk = 0;
   cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+  for (int ts = 0; ts < 2; ++ts)
   for (int n : {64, 128, 256}) {
+    if (ts && n > 128) continue;
     const int iters = 4096;
     for (int rep = 0; rep < 2; ++rep) {
       cudaEvent_t e0, e1;
       cudaEventCreate(&e0);
       cudaEventCreate(&e1);
       cudaEventRecord(e0);
-      bench<<<148, 128, 100 * 1024>>>(n, iters, d);
+      bench<<<148, 128, 100 * 1024>>>(n, iters, ts, d);
       cudaEventRecord(e1);
       cudaError_t err = cudaDeviceSynchronize();
       if (err != cudaSuccess) { printf("err %s\n", cudaGetErrorString(err)); return 1; }
@@ -85,7 +96,7 @@ int main() {
       for (int i = 0; i < 148; ++i) cyc += h[i];
       cyc /= 148;
       const double macs = 128.0 * n * 16;
-      printf("N=%d: %.1f clk/MMA, %.0f MAC/clk/SM, event %.3f ms -> %.1f TFLOP/s (all SMs)\n", n, cyc / iters,
+      printf("%s N=%d: %.1f clk/MMA, %.0f MAC/clk/SM, event %.3f ms -> %.1f TFLOP/s (all SMs)\n", ts ? "TS" : "SS", n, cyc / iters,
              macs * iters / cyc, ms, 2 * macs * iters * 148 / (ms * 1e-3) / 1e12);
     }
   }
