@@ -171,11 +171,11 @@ __device__ __forceinline__ void consume_tile(const char* tile, int lane, int val
     float kf[8];
     Cvt<T>::to_f32(raw, kf);
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-      float a = 0.f;
+    for (int g = 0; g < G; ++g) {  // packed fp32 FMA (FFMA2): 4 + 1 instructions per 8 dims
+      float2 a = __fmul2_rn(make_float2(q[g][0], q[g][1]), make_float2(kf[0], kf[1]));
 #pragma unroll
-      for (int j = 0; j < 8; ++j) a = fmaf(q[g][j], kf[j], a);
-      part[g][i] = a;
+      for (int j = 2; j < 8; j += 2) a = __ffma2_rn(make_float2(q[g][j], q[g][j + 1]), make_float2(kf[j], kf[j + 1]), a);
+      part[g][i] = a.x + a.y;
     }
   }
   const int tok = 2 * ((c >> 1) & 7) + hf;
@@ -193,8 +193,13 @@ __device__ __forceinline__ void consume_tile(const char* tile, int lane, int val
     const float alpha = exp2f(mx[g] - mnew);
     p[g] = exp2f(s - mnew);
     l[g] = l[g] * alpha + p[g];
+    const float2 a2 = make_float2(alpha, alpha);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) o[g][j] *= alpha;
+    for (int j = 0; j < 8; j += 2) {
+      const float2 r = __fmul2_rn(make_float2(o[g][j], o[g][j + 1]), a2);
+      o[g][j] = r.x;
+      o[g][j + 1] = r.y;
+    }
     mx[g] = mnew;
   }
   const char* vt = tile + kTpb * kD * 2;
@@ -208,8 +213,13 @@ __device__ __forceinline__ void consume_tile(const char* tile, int lane, int val
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const float pt = __shfl_sync(0xffffffffu, p[g], src);
+      const float2 pt2 = make_float2(pt, pt);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) o[g][j] = fmaf(pt, vf[j], o[g][j]);
+      for (int j = 0; j < 8; j += 2) {
+        const float2 r = __ffma2_rn(pt2, make_float2(vf[j], vf[j + 1]), make_float2(o[g][j], o[g][j + 1]));
+        o[g][j] = r.x;
+        o[g][j + 1] = r.y;
+      }
     }
   }
 }
