@@ -167,3 +167,24 @@ def test_split_fused_append_decode_and_grow():
             pos = (c - 1) % 16
             assert np.array_equal(blk[0, pos], k[i, 0, h].cpu().numpy())
             assert np.array_equal(blk[1, pos], v[i, 0, h].cpu().numpy())
+
+
+def test_split_tp2_tables_hold_rank_heads_and_stats_follow_reference():
+    """tp=2: each rank's split tables hold L x H/tp rows per native block; the accounting
+    (SplitCacheCounter) counts L x num_heads entries as the reference does (it has no tp)."""
+    shapes = [(3, 8, 16), (2, 4, 4)]
+    sp = P.SplitKvCache(_models(shapes), 16, 2, 4096, max_requests=16, max_blocks_per_request=16)
+    ops = [(0, 1, 0, 40), (0, 2, 1, 17), (0, 1, 0, 70), (1, 2, 0, 0), (0, 3, 1, 5)]
+    for kind, rid, m, t in ops:
+        if kind == 0:
+            assert sp.grow([rid], [m], [t]).all()
+        else:
+            sp.free([rid])
+    _, split = O.compare_schemes([(L, H, D, 2) for L, H, _ in shapes], ops, pool=4096)
+    assert sp.stats()["block_table_entries"] == split["block_table_entries"]
+    assert sp.stats()["native_reads_writes"] == split["native_reads_writes"]
+    used = 5 * 3 * (8 // 2) + 1 * 2 * (4 // 2)  # request 1: 5 blocks x 3 layers x 4 heads/rank
+    assert sp.pool_size() - sp.free_blocks() == used
+    assert len(sp.block_ids(1, 2, 3)) == 5
+    with pytest.raises(P.ArgError):
+        sp.block_ids(1, 0, 4)  # only H/tp = 4 kv heads on this rank
