@@ -588,6 +588,9 @@ def run_churn(args):
                                f"Poisson rate {args.rate}/s, skewness 4, rate x2 at half time, chunk 512, "
                                f"occupancy target 0.70, faithful pool {pool} merged blocks ({args.pool_gb} GB)"},
         "churn": summ, "gpu_launches": int(cache.kernel_launches() - launches0), "clocks": clk.summary(),
+        "note": "eager, host-driven engine: value = decode bytes / sum of per-launch event intervals, which "
+                "include host submission gaps (churn.data_path_ms is the GPU span of each step); the "
+                "kernel-level decode figures are the config 1/2/4 lines",
     }
     print(json.dumps(res), flush=True)
 
