@@ -892,7 +892,7 @@ static skv_status batch_fill(skv_pool* p, skv_batch* b, const int32_t* group_mod
   }
   if (!b->d_nitems) {
     skv_status st;
-    if ((st = dev_alloc(p, &b->d_nitems, 1)) || (st = dev_alloc(p, &b->d_counter, 4))) return st;
+    if ((st = dev_alloc(p, &b->d_nitems, 1)) || (st = dev_alloc(p, &b->d_counter, 6))) return st;  // [0..3] decode sets, [4] prefill items
   }
   if (total) {
     // stage through pinned memory on the pool stream (wait for the previous upload first)
@@ -1237,6 +1237,7 @@ skv_status skv_prefill_attention(skv_pool* p, skv_batch* b, const skv_prefill_ar
     return e ? atoi(e) : 0;
   }();
   dp.dbg = dbg;
+  dp.counter = b->d_counter + 4;  // persistent prefill work counter (reset per launch)
   static const bool trace_on = [] {
     const char* e = getenv("SKV_TRACE");
     return e && e[0] == '1';

@@ -25,6 +25,7 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
@@ -1107,6 +1108,328 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v7(const __grid_
 }
 
 // ---------------------------------------------------------------------------------------
+// v9: persistent v7 with dynamic scheduling.  One CTA per SM; the TMA warp draws work
+// items (request, kv head, query-tile pair), longest first, from a global counter and
+// publishes them through an 8-slot ring in shared memory (item_full[slot] barriers), so
+// every role walks the same sequence without per-CTA setup: TMEM, barriers and the CTA
+// launch are paid once per SM, and the next item's K/V streams in (and its Q rows are
+// written) while the current item drains.  All barrier phases run on CTA-global counters
+// (jt: key tiles, it: items).
+constexpr int kRing9 = 8;
+constexpr int kSmemV9 = kSmemV7 + 128;  // + item ring and its barriers
+
+// item order: (request, kv head) major, query-tile pair descending minor, so the pairs of
+// one (request, head) -- which read the same K/V -- run at the same time on different SMs
+// (L2 reuse) and each group starts with its longest pair
+__device__ __forceinline__ bool prefill_item9(const DataParams& p, int i, int npairs, int hmax, int& r, int& h,
+                                              int& pair) {
+  pair = npairs - 1 - i % npairs;
+  const int rem = i / npairs;
+  h = rem % hmax;
+  r = rem / hmax;
+  const DataGroup& g = p.g[p.req_group[r]];
+  return g.active && h < g.Hkv && 2 * pair * kRows < p.n_new * g.G;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v9(const __grid_constant__ DataParams p, int npairs,
+                                                                    int hmax) {
+  extern __shared__ __align__(1024) char smem[];
+  if (smem_u32(smem) & 1023) __trap();
+  char* kvbase = smem;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(kvbase + kStagesV7 * 2 * kKVBytes);
+  uint64_t* kv_full = bars;                       // [stages]
+  uint64_t* kv_empty = bars + kStagesV7;          // [stages]
+  uint64_t* q_full = bars + 2 * kStagesV7;        // count 256 (per item)
+  uint64_t* s_full = bars + 2 * kStagesV7 + 1;    // [tile]
+  uint64_t* p_full = bars + 2 * kStagesV7 + 3;    // [tile] count 128
+  uint64_t* pv_done = bars + 2 * kStagesV7 + 5;   // [tile]
+  uint64_t* item_full = bars + 2 * kStagesV7 + 7; // [kRing9]
+  int* ring = reinterpret_cast<int*>(bars + 2 * kStagesV7 + 7 + kRing9);  // [kRing9]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + kRing9);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n_items = npairs * hmax * p.nreq;
+  const int q_len = p.n_new;
+
+  if (warp == kMmaWarp) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < kStagesV7; ++i) {
+      mbar_init_n(&kv_full[i], 1);
+      mbar_init_n(&kv_empty[i], 1);
+    }
+    mbar_init_n(q_full, 2 * 128);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init_n(&s_full[i], 1);
+      mbar_init_n(&p_full[i], 128);
+      mbar_init_n(&pv_done[i], 1);
+    }
+    for (int i = 0; i < kRing9; ++i) mbar_init_n(&item_full[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  struct Geo {
+    int r, h, pair, handle, ctx, start, tpt, t0A, n_keys, n_kt, rl, G;
+    const DataGroup* g;
+  };
+  auto geo = [&](int idx) {
+    Geo e;
+    prefill_item9(p, idx, npairs, hmax, e.r, e.h, e.pair);
+    e.g = &p.g[p.req_group[e.r]];
+    e.G = e.g->G;
+    e.handle = p.handles[e.r];
+    e.ctx = p.req_tokens[e.handle];
+    e.start = e.ctx - q_len;
+    e.tpt = kRows / e.G;
+    e.t0A = 2 * e.pair * e.tpt;
+    e.n_keys = min(e.ctx, e.start + e.t0A + 2 * e.tpt);
+    e.n_kt = (e.n_keys + kKT - 1) / kKT;
+    e.rl = e.r - e.g->req_begin;
+    return e;
+  };
+  // consumers: the k-th item of this CTA (-1 = no more work)
+  auto next_item = [&](uint32_t k) {
+    mbar_wait(&item_full[k % kRing9], (k / kRing9) & 1);
+    return *reinterpret_cast<volatile int*>(&ring[k % kRing9]);
+  };
+
+  if (warp == kLoadWarp) {  // ----------------------------------------- scheduler + K/V streaming
+    if (lane == 0) {
+      uint32_t jt = 0;
+      for (uint32_t k = 0;; ++k) {
+        int idx = atomicAdd(p.counter, 1);
+        while (idx < n_items) {  // skip holes of the (pair, head, request) grid
+          int r_, h_, pr_;
+          if (prefill_item9(p, idx, npairs, hmax, r_, h_, pr_)) break;
+          idx = atomicAdd(p.counter, 1);
+        }
+        const int pub = idx < n_items ? idx : -1;
+        ring[k % kRing9] = pub;
+        asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&item_full[k % kRing9]))
+                     : "memory");
+        if (pub < 0) break;
+        const Geo e = geo(pub);
+        const int2* row_tab = p.req_table + (size_t)e.handle * p.cap;
+        const long long base_off = e.g->layer_off + (long long)e.h * e.g->head_stride;
+        const int n_blk = (e.n_keys + kTpb - 1) / kTpb;
+        for (int j = 0; j < e.n_kt; ++j, ++jt) {
+          const int st = jt % kStagesV7;
+          if (jt >= (uint32_t)kStagesV7) mbar_wait(&kv_empty[st], ((jt / kStagesV7) - 1) & 1);
+          int2 eb[4];
+          int nb = 0;
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            const int bi = j * 4 + b;
+            eb[b] = bi < n_blk ? row_tab[bi] : make_int2(-1, 0);
+            nb += bi < n_blk;
+          }
+          mbar_expect_tx_v3(&kv_full[st], nb * 4 * 2048);
+          const uint32_t sK = smem_u32(kvbase + st * 2 * kKVBytes), sV = sK + kKVBytes;
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            if (eb[b].x < 0) continue;
+            const int row0 = (int)(((long long)eb[b].x * p.merged_stride + (long long)eb[b].y * e.g->native_stride +
+                                    base_off) >> 8);
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              tma_load_2d(sK + hh * kKVHalf + b * 2048, &p.kv_tmap, hh * 64, row0, &kv_full[st]);
+              tma_load_2d(sV + hh * kKVHalf + b * 2048, &p.kv_tmap, hh * 64, row0 + kTpb, &kv_full[st]);
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == kMmaWarp) {  // -------------------------------------------- MMA issue
+    if (lane == 0) {
+      const uint32_t idesc_qk = make_idesc_n(p.dtype, 0, kKT);
+      const uint32_t idesc_pv = make_idesc_n(p.dtype, 1, kD);
+      uint32_t jt = 0;
+      for (uint32_t k = 0;; ++k) {
+        const int idx = next_item(k);
+        if (idx < 0) break;
+        const Geo e = geo(idx);
+        const uint32_t j0 = jt;
+        auto qk = [&](int x, int j) {
+          const uint32_t sK = smem_u32(kvbase + ((j0 + j) % kStagesV7) * 2 * kKVBytes);
+#pragma unroll
+          for (int kk = 0; kk < kD / 16; ++kk) {
+            const uint32_t koff = (kk >> 2) * kKVHalf + (kk & 3) * 32;
+            mma_f16_ts(tmem + 128 + x * 64, tmem + x * 64 + kk * 8, make_desc(sK + koff, 16, 1024), idesc_qk, kk > 0);
+          }
+          mma_commit(&s_full[x]);
+        };
+        auto pv = [&](int x, int j) {
+          const uint32_t sV = smem_u32(kvbase + ((j0 + j) % kStagesV7) * 2 * kKVBytes + kKVBytes);
+#pragma unroll
+          for (int kk = 0; kk < kKT / 16; ++kk)
+            mma_f16_ts(tmem + 256 + x * 128, tmem + 128 + x * 64 + kk * 8, make_desc(sV + kk * 2048, kKVHalf, 1024),
+                       idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
+          mma_commit(&pv_done[x]);
+        };
+        auto wait_kv = [&](int j) {
+          const uint32_t gj = j0 + j;
+          mbar_wait(&kv_full[gj % kStagesV7], (gj / kStagesV7) & 1);
+          tc_fence_after();
+        };
+        mbar_wait(q_full, k & 1);
+        tc_fence_after();
+        wait_kv(0);
+        qk(0, 0);
+        qk(1, 0);
+        for (int j = 0; j < e.n_kt; ++j) {
+          const uint32_t gj = j0 + j;
+          mbar_wait(&p_full[0], gj & 1);
+          tc_fence_after();
+          pv(0, j);
+          if (j + 1 < e.n_kt) {
+            wait_kv(j + 1);
+            qk(0, j + 1);
+          }
+          mbar_wait(&p_full[1], gj & 1);
+          tc_fence_after();
+          pv(1, j);
+          mma_commit(&kv_empty[gj % kStagesV7]);
+          if (j + 1 < e.n_kt) qk(1, j + 1);
+        }
+        jt += e.n_kt;
+      }
+    }
+    __syncwarp();
+  } else {  // ------------------------------------------------------------- softmax warps
+    const int x = warp >> 2;
+    const int row = tid & 127;
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const uint32_t tQ = tmem + x * 64 + lane_off, tS = tmem + 128 + x * 64 + lane_off;
+    const uint32_t tO = tmem + 256 + x * 128 + lane_off;
+    const float c2 = p.scale_log2;
+    uint32_t jt = 0;
+    for (uint32_t k = 0;; ++k) {
+      const int idx = next_item(k);
+      if (idx < 0) break;
+      const Geo e = geo(idx);
+      const int t0 = e.t0A + x * e.tpt;
+      const int my_tok = t0 + row / e.G;
+      const bool row_ok = my_tok < q_len;
+      const int my_pos = e.start + my_tok;
+      const bool tail_rows = t0 + e.tpt > q_len;
+      {  // Q rows of this item (the previous item's QK^T all retired: its S tiles were consumed)
+        const uint4* src = reinterpret_cast<const uint4*>(
+            reinterpret_cast<const char*>(e.g->q) +
+            (((size_t)e.rl * q_len + (row_ok ? my_tok : 0)) * e.g->Hq + e.h * e.G + row % e.G) * (kD * 2));
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          uint32_t qv[32];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const uint4 v = row_ok ? src[hh * 8 + i] : make_uint4(0u, 0u, 0u, 0u);
+            qv[4 * i] = v.x;
+            qv[4 * i + 1] = v.y;
+            qv[4 * i + 2] = v.z;
+            qv[4 * i + 3] = v.w;
+          }
+          tmem_st32u(tQ + hh * 32, qv);
+        }
+        tc_fence_before();
+        mbar_arrive(q_full);
+      }
+      float m = -INFINITY, l = 0.f;
+      const uint32_t j0 = jt;
+      for (int j = 0; j < e.n_kt; ++j) {
+        const uint32_t gj = j0 + j;
+        mbar_wait(&s_full[x], gj & 1);
+        tc_fence_after();
+        if (x == 0 && j == e.n_kt - 1 && (j + 1) * kKT > e.n_keys) {
+          char* sV = kvbase + (gj % kStagesV7) * 2 * kKVBytes + kKVBytes;
+          const int c = row & 15;
+          for (int key = row >> 4; key < kKT; key += 8)
+            if (j * kKT + key >= e.n_keys) *reinterpret_cast<uint4*>(sV + sw_kv(key, c)) = make_uint4(0, 0, 0, 0);
+        }
+        float s[64];
+        tmem_ld64(tS, s);
+        const bool masked = (j * kKT + kKT - 1 > e.start + t0) || tail_rows;
+        if (masked) {
+#pragma unroll
+          for (int kk = 0; kk < 64; ++kk)
+            if (!(row_ok && j * kKT + kk <= my_pos)) s[kk] = -INFINITY;
+        }
+        float mx4[4] = {s[0], s[1], s[2], s[3]};
+#pragma unroll
+        for (int kk = 4; kk < 64; ++kk) mx4[kk & 3] = fmaxf(mx4[kk & 3], s[kk]);
+        const float mt = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * c2;
+        const bool need = mt > m + kRescale;
+        float alpha = 1.f;
+        if (need) {
+          alpha = ex2(m - mt);
+          l *= alpha;
+          m = mt;
+        }
+        if (j > 0 && __any_sync(0xffffffffu, need)) {
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) {
+            float o[32];
+            tmem_ld32(tO + cc * 32, o);
+#pragma unroll
+            for (int kk = 0; kk < 32; ++kk) o[kk] *= alpha;
+            tmem_st32(tO + cc * 32, o);
+          }
+        }
+        const float mu = (m == -INFINITY) ? 0.f : m;
+        float ls[4] = {0.f, 0.f, 0.f, 0.f};
+        uint32_t pk[32];
+#pragma unroll
+        for (int kk = 0; kk < 64; kk += 2) {
+          const float v0 = ex2(fmaf(s[kk], c2, -mu));
+          const float v1 = ex2(fmaf(s[kk + 1], c2, -mu));
+          ls[(kk >> 1) & 3] += v0 + v1;
+          pk[kk >> 1] = pack2<T>(v0, v1);
+        }
+        tmem_st32u(tS, pk);
+        l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+        fence_async_smem();
+        tc_fence_before();
+        mbar_arrive(&p_full[x]);
+      }
+      const uint32_t gl = j0 + e.n_kt - 1;
+      mbar_wait(&pv_done[x], gl & 1);
+      tc_fence_after();
+      jt += e.n_kt;
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      char* dst = reinterpret_cast<char*>(e.g->out) +
+                  (((size_t)e.rl * q_len + (row_ok ? my_tok : 0)) * e.g->Hq + e.h * e.G + row % e.G) * (kD * 2);
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        float o[32];
+        tmem_ld32(tO + cc * 32, o);
+        if (row_ok) {
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            uint4 v;
+            v.x = pack2<T>(o[8 * q4] * inv, o[8 * q4 + 1] * inv);
+            v.y = pack2<T>(o[8 * q4 + 2] * inv, o[8 * q4 + 3] * inv);
+            v.z = pack2<T>(o[8 * q4 + 4] * inv, o[8 * q4 + 5] * inv);
+            v.w = pack2<T>(o[8 * q4 + 6] * inv, o[8 * q4 + 7] * inv);
+            *reinterpret_cast<uint4*>(dst + cc * 64 + q4 * 16) = v;
+          }
+        }
+      }
+      tc_fence_before();  // the next item's first P.V (after our p_full arrive) overwrites O
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kMmaWarp) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// ---------------------------------------------------------------------------------------
 // v5 (experimental, SEAKV_PREFILL_V=5): 128-key tiles.  A 128x64x16 UMMA runs at 2/3 of
 // the tensor core's rate (measured: 48 clk vs 64 clk for N=128, scripts/umma_bench), so
 // S = Q.K^T uses N = 128 keys and P.V uses K = 128 keys.  TMEM: S_A | S_B | O_A | O_B
@@ -1424,6 +1747,7 @@ void launch_prefill_t(const DataParams& p, cudaStream_t s) {
     cudaFuncSetAttribute(prefill_kernel_v3<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemV3);
     cudaFuncSetAttribute(prefill_kernel_v5<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemV5);
     cudaFuncSetAttribute(prefill_kernel_v7<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemV7);
+    cudaFuncSetAttribute(prefill_kernel_v9<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemV9);
     attr = true;
   }
   int tiles = 1, heads = 1;
@@ -1433,7 +1757,7 @@ void launch_prefill_t(const DataParams& p, cudaStream_t s) {
   }
   static const int version = [] {
     const char* e = getenv("SEAKV_PREFILL_V");
-    return e ? atoi(e) : 7;  // v7 measured fastest (profiles/r01_prefill_probe_v7.txt); 3 and 5 selectable
+    return e ? atoi(e) : 9;  // v9 measured fastest (profiles/r01_prefill_probe_v9.txt); 3, 5, 7 selectable
   }();
   if (version == 2 || !p.has_tmap) {
     dim3 grid(tiles, heads, p.nreq);
@@ -1441,6 +1765,15 @@ void launch_prefill_t(const DataParams& p, cudaStream_t s) {
   } else if (version == 3) {
     dim3 grid((tiles + 1) / 2, heads, p.nreq);
     prefill_kernel_v3<T><<<grid, kThreadsV3, kSmemV3, s>>>(p);
+  } else if (version == 9) {
+    const int npairs = (tiles + 1) / 2;
+    int nsm = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const long long items = (long long)npairs * heads * p.nreq;
+    const int grid = (int)std::min<long long>(items, nsm);
+    cudaMemsetAsync(p.counter, 0, sizeof(int), s);
+    prefill_kernel_v9<T><<<grid, kThreadsV3, kSmemV9, s>>>(p, npairs, heads);
   } else if (version == 7) {
     dim3 grid((tiles + 1) / 2, heads, p.nreq);
     prefill_kernel_v7<T><<<grid, kThreadsV3, kSmemV7, s>>>(p);
