@@ -29,8 +29,14 @@ namespace {
 constexpr int kD = 128;                       // head_dim handled by the kernels
 constexpr int kTpb = 16;                      // tokens per native block
 constexpr int kTile = 2 * kTpb * kD * 2;      // K + V tile bytes (8 KiB)
-constexpr int kWarps = 8;
-constexpr int kStages = 3;
+#ifndef SKV_DEC_WARPS
+#define SKV_DEC_WARPS 8
+#endif
+#ifndef SKV_DEC_STAGES
+#define SKV_DEC_STAGES 3
+#endif
+constexpr int kWarps = SKV_DEC_WARPS;    // independent warps per CTA (one CTA per SM)
+constexpr int kStages = SKV_DEC_STAGES;  // 8 KiB tiles in flight per warp
 constexpr int kRing = 16;
 constexpr float kLog2e = 1.4426950408889634f;
 
@@ -777,6 +783,7 @@ void launch_decode_t(const DataParams& p, int grid, cudaStream_t s) {
 }  // namespace
 
 int decode_ctas_per_sm() { return 1; }
+int decode_warps_per_cta() { return kWarps; }
 
 void launch_decode_plan(const DataParams& p, cudaStream_t s) {
   launch_pdl(plan_kernel, dim3(1), dim3(1024), 0, s, p);

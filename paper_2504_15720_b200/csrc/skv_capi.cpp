@@ -1090,7 +1090,7 @@ skv_status skv_decode_attention(skv_pool* p, skv_batch* b, const skv_decode_args
   // keep every warp slot busy (~4 pieces per slot).
   int nsm = 148;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p->device);
-  const long long slots8 = (long long)nsm * 8 * skv::decode_ctas_per_sm();
+  const long long slots8 = (long long)nsm * skv::decode_warps_per_cta() * skv::decode_ctas_per_sm();
   int split = a->split_tokens;
   if (split < 0) return fail(p, SKV_ERR_ARG, "decode: split_tokens must be >= 0");
   // Measured on B200 (scripts/sweep_sched.sh, profiles/r01_sweep_sched.txt): chunk when

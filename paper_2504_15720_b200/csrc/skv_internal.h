@@ -157,5 +157,6 @@ void launch_prefill(const DataParams& p, cudaStream_t s);
 void launch_synth_fill(void* pool, size_t bytes, int dtype, unsigned long long seed, float amp,
                        cudaStream_t s);
 int decode_ctas_per_sm();
+int decode_warps_per_cta();
 
 }  // namespace skv
