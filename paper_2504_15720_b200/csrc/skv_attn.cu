@@ -138,6 +138,25 @@ struct Cvt<__nv_bfloat16> {
   }
 };
 
+// fp32 += 16-bit x 16-bit (one FHFMA: the half/bf16 operands are read straight from the
+// packed register halves, no conversion instructions; the product is exact in fp32)
+template <typename T>
+struct MixFma;
+template <>
+struct MixFma<__half> {
+  __device__ __forceinline__ static float f(float c, unsigned short a, unsigned short b) {
+    asm("fma.rn.f32.f16 %0, %1, %2, %0;" : "+f"(c) : "h"(a), "h"(b));
+    return c;
+  }
+};
+template <>
+struct MixFma<__nv_bfloat16> {
+  __device__ __forceinline__ static float f(float c, unsigned short a, unsigned short b) {
+    asm("fma.rn.f32.bf16 %0, %1, %2, %0;" : "+f"(c) : "h"(a), "h"(b));
+    return c;
+  }
+};
+
 // Sum of 8 per-lane partials over the 16 lanes of a half-warp, scattered so lane
 // (c = lane&15) ends up with the total of index (c>>1)&7 (8 shuffles, not 32).
 __device__ __forceinline__ float reduce_scatter16(const float (&v)[8], int lane) {
@@ -237,6 +256,57 @@ __device__ __forceinline__ const int2* table_row(const DataParams& p, int handle
                    : p.req_table + (size_t)handle * p.cap;
 }
 
+// G = 1 (MHA) variant of consume_tile: q stays in 16-bit (qraw, this lane's 8 dims) and
+// both dot products run as mixed-precision FMAs (fp32 accumulate, 16-bit operands), so
+// neither K nor V is converted; P is rounded to the 16-bit type for P.V, as the tensor-core
+// prefill does.  About 30 % fewer instructions per tile than the converting path.
+template <typename T, bool PARTIAL>
+__device__ __forceinline__ void consume_tile_mha(const char* tile, int lane, int valid, const uint4& qraw,
+                                                 float scale_log2, float (&o)[8], float& mx, float& l) {
+  const int c = lane & 15, hf = lane >> 4;
+  const unsigned short* qh = reinterpret_cast<const unsigned short*>(&qraw);
+  float part[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint4 raw = *reinterpret_cast<const uint4*>(tile + (2 * i + hf) * (kD * 2) + c * 16);
+    const unsigned short* kh = reinterpret_cast<const unsigned short*>(&raw);
+    float a = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a = MixFma<T>::f(a, qh[j], kh[j]);
+    part[i] = a;
+  }
+  const int tok = 2 * ((c >> 1) & 7) + hf;
+  float sc = reduce_scatter16(part, lane) * scale_log2;
+  if (tok >= valid) sc = -INFINITY;
+  float bm = sc;
+  bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 2));
+  bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 4));
+  bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 8));
+  bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 16));
+  const float mnew = fmaxf(mx, bm);
+  const float alpha = exp2f(mx - mnew);
+  const float pr = exp2f(sc - mnew);
+  l = l * alpha + pr;
+  const float2 a2 = make_float2(alpha, alpha);
+#pragma unroll
+  for (int j = 0; j < 8; j += 2) {
+    const float2 r = __fmul2_rn(make_float2(o[j], o[j + 1]), a2);
+    o[j] = r.x;
+    o[j + 1] = r.y;
+  }
+  mx = mnew;
+  const char* vt = tile + kTpb * kD * 2;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    uint4 raw = *reinterpret_cast<const uint4*>(vt + (2 * i + hf) * (kD * 2) + c * 16);
+    if (PARTIAL && 2 * i + hf >= valid) raw = make_uint4(0u, 0u, 0u, 0u);  // unwritten slots may hold NaN
+    const unsigned short* vh = reinterpret_cast<const unsigned short*>(&raw);
+    const unsigned short ph = Cvt<T>::one(__shfl_sync(0xffffffffu, pr, (hf << 4) | (i << 1)));
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = MixFma<T>::f(o[j], ph, vh[j]);
+  }
+}
+
 // Per-warp producer: walks the same item sequence as the consumer, kStages tiles ahead.
 struct Producer {
   int idx;         // current item, -1 before the first
@@ -318,10 +388,12 @@ __device__ __forceinline__ void process_item(const DataParams& p, Producer& P, c
   const DataGroup& g = p.g[grp];
   const int rl = it.x - g.req_begin;
   float q[G][8], o[G][8], mx[G], l[G];
+  uint4 qraw = make_uint4(0u, 0u, 0u, 0u);  // G = 1: this lane's 8 raw query dims
 #pragma unroll
   for (int gg = 0; gg < G; ++gg) {
     const T* qp = reinterpret_cast<const T*>(g.q) + ((size_t)rl * g.Hq + head * G + gg) * kD;
     const uint4 raw = *reinterpret_cast<const uint4*>(qp + c * 8);
+    if (G == 1) qraw = raw;
     Cvt<T>::to_f32(raw, q[gg]);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
@@ -359,8 +431,15 @@ __device__ __forceinline__ void process_item(const DataParams& p, Producer& P, c
       __syncwarp();
     }
     const int valid = min(kTpb, it.w - b * kTpb);
-    if (valid == kTpb) consume_tile<T, G, false>(w.tiles + stage * kTile, lane, valid, q, o, mx, l);
-    else consume_tile<T, G, true>(w.tiles + stage * kTile, lane, valid, q, o, mx, l);
+    if constexpr (G == 1) {
+      if (valid == kTpb)
+        consume_tile_mha<T, false>(w.tiles + stage * kTile, lane, valid, qraw, p.scale_log2, o[0], mx[0], l[0]);
+      else
+        consume_tile_mha<T, true>(w.tiles + stage * kTile, lane, valid, qraw, p.scale_log2, o[0], mx[0], l[0]);
+    } else {
+      if (valid == kTpb) consume_tile<T, G, false>(w.tiles + stage * kTile, lane, valid, q, o, mx, l);
+      else consume_tile<T, G, true>(w.tiles + stage * kTile, lane, valid, q, o, mx, l);
+    }
     __syncwarp();
     P.consumed++;
     fill(p, P, w);
