@@ -4,12 +4,19 @@
 // serving metrics, and a hash of every request's outcome.  Built twice by
 // oracle/Makefile: against the reference kv_cache.hpp (sim_ref) and against the
 // GPU drop-in (sim_dropin); the two outputs must be identical.
+//
+// Optional 4th argument: an INI file of [cost <model> tp=<n>] sections (the reference's
+// own format, config.hpp:311-328) that replaces default_cost_model entries -- e.g. the
+// B200-measured decode attention cost written by scripts/calibrate_cost.py, so the
+// reference simulator prices decode with this repository's measured kernel time.
 #include <cinttypes>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <fstream>
 #include <vector>
 
+#include "seasim/config.hpp"
 #include "seasim/simulation.hpp"
 
 using namespace seasim;
@@ -43,7 +50,30 @@ int main(int argc, char** argv) {
   const double rate = argc > 1 ? std::atof(argv[1]) : 6.0;
   const double duration = argc > 2 ? std::atof(argv[2]) : 30.0;
   const double pool_gb = argc > 3 ? std::atof(argv[3]) : 2.0;
-  const CostModel cost = default_cost_model();
+  CostModel cost = default_cost_model();
+  if (argc > 4) {  // measured cost overrides, parsed with the reference's INI reader
+    std::ifstream in(argv[4]);
+    if (!in) {
+      std::fprintf(stderr, "cannot open %s\n", argv[4]);
+      return 2;
+    }
+    const detail::IniFile ini = detail::parse_ini(in, argv[4]);
+    for (const auto* sec : ini.all("cost")) {
+      std::istringstream hs(sec->header);
+      std::string word, model_id, tp_word;
+      hs >> word >> model_id >> tp_word;
+      detail::SectionView view(sec, sec->header);
+      CostCoeffs c;
+      c.prefill_fixed = view.num("prefill_fixed", 0.0);
+      c.prefill_per_token = view.num("prefill_per_token", 0.0);
+      c.decode_fixed = view.num("decode_fixed", 0.0);
+      c.decode_per_seq = view.num("decode_per_seq", 0.0);
+      c.decode_per_context_token = view.num("decode_per_context_token", 0.0);
+      c.activation_base = view.num("activation_base_gb", 0.5) * kGiB;
+      c.activation_per_seq = view.num("activation_per_seq_gb", 0.02) * kGiB;
+      cost.add_entry(model_id, std::stoi(tp_word.substr(3)), c);
+    }
+  }
   std::vector<ServiceProfile> profiles = {
       service(cost, "chat-7b", "llama2-7b", 73.0, 40.0, 427.0, 200.0),
       service(cost, "summ-13b", "llama2-13b", 2000.0, 600.0, 21.0, 8.0),

@@ -262,7 +262,10 @@ SIM_DROPIN = __import__("os").path.join(__import__("os").path.dirname(O.REF_TEST
 
 @pytest.mark.skipif(not (__import__("os").path.exists(SIM_REF) and __import__("os").path.exists(SIM_DROPIN)),
                     reason="simulator binaries not built")
-@pytest.mark.parametrize("args", [("6", "30", "2.0"), ("12", "20", "1.0")])
+_B200_COST = __import__("os").path.join(__import__("os").path.dirname(__file__), "..", "profiles", "r01_b200_cost.ini")
+
+
+@pytest.mark.parametrize("args", [("6", "30", "2.0"), ("12", "20", "1.0"), ("6", "30", "2.0", _B200_COST)])
 def test_reference_simulator_identical_with_gpu_cache(args):
     """simulation.hpp (event loop, EngineGate::acquire -> can_grow_to/try_allocate, evictions,
     free_request) built once with the reference kv_cache.hpp and once with the GPU drop-in:
@@ -274,3 +277,6 @@ def test_reference_simulator_identical_with_gpu_cache(args):
     assert a.returncode == 0 and b.returncode == 0, b.stderr
     assert a.stdout == b.stdout
     assert "engine 1 kv entries" in b.stdout
+    if len(args) > 3:  # B200-measured decode attention cost changes the schedule, not the parity
+        base = subprocess.run([SIM_REF, *args[:3]], capture_output=True, text=True, timeout=300)
+        assert base.stdout != a.stdout
