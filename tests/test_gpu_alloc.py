@@ -260,11 +260,11 @@ SIM_REF = __import__("os").path.join(__import__("os").path.dirname(O.REF_TEST_BI
 SIM_DROPIN = __import__("os").path.join(__import__("os").path.dirname(O.REF_TEST_BIN), "sim_dropin")
 
 
-@pytest.mark.skipif(not (__import__("os").path.exists(SIM_REF) and __import__("os").path.exists(SIM_DROPIN)),
-                    reason="simulator binaries not built")
 _B200_COST = __import__("os").path.join(__import__("os").path.dirname(__file__), "..", "profiles", "r01_b200_cost.ini")
 
 
+@pytest.mark.skipif(not (__import__("os").path.exists(SIM_REF) and __import__("os").path.exists(SIM_DROPIN)),
+                    reason="simulator binaries not built")
 @pytest.mark.parametrize("args", [("6", "30", "2.0"), ("12", "20", "1.0"), ("6", "30", "2.0", _B200_COST)])
 def test_reference_simulator_identical_with_gpu_cache(args):
     """simulation.hpp (event loop, EngineGate::acquire -> can_grow_to/try_allocate, evictions,
