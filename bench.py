@@ -366,10 +366,11 @@ def run_gpu(args):
 
     # ---- e2e through the C-ABI with host buffers -----------------------------------------
     # Every step copies its inputs (q, k, v of every layer: [NLAYERS, B, H, d] per group)
-    # from pinned host memory and reads every layer's attention output back.  Device
-    # buffers are double-buffered per step: the H2D of step i (h2d stream) overlaps the
-    # attention of step i-1, the D2H of step i (d2h stream) overlaps step i+1, and the
-    # NLAYERS launches of a step run back to back on the compute stream.
+    # from pinned host memory and reads every layer's attention output back, in 4 chunks
+    # of layers: the H2D of chunk c+1 (h2d stream) overlaps the attention of chunk c, whose
+    # outputs go back (d2h stream) while chunk c+1 runs; within a chunk the launches stay
+    # back to back (no event between them, so programmatic dependent launch still
+    # overlaps them).  Device buffers are double-buffered by step parity.
     def pinned_like(x):
         return torch.empty((NLAYERS,) + tuple(x.shape), dtype=x.dtype, pin_memory=True)
 
@@ -388,9 +389,12 @@ def run_gpu(args):
     dk = [[torch.empty(x.shape, dtype=x.dtype, device=local) for x in hk] for _ in range(2)]
     dv = [[torch.empty(x.shape, dtype=x.dtype, device=local) for x in hv] for _ in range(2)]
     do = [[torch.empty(x.shape, dtype=x.dtype, device=local) for x in ho] for _ in range(2)]
-    h2d_ev = [torch.cuda.Event() for _ in range(2)]
-    comp_ev = [torch.cuda.Event() for _ in range(2)]
-    d2h_ev = [torch.cuda.Event() for _ in range(2)]
+    CH = -(-NLAYERS // 4)  # layers per copy chunk
+    chunks = [range(c, min(NLAYERS, c + CH)) for c in range(0, NLAYERS, CH)]
+    in_ev = [torch.cuda.Event() for _ in chunks]   # chunk c's inputs are on the device
+    out_ev = [torch.cuda.Event() for _ in chunks]  # chunk c's attention is done
+    comp_ev = [torch.cuda.Event() for _ in range(2)]       # step done with buffer set j
+    d2h_ev = [torch.cuda.Event() for _ in range(2)]        # buffer set j's outputs drained
     for e in comp_ev + d2h_ev:
         e.record(stream)
     e2e_step = [0]
@@ -400,21 +404,24 @@ def run_gpu(args):
         e2e_step[0] += 1
         with torch.cuda.stream(h2d_stream):
             h2d_stream.wait_event(comp_ev[j])  # step i-2 is done with buffer set j
-            for a, b in zip(dq[j] + dk[j] + dv[j], hq + hk + hv):
-                a.copy_(b, non_blocking=True)
-            h2d_ev[j].record(h2d_stream)
+            for ci, ls in enumerate(chunks):
+                for a, b in zip(dq[j] + dk[j] + dv[j], hq + hk + hv):
+                    a[ls.start:ls.stop].copy_(b[ls.start:ls.stop], non_blocking=True)
+                in_ev[ci].record(h2d_stream)
         batch.grow(1)
-        stream.wait_event(h2d_ev[j])
         stream.wait_event(d2h_ev[j])  # output set j drained to host
-        for layer in range(NLAYERS):
-            batch.decode([x[layer] for x in dq[j]], [x[layer] for x in do[j]], layer, stream=stream,
-                         k=[x[layer] for x in dk[j]], v=[x[layer] for x in dv[j]])
+        for ci, ls in enumerate(chunks):
+            stream.wait_event(in_ev[ci])
+            for layer in ls:
+                batch.decode([x[layer] for x in dq[j]], [x[layer] for x in do[j]], layer, stream=stream,
+                             k=[x[layer] for x in dk[j]], v=[x[layer] for x in dv[j]])
+            out_ev[ci].record(stream)
+            with torch.cuda.stream(d2h_stream):
+                d2h_stream.wait_event(out_ev[ci])
+                for a, b in zip(ho, do[j]):
+                    a[ls.start:ls.stop].copy_(b[ls.start:ls.stop], non_blocking=True)
         comp_ev[j].record(stream)
-        with torch.cuda.stream(d2h_stream):
-            d2h_stream.wait_event(comp_ev[j])
-            for a, b in zip(ho, do[j]):
-                a.copy_(b, non_blocking=True)
-            d2h_ev[j].record(d2h_stream)
+        d2h_ev[j].record(d2h_stream)
 
     for _ in range(args.warmup):
         step_e2e()
