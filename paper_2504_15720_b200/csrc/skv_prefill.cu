@@ -1430,6 +1430,484 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v9(const __grid_
 }
 
 // ---------------------------------------------------------------------------------------
+// v10: CTA pairs (cta_group::2).  A 128x64x16 UMMA issues at 55 clk instead of 32
+// (profiles/r01_umma_bench.txt), so v9's 64-key QK^T runs the tensor core at ~58 %, and a
+// 128-key QK^T with two query tiles per SM does not fit TMEM (Q 2x64 + S 2x128 + O 2x128
+// columns).  Here the two query tiles of a work item sit on the two SMs of a cluster and
+// every MMA is one 256-row tcgen05.mma.cta_group::2 issued by the leader CTA: M = 256
+// (128 query rows per SM, each SM's TMEM holds its rows), N = 128 keys for S = Q.K^T and
+// N = 128 dims for O += P.V, both at the full 64 clk per K=16 step.  The B operands are
+// split across the pair: CTA c holds keys [64c, 64c+64) of the K tile (all 128 dims) and
+// dims [64c, 64c+64) of the V tile (all 128 keys), each loaded by its own TMA warp and
+// signalling the leader's kv_full barrier, so K/V shared-memory traffic per SM halves.
+// TMEM per SM: O [0,128) | S0 [128,256) | S1 [256,384) | Q [384,448): S is double
+// buffered, so QK^T(j+1) runs while the softmax works on S(j) (P(j) is written over the
+// first 64 columns of S(j) and read by the TS-form P.V).  Softmax: 8 warps per SM, warps
+// w and w+4 share the TMEM lanes of rows 32(w%4).. and take key columns [0,64) and
+// [64,128) resp.; the row max is exchanged through shared memory each tile.
+constexpr int kStagesV10 = 6;
+constexpr int kKV10 = 2 * kKVHalf * 2;  // per CTA per stage: K half-tile 16 KiB + V half-tile 16 KiB
+constexpr int kSmemV10 = kStagesV10 * kKV10 + 4096 + 512;
+constexpr int kKT10 = 128;
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t saddr, uint32_t rank) {
+  uint32_t d;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(d) : "r"(saddr), "r"(rank));
+  return d;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// default (.release.cta) semantics: the data behind these arrivals is TMEM, ordered by
+// tcgen05.fence::before_thread_sync; .release.cluster compiles to MEMBAR.ALL.GPU + ERRBAR
+// (27 % of the warp-stall samples of the first v10 build)
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster_rel(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cl(uint64_t* bar, uint32_t phase) {
+  uint32_t ok = 0;
+#ifdef SKV_WATCHDOG
+  long long spins = 0;
+#endif
+  while (!ok) {
+#ifdef SKV_WATCHDOG
+    ++spins;
+    if (spins == (1ll << 22) && (threadIdx.x & 31) == 0)
+      printf("SKV_WATCHDOG v10 block %d warp %d bar_off %u parity %u\n", blockIdx.x, threadIdx.x >> 5,
+             smem_u32(bar) & 0xffff, phase);
+    if (spins == (1ll << 25)) __trap();
+#endif
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  }
+}
+// TMA box into this CTA's shared memory, completion counted on the leader CTA's barrier
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const void* tmap, int x, int y, uint32_t bar_cl) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(x), "r"(y), "r"(bar_cl)
+      : "memory");
+}
+__device__ __forceinline__ void mma_f16_ts_pair(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                                uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// arrive on the barrier at this offset in both CTAs of the pair once the issued MMAs retire
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((unsigned short)3)
+      : "memory");
+}
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ uint32_t make_idesc_pair(int bf16, int b_mn_major) {
+  uint32_t d = 0;
+  d |= 1u << 4;
+  d |= (uint32_t)bf16 << 7;
+  d |= (uint32_t)bf16 << 10;
+  d |= (uint32_t)b_mn_major << 16;
+  d |= (uint32_t)(128 >> 3) << 17;  // N = 128
+  d |= (uint32_t)(256 >> 4) << 24;  // M = 256 (128 rows per CTA)
+  return d;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v10(const __grid_constant__ DataParams p, int npairs,
+                                                                     int hmax) {
+  extern __shared__ __align__(1024) char smem[];
+  if (smem_u32(smem) & 1023) __trap();
+#ifdef SKV_PF_TRACE
+  long long pf_acc[4] = {0, 0, 0, 0};
+  const long long pf_start = clock64();
+  long long pf_tiles = 0;
+#endif
+  char* kvbase = smem;
+  float* xm = reinterpret_cast<float*>(smem + kStagesV10 * kKV10);  // [2 parity][2 half][128 rows]
+  float* xl = xm + 512;                                              // [2 half][128 rows]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStagesV10 * kKV10 + 4096);
+  uint64_t* kv_full = bars;                         // [stages] leader: both CTAs' bytes
+  uint64_t* kv_empty = bars + kStagesV10;           // [stages] both CTAs (multicast commit)
+  // Barriers indexed by [tile parity]: a softmax warp can finish S(j+1) before the MMA warp
+  // has consumed P(j), and parity waits cannot tell phases two apart.
+  uint64_t* q_full = bars + 2 * kStagesV10;         // leader: 16 warp arrivals per item
+  uint64_t* p_full = bars + 2 * kStagesV10 + 1;     // [2] leader: 16 warp arrivals
+  uint64_t* s_full = bars + 2 * kStagesV10 + 3;     // [2] both CTAs (multicast commit)
+  uint64_t* pv_done = bars + 2 * kStagesV10 + 5;    // [2] both CTAs (multicast commit)
+  uint64_t* item_full = bars + 2 * kStagesV10 + 7;  // [kRing9] both CTAs
+  int* ring = reinterpret_cast<int*>(bars + 2 * kStagesV10 + 7 + kRing9);  // [kRing9]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + kRing9);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t rank = cluster_rank();
+  const int n_items = npairs * hmax * p.nreq;
+  const int q_len = p.n_new;
+
+  if (warp == kMmaWarp) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < kStagesV10; ++i) {
+      mbar_init_n(&kv_full[i], 1);
+      mbar_init_n(&kv_empty[i], 1);
+    }
+    mbar_init_n(q_full, 16);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init_n(&p_full[i], 16);
+      mbar_init_n(&s_full[i], 1);
+      mbar_init_n(&pv_done[i], 1);
+    }
+    for (int i = 0; i < kRing9; ++i) mbar_init_n(&item_full[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t q_full_l = mapa_u32(smem_u32(q_full), 0), p_full_l = mapa_u32(smem_u32(p_full), 0);
+
+  struct Geo {
+    int r, h, pair, handle, ctx, start, tpt, t0A, n_keys, n_kt, rl, G;
+    const DataGroup* g;
+  };
+  auto geo = [&](int idx) {
+    Geo e;
+    prefill_item9(p, idx, npairs, hmax, e.r, e.h, e.pair);
+    e.g = &p.g[p.req_group[e.r]];
+    e.G = e.g->G;
+    e.handle = p.handles[e.r];
+    e.ctx = p.req_tokens[e.handle];
+    e.start = e.ctx - q_len;
+    e.tpt = kRows / e.G;
+    e.t0A = 2 * e.pair * e.tpt;
+    e.n_keys = min(e.ctx, e.start + e.t0A + 2 * e.tpt);
+    e.n_kt = (e.n_keys + kKT10 - 1) / kKT10;
+    e.rl = e.r - e.g->req_begin;
+    return e;
+  };
+  auto next_item = [&](uint32_t k) {
+    mbar_wait_cl(&item_full[k % kRing9], (k / kRing9) & 1);
+    return *reinterpret_cast<volatile int*>(&ring[k % kRing9]);
+  };
+
+  if (warp == kLoadWarp) {  // --------------------------------- scheduler (leader) + K/V streaming (both)
+    // Whole warp: lane i holds block-table entry i of the current 32-entry chunk (4 key tiles)
+    // and the next chunk is already in flight, so the table's load latency is off the TMA
+    // issue path; the 8 lanes of a tile issue its boxes in parallel.
+    uint32_t jt = 0;
+    const uint32_t ring_peer = mapa_u32(smem_u32(ring), 1), item_peer = mapa_u32(smem_u32(item_full), 1);
+    const uint32_t kv_full_l = mapa_u32(smem_u32(kv_full), 0);
+    for (uint32_t k = 0;; ++k) {
+      int pub;
+      if (rank == 0) {
+        if (lane == 0) {
+          int idx = atomicAdd(p.counter, 1);
+          while (idx < n_items) {
+            int r_, h_, pr_;
+            if (prefill_item9(p, idx, npairs, hmax, r_, h_, pr_)) break;
+            idx = atomicAdd(p.counter, 1);
+          }
+          pub = idx < n_items ? idx : -1;
+          const uint32_t slot = k % kRing9;
+          ring[slot] = pub;
+          asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(ring_peer + 4 * slot), "r"(pub) : "memory");
+          asm volatile("mbarrier.arrive.release.cluster.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&item_full[slot]))
+                       : "memory");
+          mbar_arrive_cluster_rel(item_peer + 8 * slot);
+        }
+        pub = __shfl_sync(0xffffffffu, pub, 0);
+      } else {
+        pub = next_item(k);
+      }
+      if (pub < 0) break;
+      const Geo e = geo(pub);
+      const int2* row_tab = p.req_table + (size_t)e.handle * p.cap;
+      const long long base_off = e.g->layer_off + (long long)e.h * e.g->head_stride;
+      const int n_blk = (e.n_keys + kTpb - 1) / kTpb;
+      int2 ent_next = lane < n_blk ? row_tab[lane] : make_int2(-1, 0);
+      int row0 = 0;
+      bool valid = false;
+      for (int j = 0; j < e.n_kt; ++j, ++jt) {
+        if ((j & 3) == 0) {
+          valid = ent_next.x >= 0;
+          row0 = valid ? (int)(((long long)ent_next.x * p.merged_stride + (long long)ent_next.y * e.g->native_stride +
+                                base_off) >> 8)
+                       : 0;
+          const int nx = (j + 4) * 8 + lane;
+          ent_next = nx < n_blk ? row_tab[nx] : make_int2(-1, 0);
+        }
+        const int st = jt % kStagesV10;
+        if (jt >= (uint32_t)kStagesV10) {
+          if (lane == 0) PF_T(0, mbar_wait(&kv_empty[st], ((jt / kStagesV10) - 1) & 1));
+          __syncwarp();
+        }
+        const int grp = (j & 3) * 8;
+        const bool mine = lane >= grp && lane < grp + 8 && valid;
+        const int nb = __popc(__ballot_sync(0xffffffffu, mine));
+        // leader expects both CTAs' bytes: K 2 halves x 2 KiB and V 2 x 2 KiB per valid block
+        if (rank == 0 && lane == 0) mbar_expect_tx_v3(&kv_full[st], nb * 8192);
+        __syncwarp();
+        if (mine) {
+          const int b = lane - grp;
+          const uint32_t sK = smem_u32(kvbase + st * kKV10), sV = sK + 2 * kKVHalf;
+          const uint32_t bar = kv_full_l + 8 * st;
+          if ((b >> 2) == (int)rank) {  // this CTA's 64 keys of K, both d-halves
+            tma_load_2d_pair(sK + (b & 3) * 2048, &p.kv_tmap, 0, row0, bar);
+            tma_load_2d_pair(sK + kKVHalf + (b & 3) * 2048, &p.kv_tmap, 64, row0, bar);
+          }
+          tma_load_2d_pair(sV + b * 2048, &p.kv_tmap, (int)rank * 64, row0 + kTpb, bar);  // this CTA's d-half of V
+        }
+      }
+    }
+  } else if (warp == kMmaWarp) {  // ------------------------------------- MMA issue (leader only)
+    if (lane == 0 && rank == 0) {
+      const uint32_t idesc_qk = make_idesc_pair(p.dtype, 0);
+      const uint32_t idesc_pv = make_idesc_pair(p.dtype, 1);
+      uint32_t jt = 0;
+      for (uint32_t k = 0;; ++k) {
+        const int idx = next_item(k);
+        if (idx < 0) break;
+        const Geo e = geo(idx);
+        const uint32_t j0 = jt;
+        const int J = e.n_kt;
+        auto wait_kv = [&](int j) {
+          const uint32_t gj = j0 + j;
+          PF_T(1, mbar_wait(&kv_full[gj % kStagesV10], (gj / kStagesV10) & 1));
+          tc_fence_after();
+        };
+        auto qk = [&](int j) {
+          const uint32_t gj = j0 + j;
+          const uint32_t sK = smem_u32(kvbase + (gj % kStagesV10) * kKV10);
+          const uint32_t tS = tmem + 128 + (gj & 1) * 128;
+#pragma unroll
+          for (int kk = 0; kk < kD / 16; ++kk) {
+            const uint32_t koff = (kk >> 2) * kKVHalf + (kk & 3) * 32;
+            mma_f16_ts_pair(tS, tmem + 384 + kk * 8, make_desc(sK + koff, 16, 1024), idesc_qk, kk > 0);
+          }
+          mma_commit_pair(&s_full[gj & 1]);
+        };
+        auto pv = [&](int j) {
+          const uint32_t gj = j0 + j;
+          const uint32_t sV = smem_u32(kvbase + (gj % kStagesV10) * kKV10) + 2 * kKVHalf;
+          const uint32_t tP = tmem + 128 + (gj & 1) * 128;
+#pragma unroll
+          for (int kk = 0; kk < kKT10 / 16; ++kk)
+            mma_f16_ts_pair(tmem, tP + kk * 8, make_desc(sV + kk * 2048, 2 * kKVHalf, 1024), idesc_pv,
+                            (j > 0 || kk > 0) ? 1u : 0u);
+          mma_commit_pair(&pv_done[gj & 1]);
+          mma_commit_pair(&kv_empty[gj % kStagesV10]);
+        };
+        PF_T(0, mbar_wait(q_full, k & 1));
+        tc_fence_after();
+        wait_kv(0);
+        qk(0);
+        if (J > 1) {
+          wait_kv(1);
+          qk(1);
+        }
+        for (int j = 0; j < J; ++j) {
+          PF_T(2, mbar_wait(&p_full[(j0 + j) & 1], ((j0 + j) >> 1) & 1));
+          tc_fence_after();
+          pv(j);
+          if (j + 2 < J) {
+            wait_kv(j + 2);
+            qk(j + 2);
+          }
+        }
+        jt += J;
+      }
+    }
+    __syncwarp();
+  } else {  // ------------------------------------------------------------- softmax warps
+    const int c = warp >> 2;  // key-column half of S / dim half of Q and O
+    const int row = (warp & 3) * 32 + lane;
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const uint32_t tQ = tmem + 384 + 32 * c + lane_off;
+    const uint32_t tO = tmem + 64 * c + lane_off;
+    const float c2 = p.scale_log2;
+    const int nbar = 1 + (warp & 3);  // named barrier of the two warps sharing these rows
+    uint32_t jt = 0;
+    for (uint32_t k = 0;; ++k) {
+      const int idx = next_item(k);
+      if (idx < 0) break;
+      const Geo e = geo(idx);
+      const int t0 = e.t0A + (int)rank * e.tpt;
+      const int my_tok = t0 + row / e.G;
+      const bool row_ok = my_tok < q_len;
+      const int my_pos = e.start + my_tok;
+      const bool tail_rows = t0 + e.tpt > q_len;
+      {  // this thread's half of its Q row (all QK^T of the previous item retired)
+        const uint4* src = reinterpret_cast<const uint4*>(
+            reinterpret_cast<const char*>(e.g->q) +
+            (((size_t)e.rl * q_len + (row_ok ? my_tok : 0)) * e.g->Hq + e.h * e.G + row % e.G) * (kD * 2) + c * 128);
+        uint32_t qv[32];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const uint4 v = row_ok ? src[i] : make_uint4(0u, 0u, 0u, 0u);
+          qv[4 * i] = v.x;
+          qv[4 * i + 1] = v.y;
+          qv[4 * i + 2] = v.z;
+          qv[4 * i + 3] = v.w;
+        }
+        tmem_st32u(tQ, qv);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(q_full_l);
+      }
+      float m = -INFINITY, l = 0.f;
+      const uint32_t j0 = jt;
+      for (int j = 0; j < e.n_kt; ++j) {
+        const uint32_t gj = j0 + j;
+        const uint32_t tS = tmem + 128 + (gj & 1) * 128 + lane_off;
+        PF_T(0, mbar_wait(&s_full[gj & 1], (gj >> 1) & 1));
+        tc_fence_after();
+        const bool last_partial = j == e.n_kt - 1 && (j + 1) * kKT10 > e.n_keys;
+        if (last_partial) {  // V rows past the keys (stale or another owner's bytes) -> 0
+          char* sV = kvbase + (gj % kStagesV10) * kKV10 + 2 * kKVHalf;
+          const int first = e.n_keys - j * kKT10;
+          for (int i = tid; i < kKT10 * 8; i += 256) {
+            const int key = i >> 3, ch = i & 7;
+            if (key >= first)
+              *reinterpret_cast<uint4*>(sV + (key >> 3) * 1024 + (key & 7) * 128 + ((ch ^ (key & 7)) << 4)) =
+                  make_uint4(0, 0, 0, 0);
+          }
+        }
+        float s[64];
+        tmem_ld64(tS + 64 * c, s);
+        const int kbase = j * kKT10 + 64 * c;
+        const bool masked = (kbase + 63 > e.start + t0) || tail_rows;
+        if (masked) {
+#pragma unroll
+          for (int kk = 0; kk < 64; ++kk)
+            if (!(row_ok && kbase + kk <= my_pos)) s[kk] = -INFINITY;
+        }
+        float mx4[4] = {s[0], s[1], s[2], s[3]};
+#pragma unroll
+        for (int kk = 4; kk < 64; kk += 4) {
+          mx4[0] = fmaxf(mx4[0], s[kk]);
+          mx4[1] = fmaxf(mx4[1], s[kk + 1]);
+          mx4[2] = fmaxf(mx4[2], s[kk + 2]);
+          mx4[3] = fmaxf(mx4[3], s[kk + 3]);
+        }
+        float* xmb = xm + (gj & 1) * 256;
+        xmb[c * 128 + row] = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+        PF_T(3, named_bar(nbar, 64));
+        const float mt = fmaxf(xmb[row], xmb[128 + row]) * c2;
+        const bool need = mt > m + kRescale;
+        float alpha = 1.f;
+        if (need) {
+          alpha = ex2(m - mt);
+          l *= alpha;
+          m = mt;
+        }
+        if (j > 0 && __any_sync(0xffffffffu, need)) {
+          PF_T(1, mbar_wait(&pv_done[(gj - 1) & 1], ((gj - 1) >> 1) & 1));  // O holds P.V through tile j-1
+          tc_fence_after();
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc) {
+            float o[32];
+            tmem_ld32(tO + cc * 32, o);
+#pragma unroll
+            for (int kk = 0; kk < 32; ++kk) o[kk] *= alpha;
+            tmem_st32(tO + cc * 32, o);
+          }
+        }
+        const float mu = (m == -INFINITY) ? 0.f : m;
+        float ls[4] = {0.f, 0.f, 0.f, 0.f};
+        uint32_t pk[32];
+#pragma unroll
+        for (int kk = 0; kk < 64; kk += 2) {
+          const float v0 = ex2(fmaf(s[kk], c2, -mu));
+          const float v1 = ex2(fmaf(s[kk + 1], c2, -mu));
+          ls[(kk >> 1) & 3] += v0 + v1;
+          pk[kk >> 1] = pack2<T>(v0, v1);
+        }
+        tmem_st32u(tS + 32 * c, pk);
+        l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+        if (last_partial) fence_async_smem();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(p_full_l + 8 * (gj & 1));
+      }
+      const uint32_t gl = j0 + e.n_kt - 1;
+      xl[c * 128 + row] = l;
+      PF_T(2, mbar_wait(&pv_done[gl & 1], (gl >> 1) & 1));
+      tc_fence_after();
+      named_bar(nbar, 64);
+      const float lt = xl[row] + xl[128 + row];
+      jt += e.n_kt;
+#ifdef SKV_PF_TRACE
+      pf_tiles += e.n_kt;
+#endif
+      const float inv = lt > 0.f ? 1.f / lt : 0.f;
+      char* dst = reinterpret_cast<char*>(e.g->out) +
+                  (((size_t)e.rl * q_len + (row_ok ? my_tok : 0)) * e.g->Hq + e.h * e.G + row % e.G) * (kD * 2) +
+                  c * 128;
+#pragma unroll
+      for (int cc = 0; cc < 2; ++cc) {
+        float o[32];
+        tmem_ld32(tO + cc * 32, o);
+        if (row_ok) {
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            uint4 v;
+            v.x = pack2<T>(o[8 * q4] * inv, o[8 * q4 + 1] * inv);
+            v.y = pack2<T>(o[8 * q4 + 2] * inv, o[8 * q4 + 3] * inv);
+            v.z = pack2<T>(o[8 * q4 + 4] * inv, o[8 * q4 + 5] * inv);
+            v.w = pack2<T>(o[8 * q4 + 6] * inv, o[8 * q4 + 7] * inv);
+            *reinterpret_cast<uint4*>(dst + cc * 64 + q4 * 16) = v;
+          }
+        }
+      }
+      named_bar(nbar, 64);  // xl reused by the next item
+      tc_fence_before();    // the next item's first P.V (after our p_full arrive) overwrites O
+    }
+  }
+#ifdef SKV_PF_TRACE
+  if (p.trace) {  // [cta][16]: loader 0, mma 1-3, softmax c=0 5-8, c=1 9-12, cta cycles 13, tiles 14
+    unsigned long long* t = p.trace + (size_t)blockIdx.x * 16;
+    if (warp == kLoadWarp && lane == 0) t[0] = pf_acc[0];
+    if (warp == kMmaWarp && lane == 0)
+      for (int i = 0; i < 3; ++i) t[1 + i] = pf_acc[i];
+    if (warp < kSoftmaxWarps && (tid & 127) == 0)
+      for (int i = 0; i < 4; ++i) t[5 + 4 * (warp >> 2) + i] = pf_acc[i];
+    if (tid == 0) {
+      t[13] = clock64() - pf_start;
+      t[14] = pf_tiles;
+    }
+  }
+#endif
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == kMmaWarp) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// ---------------------------------------------------------------------------------------
 // v5 (experimental, SEAKV_PREFILL_V=5): 128-key tiles.  A 128x64x16 UMMA runs at 2/3 of
 // the tensor core's rate (measured: 48 clk vs 64 clk for N=128, scripts/umma_bench), so
 // S = Q.K^T uses N = 128 keys and P.V uses K = 128 keys.  TMEM: S_A | S_B | O_A | O_B
@@ -1748,6 +2226,7 @@ void launch_prefill_t(const DataParams& p, cudaStream_t s) {
     cudaFuncSetAttribute(prefill_kernel_v5<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemV5);
     cudaFuncSetAttribute(prefill_kernel_v7<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemV7);
     cudaFuncSetAttribute(prefill_kernel_v9<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemV9);
+    cudaFuncSetAttribute(prefill_kernel_v10<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemV10);
     attr = true;
   }
   int tiles = 1, heads = 1;
@@ -1774,6 +2253,27 @@ void launch_prefill_t(const DataParams& p, cudaStream_t s) {
     const int grid = (int)std::min<long long>(items, nsm);
     cudaMemsetAsync(p.counter, 0, sizeof(int), s);
     prefill_kernel_v9<T><<<grid, kThreadsV3, kSmemV9, s>>>(p, npairs, heads);
+  } else if (version == 10) {
+    const int npairs = (tiles + 1) / 2;
+    int nsm = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const long long items = (long long)npairs * heads * p.nreq;
+    const int clusters = (int)std::min<long long>(items, nsm / 2);
+    cudaMemsetAsync(p.counter, 0, sizeof(int), s);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * clusters, 1, 1);
+    cfg.blockDim = dim3(kThreadsV3, 1, 1);
+    cfg.dynamicSmemBytes = kSmemV10;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, prefill_kernel_v10<T>, p, npairs, heads);
   } else if (version == 7) {
     dim3 grid((tiles + 1) / 2, heads, p.nreq);
     prefill_kernel_v7<T><<<grid, kThreadsV3, kSmemV7, s>>>(p);
