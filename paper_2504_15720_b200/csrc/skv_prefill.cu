@@ -2236,7 +2236,7 @@ void launch_prefill_t(const DataParams& p, cudaStream_t s) {
   }
   static const int version = [] {
     const char* e = getenv("SEAKV_PREFILL_V");
-    return e ? atoi(e) : 9;  // v9 measured fastest (profiles/r01_prefill_probe_v9.txt); 3, 5, 7 selectable
+    return e ? atoi(e) : 10;  // v10 measured fastest (profiles/r01_prefill_probe_v10.txt); 3, 5, 7, 9 selectable
   }();
   if (version == 2 || !p.has_tmap) {
     dim3 grid(tiles, heads, p.nreq);

@@ -1,15 +1,15 @@
 # v10 prefill: parity tests + probe vs v9 (scratch script for the 2-CTA prefill bring-up)
 mkdir -p gpurun_out
 rm -f gpurun_out/v10_probe.log
-SEAKV_PREFILL_V=10 timeout 300 python -m pytest tests/test_gpu_prefill.py -x -q -p no:cacheprovider > gpurun_out/v10_tests.log 2>&1; echo "exit $?" >> gpurun_out/v10_tests.log
+SEAKV_PREFILL_V=${TV:-10} timeout 120 python -m pytest tests/test_gpu_prefill.py -x -q -p no:cacheprovider > gpurun_out/v10_tests.log 2>&1; echo "exit $?" >> gpurun_out/v10_tests.log
 for a in "8 2048 512" "16 4096 1024" "4 16384 2048" "2 1024 512"; do
   for V in ${VERS:-10 9}; do
   echo -n "v$V " >> gpurun_out/v10_probe.log
-  SEAKV_PREFILL_V=$V timeout 120 python scripts/prefill_probe.py $a >> gpurun_out/v10_probe.log 2>&1
+  SEAKV_PREFILL_V=$V timeout 60 python scripts/prefill_probe.py $a >> gpurun_out/v10_probe.log 2>&1
   done
 done
 nvidia-smi --query-gpu=clocks.sm,clocks_throttle_reasons.active --format=csv >> gpurun_out/v10_probe.log
 if [ -n "$PROF" ]; then
-SEAKV_PREFILL_V=10 timeout 600 ncu --set full --import-source on --clock-control none -k regex:prefill_kernel_v -s 2 -c 1 \
+SEAKV_PREFILL_V=${TV:-10} timeout 600 ncu --set full --import-source on --clock-control none -k regex:prefill_kernel_v -s 2 -c 1 \
   -o gpurun_out/prof_pf_v10 -f python scripts/prefill_probe.py 4 16384 2048 3 > gpurun_out/prof_pf_v10.log 2>&1
 fi
