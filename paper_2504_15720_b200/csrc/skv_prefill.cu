@@ -1445,6 +1445,44 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v9(const __grid_
 // first 64 columns of S(j) and read by the TS-form P.V).  Softmax: 8 warps per SM, warps
 // w and w+4 share the TMEM lanes of rows 32(w%4).. and take key columns [0,64) and
 // [64,128) resp.; the row max is exchanged through shared memory each tile.
+// asynchronous TMEM load: the registers are valid only after tmem_ld32_wait on the same array
+// (which takes them as in/out operands so no use can be scheduled above the wait)
+__device__ __forceinline__ void tmem_ld32_issue(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+        "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+        "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+        "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld32_wait(uint32_t (&r)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                 "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]),
+                 "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]),
+                 "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+               :
+               : "memory");
+}
+
+// 2^x as a degree-3 polynomial on the FMA pipe (2^f on [-1/2, 1/2], max rel. error 7.5e-5), used by
+// v5's dbg bit 1; on v10 a quarter of the exponentials this way measured 952 vs 1025 TFLOP/s at 16K
+__device__ __forceinline__ float ex2_poly(float x) {
+  // clamp: for j <= -127 the exponent add below would underflow into the sign bit
+  x = fmaxf(x, -125.f);
+  const float t = x + 12582912.f;  // 1.5 * 2^23: round to nearest integer in the low bits
+  const float f = x - (t - 12582912.f);
+  float p = fmaf(0.05517166207399859f, f, 0.2426111584161752f);
+  p = fmaf(p, f, 0.6932609899481472f);
+  p = fmaf(p, f, 0.9999280714420054f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
 constexpr int kStagesV10 = 6;
 constexpr int kKV10 = 2 * kKVHalf * 2;  // per CTA per stage: K half-tile 16 KiB + V half-tile 16 KiB
 constexpr int kSmemV10 = kStagesV10 * kKV10 + 4096 + 512;
@@ -1793,55 +1831,120 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v10(const __grid
                   make_uint4(0, 0, 0, 0);
           }
         }
-        float s[64];
-        tmem_ld64(tS + 64 * c, s);
         const int kbase = j * kKT10 + 64 * c;
         const bool masked = (kbase + 63 > e.start + t0) || tail_rows;
-        if (masked) {
-#pragma unroll
-          for (int kk = 0; kk < 64; ++kk)
-            if (!(row_ok && kbase + kk <= my_pos)) s[kk] = -INFINITY;
-        }
-        float mx4[4] = {s[0], s[1], s[2], s[3]};
-#pragma unroll
-        for (int kk = 4; kk < 64; kk += 4) {
-          mx4[0] = fmaxf(mx4[0], s[kk]);
-          mx4[1] = fmaxf(mx4[1], s[kk + 1]);
-          mx4[2] = fmaxf(mx4[2], s[kk + 2]);
-          mx4[3] = fmaxf(mx4[3], s[kk + 3]);
-        }
+        // path decision shared by the two warps of a row pair (same rows, same tile)
+        const bool tile_masked = (j * kKT10 + kKT10 - 1 > e.start + t0) || tail_rows;
         float* xmb = xm + (gj & 1) * 256;
-        xmb[c * 128 + row] = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
-        PF_T(3, named_bar(nbar, 64));
-        const float mt = fmaxf(xmb[row], xmb[128 + row]) * c2;
-        const bool need = mt > m + kRescale;
-        float alpha = 1.f;
-        if (need) {
-          alpha = ex2(m - mt);
-          l *= alpha;
-          m = mt;
-        }
-        if (j > 0 && __any_sync(0xffffffffu, need)) {
-          PF_T(1, mbar_wait(&pv_done[(gj - 1) & 1], ((gj - 1) >> 1) & 1));  // O holds P.V through tile j-1
-          tc_fence_after();
-#pragma unroll
-          for (int cc = 0; cc < 2; ++cc) {
-            float o[32];
-            tmem_ld32(tO + cc * 32, o);
-#pragma unroll
-            for (int kk = 0; kk < 32; ++kk) o[kk] *= alpha;
-            tmem_st32(tO + cc * 32, o);
-          }
-        }
-        const float mu = (m == -INFINITY) ? 0.f : m;
         float ls[4] = {0.f, 0.f, 0.f, 0.f};
         uint32_t pk[32];
+        if (j > 0 && !tile_masked && !(p.dbg & 4) && __all_sync(0xffffffffu, m != -INFINITY)) {
+          // Speculative path: exponentials against the running max m while the second 32-column
+          // TMEM load is in flight, the row max exchanged only after them; valid unless the tile
+          // raises a row max by more than 2^kRescale (rare: then the tile is recomputed from the
+          // S values still in registers).  Keeps the TMEM-load latency and the max reduction off
+          // the path between the tile barrier and the MUFU work.
+          uint32_t ra[32], rb[32];
+          float mxa = -INFINITY, mxb = -INFINITY;
+          tmem_ld32_issue(tS + 64 * c, ra);
+          tmem_ld32_wait(ra);
+          tmem_ld32_issue(tS + 64 * c + 32, rb);
 #pragma unroll
-        for (int kk = 0; kk < 64; kk += 2) {
-          const float v0 = ex2(fmaf(s[kk], c2, -mu));
-          const float v1 = ex2(fmaf(s[kk + 1], c2, -mu));
-          ls[(kk >> 1) & 3] += v0 + v1;
-          pk[kk >> 1] = pack2<T>(v0, v1);
+          for (int kk = 0; kk < 32; kk += 2) {
+            const float x0 = __uint_as_float(ra[kk]), x1 = __uint_as_float(ra[kk + 1]);
+            mxa = fmaxf(mxa, x0);
+            mxb = fmaxf(mxb, x1);
+            const float v0 = ex2(fmaf(x0, c2, -m)), v1 = ex2(fmaf(x1, c2, -m));
+            ls[(kk >> 1) & 3] += v0 + v1;
+            pk[kk >> 1] = pack2<T>(v0, v1);
+          }
+          tmem_ld32_wait(rb);
+#pragma unroll
+          for (int kk = 0; kk < 32; kk += 2) {
+            const float x0 = __uint_as_float(rb[kk]), x1 = __uint_as_float(rb[kk + 1]);
+            mxa = fmaxf(mxa, x0);
+            mxb = fmaxf(mxb, x1);
+            const float v0 = ex2(fmaf(x0, c2, -m)), v1 = ex2(fmaf(x1, c2, -m));
+            ls[(kk >> 1) & 3] += v0 + v1;
+            pk[16 + (kk >> 1)] = pack2<T>(v0, v1);
+          }
+          xmb[c * 128 + row] = fmaxf(mxa, mxb);
+          PF_T(3, named_bar(nbar, 64));
+          const float mt = fmaxf(xmb[row], xmb[128 + row]) * c2;
+          const bool need = mt > m + kRescale;
+          if (__any_sync(0xffffffffu, need)) {  // redo the tile with the new max
+            float alpha = 1.f;
+            if (need) {
+              alpha = ex2(m - mt);
+              l *= alpha;
+              m = mt;
+            }
+            PF_T(1, mbar_wait(&pv_done[(gj - 1) & 1], ((gj - 1) >> 1) & 1));  // O holds P.V through tile j-1
+            tc_fence_after();
+#pragma unroll
+            for (int cc = 0; cc < 2; ++cc) {
+              float o[32];
+              tmem_ld32(tO + cc * 32, o);
+#pragma unroll
+              for (int kk = 0; kk < 32; ++kk) o[kk] *= alpha;
+              tmem_st32(tO + cc * 32, o);
+            }
+            ls[0] = ls[1] = ls[2] = ls[3] = 0.f;
+#pragma unroll
+            for (int kk = 0; kk < 64; kk += 2) {
+              const uint32_t* src = kk < 32 ? ra : rb;
+              const float v0 = ex2(fmaf(__uint_as_float(src[kk & 31]), c2, -m));
+              const float v1 = ex2(fmaf(__uint_as_float(src[(kk & 31) + 1]), c2, -m));
+              ls[(kk >> 1) & 3] += v0 + v1;
+              pk[kk >> 1] = pack2<T>(v0, v1);
+            }
+          }
+        } else {
+          float s[64];
+          tmem_ld64(tS + 64 * c, s);
+          if (masked) {
+#pragma unroll
+            for (int kk = 0; kk < 64; ++kk)
+              if (!(row_ok && kbase + kk <= my_pos)) s[kk] = -INFINITY;
+          }
+          float mx4[4] = {s[0], s[1], s[2], s[3]};
+#pragma unroll
+          for (int kk = 4; kk < 64; kk += 4) {
+            mx4[0] = fmaxf(mx4[0], s[kk]);
+            mx4[1] = fmaxf(mx4[1], s[kk + 1]);
+            mx4[2] = fmaxf(mx4[2], s[kk + 2]);
+            mx4[3] = fmaxf(mx4[3], s[kk + 3]);
+          }
+          xmb[c * 128 + row] = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+          PF_T(3, named_bar(nbar, 64));
+          const float mt = fmaxf(xmb[row], xmb[128 + row]) * c2;
+          const bool need = mt > m + kRescale;
+          float alpha = 1.f;
+          if (need) {
+            alpha = ex2(m - mt);
+            l *= alpha;
+            m = mt;
+          }
+          if (j > 0 && __any_sync(0xffffffffu, need)) {
+            PF_T(1, mbar_wait(&pv_done[(gj - 1) & 1], ((gj - 1) >> 1) & 1));  // O holds P.V through tile j-1
+            tc_fence_after();
+#pragma unroll
+            for (int cc = 0; cc < 2; ++cc) {
+              float o[32];
+              tmem_ld32(tO + cc * 32, o);
+#pragma unroll
+              for (int kk = 0; kk < 32; ++kk) o[kk] *= alpha;
+              tmem_st32(tO + cc * 32, o);
+            }
+          }
+          const float mu = (m == -INFINITY) ? 0.f : m;
+#pragma unroll
+          for (int kk = 0; kk < 64; kk += 2) {
+            const float v0 = ex2(fmaf(s[kk], c2, -mu));
+            const float v1 = ex2(fmaf(s[kk + 1], c2, -mu));
+            ls[(kk >> 1) & 3] += v0 + v1;
+            pk[kk >> 1] = pack2<T>(v0, v1);
+          }
         }
         tmem_st32u(tS + 32 * c, pk);
         l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
@@ -1922,16 +2025,6 @@ constexpr int kKT5 = 128;
 constexpr int kKStages5 = 3, kVStages5 = 2;
 constexpr int kSmemV5 = 2 * kTileBytes + (kKStages5 + kVStages5) * kTileBytes + 256;
 
-__device__ __forceinline__ float ex2_poly(float x) {
-  // clamp: for j <= -127 the exponent add below would underflow into the sign bit
-  x = fmaxf(x, -125.f);
-  const float t = x + 12582912.f;  // 1.5 * 2^23: round to nearest integer in the low bits
-  const float f = x - (t - 12582912.f);
-  float p = fmaf(0.05517166207399859f, f, 0.2426111584161752f);
-  p = fmaf(p, f, 0.6932609899481472f);
-  p = fmaf(p, f, 0.9999280714420054f);
-  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
-}
 
 
 template <typename T>
