@@ -182,6 +182,41 @@ class ChurnEngine:
             b.reset(groups)
         return b
 
+    # -- steady-state start -------------------------------------------------------------------
+    def warm_start(self, arrivals: Sequence[Arrival], seed: int = 11) -> int:
+        """Bring the pool to the occupancy target before timing: requests from ``arrivals``
+        (in order) are admitted as already prefilled -- one grow to their input length plus
+        a seeded part of their output, K/V from the pool's synthetic fill -- and join the
+        decode set while they fit under the target; one that does not fit joins the waiting
+        queue (normal admission later).  Stops once the pool is within 5 % of the target.
+        Returns the number of arrivals consumed.  The grows are recorded like every other
+        allocator call."""
+        cache, pool = self.cache, self.cache.pool_size()
+        target = self.occupancy * pool
+        rng = Rng(seed)
+        used = 0
+        for a in arrivals:
+            if cache.allocated_blocks() >= 0.95 * target or len(self.running) >= self.max_decode:
+                break
+            used += 1
+            p = self.profiles[a.svc]
+            r = Req(self.next_id, a.svc, p.model_idx, a.in_len, a.out_len)
+            self.next_id += 1
+            gen = 1 + int(rng.next_double() * max(0, a.out_len - 1))
+            need = cache.native_blocks_for(r.in_len + gen) / max(1, cache.sub_slots_per_merged(r.model))
+            if cache.allocated_blocks() + need > target or not self._grow(r, r.in_len + gen):
+                self.waiting.append(r)
+                continue
+            r.phase, r.done, r.generated = "decode", r.in_len, gen
+            self.running[r.rid] = r
+        self.cache.flush(self.stream)
+        return used
+
+    def reset_stats(self) -> None:
+        """Zero the counters (the recorded KvOp stream is kept)."""
+        for k in self.stats:
+            self.stats[k] = 0.0 if isinstance(self.stats[k], float) else 0
+
     # -- one serving iteration ------------------------------------------------------------------
     def step(self) -> dict:
         cache, st = self.cache, self.stats

@@ -64,3 +64,44 @@ def test_churn_engine_block_tables_bit_exact_vs_oracle():
     assert cache.fragmentation_bytes() == oracle.fragmentation_bytes()
     for o in eng.o_dec:
         assert torch.isfinite(o[:4]).all()
+
+
+@pytest.mark.gpu
+def test_churn_warm_start_reaches_target_and_replays_bit_exact():
+    """warm_start (config-3 steady state): pool brought near the occupancy target with
+    prefilled requests, then serving iterations; the whole recorded op stream replays through
+    the oracle to identical tables."""
+    shapes = [(2, 4, 16), (3, 8, 8)]
+    models = [P.ModelSpec(f"m{i}", L, H, 128, 2, Hq) for i, (L, H, Hq) in enumerate(shapes)]
+    pool = 64
+    cache = P.UnifiedKvCache(models, 16, 1, pool, allocate_storage=True, max_blocks_per_request=512)
+    s = torch.cuda.Stream()
+    torch.cuda.set_stream(s)
+    cache.set_stream(s)
+    cache.synth_fill(6, 1.0, s)
+    prof = [ServiceProfile("chat0", 0, 60, 30, 25, 10), ServiceProfile("summ0", 0, 400, 100, 6, 2),
+            ServiceProfile("chat1", 1, 50, 20, 30, 10), ServiceProfile("summ1", 1, 300, 80, 5, 2)]
+    trace = generate_trace(prof, rate=40.0, duration=3.0, skewness=2, seed=12, step_time=1.5, step_factor=2.0)
+    eng = ChurnEngine(cache, shapes, prof, chunk=64, occupancy=0.7, max_decode=64, max_prefill=4, stream=s)
+    k = eng.warm_start(trace)
+    assert k > 0 and 0.6 * pool <= cache.allocated_blocks() <= 0.7 * pool + 1
+    eng.reset_stats()
+    t = 0.0
+    for _ in range(30):
+        t += 0.05
+        new = []
+        while k < len(trace) and trace[k].t <= t:
+            new.append(trace[k])
+            k += 1
+        eng.add_arrivals(new)
+        eng.step()
+    assert eng.summary()["mean_occupancy"] > 0.4
+    oracle = O.OracleCache([(L, H, 128, 2) for L, H, _ in shapes], pool=pool)
+    for kind, rid, m, tok in eng.ops:
+        if kind == 0:
+            oracle.try_allocate(rid, m, tok)
+        else:
+            oracle.free_request(rid)
+    for rid in eng.running:
+        assert np.array_equal(cache.block_table_np(rid), oracle.block_table_np(rid))
+    assert cache.stats() == oracle.stats()
