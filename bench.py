@@ -609,9 +609,9 @@ def run_churn(args):
                                f"occupancy target 0.70 (pool filled with {k} prefilled trace requests, then "
                                f"{n_warm} untimed iterations), faithful pool {pool} merged blocks ({args.pool_gb} GB)"},
         "churn": summ, "gpu_launches": int(cache.kernel_launches() - launches0), "clocks": clk.summary(),
-        "note": "eager, host-driven engine: value = decode bytes / sum of per-launch event intervals, which "
-                "include host submission gaps (churn.data_path_ms is the GPU span of each step); the "
-                "kernel-level decode figures are the config 1/2/4 lines",
+        "note": "eager, host-driven engine (allocator decisions on the host each iteration); value = decode "
+                "bytes / GPU span of each iteration's decode phase (one fused append+decode launch per layer); "
+                "churn.data_path_ms is the GPU span of each whole step",
     }
     print(json.dumps(res), flush=True)
 

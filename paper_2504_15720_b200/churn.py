@@ -266,24 +266,19 @@ class ChurnEngine:
             q = [self.q_dec[m][: len(ids)] for m, ids in groups]
             o = [self.o_dec[m][: len(ids)] for m, ids in groups]
             kv = [self.kv_dec[m][: len(ids)] for m, ids in groups]
-            # separate append and decode launches, each bracketed by events (per-kernel
-            # accounting; the benchmark's decode step uses the fused launch instead).
-            # This driver is host-bound: the intervals include host submission gaps, and
-            # data_path_ms is the GPU span of the whole step.
+            # one launch per layer: the new token's K/V is appended inside the decode kernel
+            # (fused append); the layer loop is bracketed by one pair of events, so decode_ms
+            # is the GPU span of the decode phase (host submission runs ahead of it)
+            e = [ev(), ev(), ev()]
+            e[0].record(self.stream)
+            e[1].record(self.stream)
             for layer in range(self.nlayers):
-                e = [ev(), ev(), ev()]
-                e[0].record(self.stream)
-                b.append(kv, kv, layer, 1, self.stream)
-                e[1].record(self.stream)
-                b.decode(q, o, layer, stream=self.stream)
-                e[2].record(self.stream)
-                marks.append(("dec", e))
+                b.decode(q, o, layer, stream=self.stream, k=kv, v=kv)
+            e[2].record(self.stream)
+            marks.append(("dec", e))
             for layer in range(self.nlayers):
                 kvb, _ = b.decode_bytes(layer)
                 st["decode_bytes"] += kvb
-            for m, ids in groups:
-                L, H, Hq = self.shapes[m]
-                st["append_bytes"] += len(ids) * L * 2 * H * 128 * 2 * 2  # read + write of the new token
         for c, rs in pre_ok.items():
             groups = [(m, [r.rid for r in rs if r.model == m]) for m in range(self.M)]
             groups = [g for g in groups if g[1]]
@@ -345,6 +340,7 @@ class ChurnEngine:
             "alloc_ops_per_s": round((st["grow_ops"] + st["free_ops"]) / max(st["alloc_s"], 1e-9), 1),
             "mean_occupancy": round(st["occupancy_sum"] / it, 4),
             "decode_GBps": round(st["decode_bytes"] / max(st["decode_ms"], 1e-9) / 1e6, 1),
+            # prefill-chunk appends (a decode step's append is fused into its decode launch)
             "append_GBps": round(st["append_bytes"] / max(st["append_ms"], 1e-9) / 1e6, 1),
             "prefill_TFLOPs": round(st["prefill_flops"] / max(st["prefill_ms"], 1e-9) / 1e9, 1),
             "decode_ms": round(st["decode_ms"], 2), "prefill_ms": round(st["prefill_ms"], 2),
