@@ -237,9 +237,13 @@ __device__ __forceinline__ void tmem_st16u(uint32_t taddr, const uint32_t (&v)[1
 }
 
 __device__ __forceinline__ float ex2(float x) {
+#ifdef SKV_PF_NOMUFU  // diagnostic build only (wrong results): exponentials off the MUFU
+  return fmaf(x, 0.0078125f, 0.5f);
+#else
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+#endif
 }
 
 // v2: 64-key tiles (112 KiB smem -> two CTAs per SM overlap each other's MMA and
@@ -1838,6 +1842,13 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v10(const __grid
         float* xmb = xm + (gj & 1) * 256;
         float ls[4] = {0.f, 0.f, 0.f, 0.f};
         uint32_t pk[32];
+#ifdef SKV_PF_NOSOFTMAX  // diagnostic build only (wrong results): protocol without the tile math
+        if (true) {
+#pragma unroll
+          for (int kk = 0; kk < 32; ++kk) pk[kk] = 0x3c003c00u;
+          PF_T(3, named_bar(nbar, 64));
+        } else
+#endif
         if (j > 0 && !tile_masked && !(p.dbg & 4) && __all_sync(0xffffffffu, m != -INFINITY)) {
           // Speculative path: exponentials against the running max m while the second 32-column
           // TMEM load is in flight, the row max exchanged only after them; valid unless the tile

@@ -15,7 +15,7 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint
   d |= (uint64_t)2 << 61;
   return d;
 }
-__global__ void __launch_bounds__(128, 1) bench(int n, int iters, int ts, long long* out, int vary) {
+__global__ void __launch_bounds__(128, 1) bench(int n, int iters, int ts, long long* out, int vary, int warpmode) {
   extern __shared__ __align__(1024) char smem[];
   __shared__ uint32_t slot;
   __shared__ __align__(8) uint64_t bar;
@@ -37,7 +37,40 @@ __global__ void __launch_bounds__(128, 1) bench(int n, int iters, int ts, long l
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = slot;
-  if (tid == 0 && rank == 0) {
+  if (warpmode && tid < 32 && rank == 0) {  // whole warp walks the loop; elect.sync picks the issuer
+    uint32_t idesc = (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+    const uint32_t sa = smem_u32(smem), sb = smem_u32(smem + 32768);
+    const uint64_t da = make_desc(sa, 16, 1024), db = make_desc(sb, 16, 1024);
+    long long t0 = clock64();
+    for (int i = 0; i < iters; i += 8) {
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const uint64_t bd = db + (uint64_t)((((i >> 3) % 4) * 16384 + (kk >> 2) * 8192 + (kk & 3) * 32) >> 4);
+        if (ts)
+          asm volatile(
+              "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+              "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem + (kk & 1) * 128),
+              "r"(tmem + 384 + kk * 8), "l"(bd), "r"(idesc), "r"(1));
+        else
+          asm volatile(
+              "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+              "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + (kk & 1) * 256),
+              "l"(da + (uint64_t)(((kk >> 2) * 16384 + (kk & 3) * 32) >> 4)), "l"(bd), "r"(idesc), "r"(1));
+      }
+    }
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+            smem_u32(&bar)), "h"((unsigned short)3)
+        : "memory");
+    uint32_t ok = 0;
+    while (!ok)
+      asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                   : "=r"(ok) : "r"(smem_u32(&bar)) : "memory");
+    long long t1 = clock64();
+    if (tid == 0) out[blockIdx.x / 2] = t1 - t0;
+  }
+  if (!warpmode && tid == 0 && rank == 0) {
     uint32_t idesc = (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
     const uint32_t sa = smem_u32(smem), sb = smem_u32(smem + 32768);
     long long t0 = clock64();
@@ -86,7 +119,7 @@ int main() {
   long long* d;
   cudaMalloc(&d, 74 * sizeof(long long));
   cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024 + 1024);
-  for (int vary = 0; vary < 2; ++vary)
+  for (int vary = 0; vary < 3; ++vary)
   for (int ts = 0; ts < 2; ++ts)
     for (int n : {128}) {
       if (ts && n > 128) continue;
@@ -107,7 +140,7 @@ int main() {
         cudaEventCreate(&e0);
         cudaEventCreate(&e1);
         cudaEventRecord(e0);
-        cudaLaunchKernelEx(&cfg, bench, n, iters, ts, d, vary);
+        cudaLaunchKernelEx(&cfg, bench, n, iters, ts, d, vary & 1, vary == 2);
         cudaEventRecord(e1);
         cudaError_t err = cudaDeviceSynchronize();
         if (err != cudaSuccess) { printf("err %s\n", cudaGetErrorString(err)); return 1; }
@@ -119,7 +152,7 @@ int main() {
         for (int i = 0; i < 74; ++i) cyc += h[i];
         cyc /= 74;
         const double macs_sm = 128.0 * n * 16;  // per SM per instruction
-        printf("%s pair %s N=%d: %.1f clk/MMA, %.0f MAC/clk/SM, event %.3f ms -> %.1f TFLOP/s (all SMs)\n", vary ? "varying addr" : "fixed addr  ", ts ? "TS" : "SS", n,
+        printf("%s pair %s N=%d: %.1f clk/MMA, %.0f MAC/clk/SM, event %.3f ms -> %.1f TFLOP/s (all SMs)\n", vary == 2 ? "warp+elect, base+const" : vary ? "varying addr" : "fixed addr  ", ts ? "TS" : "SS", n,
                cyc / iters, macs_sm * iters / cyc, ms, 2 * macs_sm * iters * 148 / (ms * 1e-3) / 1e12);
       }
     }
