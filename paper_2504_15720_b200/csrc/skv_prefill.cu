@@ -1738,43 +1738,64 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v10(const __grid
           PF_T(1, mbar_wait(&kv_full[gj % kStagesV10], (gj / kStagesV10) & 1));
           tc_fence_after();
         };
-        auto qk = [&](int j) {
+        // descriptors of a tile's 8 MMAs are materialised before the barrier wait that gates
+        // them, so the issue burst after the wait is MMAs only (per-MMA descriptor arithmetic
+        // on the issuing thread left the 64-clk MMAs issue-bound, profiles/r01_prefill_v10_diagnostics.txt)
+        auto k_descs = [&](int j, uint64_t (&d)[8]) {
+          const uint32_t sK = smem_u32(kvbase + ((j0 + j) % kStagesV10) * kKV10);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) d[kk] = make_desc(sK + (kk >> 2) * kKVHalf + (kk & 3) * 32, 16, 1024);
+        };
+        auto v_descs = [&](int j, uint64_t (&d)[8]) {
+          const uint32_t sV = smem_u32(kvbase + ((j0 + j) % kStagesV10) * kKV10) + 2 * kKVHalf;
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) d[kk] = make_desc(sV + kk * 2048, 2 * kKVHalf, 1024);
+        };
+        auto pin = [](const uint64_t (&d)[8]) {  // force the values into registers here
+          asm volatile("" ::"l"(d[0]), "l"(d[1]), "l"(d[2]), "l"(d[3]), "l"(d[4]), "l"(d[5]), "l"(d[6]), "l"(d[7]));
+        };
+        auto qk = [&](int j, const uint64_t (&d)[8]) {
           const uint32_t gj = j0 + j;
-          const uint32_t sK = smem_u32(kvbase + (gj % kStagesV10) * kKV10);
           const uint32_t tS = tmem + 128 + (gj & 1) * 128;
 #pragma unroll
-          for (int kk = 0; kk < kD / 16; ++kk) {
-            const uint32_t koff = (kk >> 2) * kKVHalf + (kk & 3) * 32;
-            mma_f16_ts_pair(tS, tmem + 384 + kk * 8, make_desc(sK + koff, 16, 1024), idesc_qk, kk > 0);
-          }
+          for (int kk = 0; kk < 8; ++kk) mma_f16_ts_pair(tS, tmem + 384 + kk * 8, d[kk], idesc_qk, kk > 0);
           mma_commit_pair(&s_full[gj & 1]);
         };
-        auto pv = [&](int j) {
+        auto pv = [&](int j, const uint64_t (&d)[8]) {
           const uint32_t gj = j0 + j;
-          const uint32_t sV = smem_u32(kvbase + (gj % kStagesV10) * kKV10) + 2 * kKVHalf;
           const uint32_t tP = tmem + 128 + (gj & 1) * 128;
 #pragma unroll
-          for (int kk = 0; kk < kKT10 / 16; ++kk)
-            mma_f16_ts_pair(tmem, tP + kk * 8, make_desc(sV + kk * 2048, 2 * kKVHalf, 1024), idesc_pv,
-                            (j > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < 8; ++kk) mma_f16_ts_pair(tmem, tP + kk * 8, d[kk], idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
           mma_commit_pair(&pv_done[gj & 1]);
           mma_commit_pair(&kv_empty[gj % kStagesV10]);
         };
-        PF_T(0, mbar_wait(q_full, k & 1));
-        tc_fence_after();
-        wait_kv(0);
-        qk(0);
-        if (J > 1) {
-          wait_kv(1);
-          qk(1);
+        {
+          uint64_t d0[8], d1[8];
+          k_descs(0, d0);
+          if (J > 1) k_descs(1, d1);
+          pin(d0);
+          pin(d1);
+          PF_T(0, mbar_wait(q_full, k & 1));
+          tc_fence_after();
+          wait_kv(0);
+          qk(0, d0);
+          if (J > 1) {
+            wait_kv(1);
+            qk(1, d1);
+          }
         }
         for (int j = 0; j < J; ++j) {
+          uint64_t vd[8], kd[8];
+          v_descs(j, vd);
+          k_descs(j + 2, kd);
+          pin(vd);
+          pin(kd);
           PF_T(2, mbar_wait(&p_full[(j0 + j) & 1], ((j0 + j) >> 1) & 1));
           tc_fence_after();
-          pv(j);
+          pv(j, vd);
           if (j + 2 < J) {
             wait_kv(j + 2);
-            qk(j + 2);
+            qk(j + 2, kd);
           }
         }
         jt += J;
