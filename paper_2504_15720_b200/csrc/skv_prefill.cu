@@ -1580,7 +1580,7 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v10(const __grid
   extern __shared__ __align__(1024) char smem[];
   if (smem_u32(smem) & 1023) __trap();
 #ifdef SKV_PF_TRACE
-  long long pf_acc[4] = {0, 0, 0, 0};
+  long long pf_acc[5] = {0, 0, 0, 0, 0};
   const long long pf_start = clock64();
   long long pf_tiles = 0;
 #endif
@@ -1726,6 +1726,8 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v10(const __grid
     if (lane == 0 && rank == 0) {
       const uint32_t idesc_qk = make_idesc_pair(p.dtype, 0);
       const uint32_t idesc_pv = make_idesc_pair(p.dtype, 1);
+      const uint64_t k_desc0 = make_desc(smem_u32(kvbase), 16, 1024);
+      const uint64_t v_desc0 = make_desc(smem_u32(kvbase) + 2 * kKVHalf, 2 * kKVHalf, 1024);
       uint32_t jt = 0;
       for (uint32_t k = 0;; ++k) {
         const int idx = next_item(k);
@@ -1741,15 +1743,17 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v10(const __grid
         // descriptors of a tile's 8 MMAs are materialised before the barrier wait that gates
         // them, so the issue burst after the wait is MMAs only (per-MMA descriptor arithmetic
         // on the issuing thread left the 64-clk MMAs issue-bound, profiles/r01_prefill_v10_diagnostics.txt)
+        // descriptor = base descriptor of stage 0 + (byte offset >> 4) in the address field
+        // (shared-memory addresses < 256 KiB: the 14-bit field never carries)
         auto k_descs = [&](int j, uint64_t (&d)[8]) {
-          const uint32_t sK = smem_u32(kvbase + ((j0 + j) % kStagesV10) * kKV10);
+          const uint64_t b = k_desc0 + (uint64_t)(((j0 + j) % kStagesV10) * (kKV10 >> 4));
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk) d[kk] = make_desc(sK + (kk >> 2) * kKVHalf + (kk & 3) * 32, 16, 1024);
+          for (int kk = 0; kk < 8; ++kk) d[kk] = b + (uint64_t)(((kk >> 2) * kKVHalf + (kk & 3) * 32) >> 4);
         };
         auto v_descs = [&](int j, uint64_t (&d)[8]) {
-          const uint32_t sV = smem_u32(kvbase + ((j0 + j) % kStagesV10) * kKV10) + 2 * kKVHalf;
+          const uint64_t b = v_desc0 + (uint64_t)(((j0 + j) % kStagesV10) * (kKV10 >> 4));
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk) d[kk] = make_desc(sV + kk * 2048, 2 * kKVHalf, 1024);
+          for (int kk = 0; kk < 8; ++kk) d[kk] = b + (uint64_t)((kk * 2048) >> 4);
         };
         auto pin = [](const uint64_t (&d)[8]) {  // force the values into registers here
           asm volatile("" ::"l"(d[0]), "l"(d[1]), "l"(d[2]), "l"(d[3]), "l"(d[4]), "l"(d[5]), "l"(d[6]), "l"(d[7]));
@@ -1786,16 +1790,18 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v10(const __grid
         }
         for (int j = 0; j < J; ++j) {
           uint64_t vd[8], kd[8];
-          v_descs(j, vd);
-          k_descs(j + 2, kd);
-          pin(vd);
-          pin(kd);
+          PF_T(4, {
+            v_descs(j, vd);
+            k_descs(j + 2, kd);
+            pin(vd);
+            pin(kd);
+          });
           PF_T(2, mbar_wait(&p_full[(j0 + j) & 1], ((j0 + j) >> 1) & 1));
           tc_fence_after();
-          pv(j, vd);
+          PF_T(3, pv(j, vd));
           if (j + 2 < J) {
             wait_kv(j + 2);
-            qk(j + 2, kd);
+            PF_T(3, qk(j + 2, kd));
           }
         }
         jt += J;
@@ -2024,9 +2030,10 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v10(const __grid
     unsigned long long* t = p.trace + (size_t)blockIdx.x * 16;
     if (warp == kLoadWarp && lane == 0) t[0] = pf_acc[0];
     if (warp == kMmaWarp && lane == 0)
-      for (int i = 0; i < 3; ++i) t[1 + i] = pf_acc[i];
+      for (int i = 0; i < 4; ++i) t[1 + i] = pf_acc[i];
     if (warp < kSoftmaxWarps && (tid & 127) == 0)
       for (int i = 0; i < 4; ++i) t[5 + 4 * (warp >> 2) + i] = pf_acc[i];
+    if (warp == kMmaWarp && lane == 0) t[15] = pf_acc[4];
     if (tid == 0) {
       t[13] = clock64() - pf_start;
       t[14] = pf_tiles;

@@ -41,7 +41,7 @@ names = ["load:kv_empty", "mma:q_full", "mma:kv_full", "mma:p_full_A", "mma:p_fu
 if os.environ.get("SEAKV_PREFILL_V") in ("10", "11"):  # CTA pairs: softmax halves c=0/1 of the same rows
     names = ["load:kv_empty", "mma:q_full", "mma:kv_full", "mma:p_full", "mma:issue",
              "sm0:s_full", "sm0:pv_corr", "sm0:pv_last", "sm0:max_xchg", "sm1:s_full", "sm1:pv_corr", "sm1:pv_last",
-             "sm1:max_xchg"]
+             "sm1:max_xchg", "-", "-", "mma:descs"]
 res = {n: round(float((t[:, i] / tot).mean()), 4) for i, n in enumerate(names) if n != "-"}
 res["ctas"] = int(len(t))
 res["mean_cta_us_at_1.9GHz"] = round(float(tot.mean()) / 1.9e3, 1)
