@@ -1,27 +1,26 @@
 // skv_prefill.cu — causal chunked-prefill attention over the unified pool on the
 // 5th-generation tensor cores (tcgen05.mma, accumulators in TMEM), sm_100a.
 //
-// One CTA (4 warps, 128 threads) per (request, kv head, 128-row query tile).
-// GQA query rows are folded into M: row i of a tile is (token t0 + i/G, q head
-// kv_head*G + i%G), so one K/V tile feeds G query heads.  Per 128-key tile:
+// Each request's last n_new tokens attend causally to every key at or before their own
+// position; K/V are read through the request's block table (reference block layout,
+// kv_cache.hpp:178-182; per-(layer, kv head) runs of 16 tokens).  GQA query
+// rows are folded into M: row i of a 128-row query tile is (token t0 + i/G, q head
+// kv_head*G + i%G), so one K/V tile feeds G query heads.
 //
-//   K_j, V_j  : gathered from the pool through the block table with cp.async
-//               (16 B per thread, written straight into the 128B-swizzled UMMA
-//               operand layout), double buffered so tile j+1 streams in while
-//               tile j is on the tensor cores;
-//   S   = Q·K_jᵀ    tcgen05.mma kind::f16, M=128 N=128 K=16 x8, fp32 in TMEM
-//   softmax         thread i owns row i: tcgen05.ld its S row from TMEM lanes,
-//                   causal mask, online max/sum in the log2 domain, P (fp16/bf16)
-//                   written to smem in the swizzled K-major layout;
-//   O_j = P·V_j     tcgen05.mma (B = V, MN-major), fp32 in TMEM, folded into the
-//                   per-thread fp32 output row with the softmax correction.
+// Kernels (SEAKV_PREFILL_V selects; DESIGN.md §5 has the measurements):
+//   v10 (default) prefill_kernel_v10: CTA pairs, one 256-row tcgen05.mma.cta_group::2 per
+//       K=16 step (N = 128 keys / 128 dims), K/V halves per SM by TMA, S double-buffered
+//       in TMEM, persistent with a dynamic work counter;
+//   v9  prefill_kernel_v9: one CTA per SM, two 128-row tiles ping-ponging on 64-key tiles;
+//   v2  prefill_kernel: one CTA per tile with cp.async staging -- the fallback when the pool
+//       has no TMA descriptor.
 //
-// UMMA operand layouts (cute canonical SW128): a [R rows x 128
-// d] fp16 tile is two 64-element column halves of R x 128 B; row r of a half at
-// (r/8)*1024 + (r%8)*128, 16-byte chunk c stored at chunk c ^ (r%8).  Q, K and P
-// use K-major descriptors (SBO = 1024 B, advance 32 B per K=16 step); V uses an
-// MN-major descriptor (LBO = 16 KiB between d-halves, SBO = 1024 B, advance
-// 2 KiB per 16 keys).
+// UMMA operand layouts (cute canonical SW128): a [R rows x 128 d] fp16 tile is two
+// 64-element column halves of R x 128 B; row r of a half at (r/8)*1024 + (r%8)*128,
+// 16-byte chunk c stored at chunk c ^ (r%8).  Q and K use K-major descriptors (SBO =
+// 1024 B, advance 32 B per K=16 step); V uses an MN-major descriptor (SBO = 1024 B,
+// advance 2 KiB per 16 keys).  One TMA box {64 elements, 16 rows} = one 2 KiB d-half of a
+// native block's K or V run lands directly in this layout.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -503,19 +502,14 @@ __global__ void __launch_bounds__(kThreads, 2) prefill_kernel(const __grid_const
 }
 
 // ---------------------------------------------------------------------------------------
-// v3: warp-specialised ping-pong (FA4-style).  One CTA = two 128-row query tiles (A, B)
-// sharing every K/V tile; warps 0-3 run the softmax of tile A, warps 4-7 of tile B (both
-// warpgroups address TMEM lanes 0-127 via warp%4, in different columns), warp 8 issues
-// all tcgen05.mma, warps 9-10 stream Q and a 3-stage K/V ring with cp.async signalled
-// through mbarriers.  Tensor-core order: QK_A QK_B | PV_A QK_A' | PV_B QK_B' | ... so the
-// tensor core works on one tile while the other tile's softmax runs on the CUDA cores.
-constexpr int kStagesV3 = 5;  // K/V ring depth (P lives in TMEM, so smem holds only Q and K/V)
+// Warp-specialised kernels (v9, v10; earlier v3/v5/v7 steps are in git history and in
+// DESIGN.md): warps 0-7 softmax (two warps per TMEM lane quarter), warp 8 issues every
+// tcgen05.mma from one thread, warp 9 streams K/V with TMA, all handshakes on mbarriers.
 constexpr int kSoftmaxWarps = 8;             // 4 per query tile, one thread per query row
-constexpr int kMmaWarp = kSoftmaxWarps;      // warp 16
-constexpr int kLoadWarp = kSoftmaxWarps + 1; // warp 17
+constexpr int kMmaWarp = kSoftmaxWarps;      // warp 8
+constexpr int kLoadWarp = kSoftmaxWarps + 1; // warp 9
 constexpr int kThreadsV3 = (kSoftmaxWarps + 2) * 32;
 constexpr int kLoadThreads = 32;
-constexpr int kSmemV3 = 2 * kTileBytes + kStagesV3 * 2 * kKVBytes + 256;
 
 __device__ __forceinline__ void mbar_init_n(uint64_t* b, uint32_t n) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(n));
@@ -550,566 +544,17 @@ __device__ __forceinline__ void cp_async_arrive(uint64_t* b) {
 #define PF_T(slot, stmt) stmt
 #endif
 
-template <typename T>
-__global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v3(const __grid_constant__ DataParams p) {
-#ifdef SKV_PF_TRACE
-  long long pf_acc[4] = {0, 0, 0, 0};
-  const long long pf_start = clock64();
-#endif
-  extern __shared__ __align__(1024) char smem[];
-  if (smem_u32(smem) & 1023) __trap();
-  char* sQ[2] = {smem, smem + kTileBytes};
-  char* kvbase = smem + 2 * kTileBytes;
-  // P(j) is written by the softmax into TMEM over S(j) (fp16/bf16 pairs in the first 32
-  // columns of the S buffer) and read from there by the P.V MMA (A operand in TMEM), so the
-  // softmax never waits for a P buffer: it may run a key tile ahead of the tensor core.
-  uint64_t* bars = reinterpret_cast<uint64_t*>(kvbase + kStagesV3 * 2 * kKVBytes);
-  uint64_t* kv_full = bars;                       // [stages] count 1 (TMA arrive.expect_tx)
-  uint64_t* kv_empty = bars + kStagesV3;          // [stages] count 1 (tcgen05.commit after PV_B)
-  uint64_t* q_full = bars + 2 * kStagesV3;        // count 32 (cp.async arrive.noinc per loader lane)
-  uint64_t* s_full = bars + 2 * kStagesV3 + 1;    // [tile][S buffer] count 1
-  // per (tile, S/P buffer): each completes once per two key tiles and is waited on in
-  // order, so no waiter can fall two phases behind
-  uint64_t* p_full = bars + 2 * kStagesV3 + 5;    // [tile][buffer] count 128
-  uint64_t* pv_done = bars + 2 * kStagesV3 + 9;   // [tile][buffer] count 1
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStagesV3 + 13);
-
-  const int r = blockIdx.z, h = blockIdx.y;
-  const int grp = p.req_group[r];
-  const DataGroup& g = p.g[grp];
-  const int G = g.G;
-  const int q_len = p.n_new;
-  const int tileA = 2 * blockIdx.x;
-  if (!g.active || h >= g.Hkv || tileA * kRows >= q_len * G) return;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int handle = p.handles[r];
-  const int ctx = p.req_tokens[handle];
-  const int start = ctx - q_len;
-  const int tpt = kRows / G;
-  const int t0A = tileA * tpt;
-  const int n_keys = min(ctx, start + t0A + 2 * tpt);  // the last row of tile B
-  const int n_kt = (n_keys + kKT - 1) / kKT;
-  const int rl = r - g.req_begin;
-
-  if (warp == kMmaWarp) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  if (tid == 0) {
-    for (int i = 0; i < kStagesV3; ++i) {
-      mbar_init_n(&kv_full[i], 1);  // the TMA thread's arrive.expect_tx
-      mbar_init_n(&kv_empty[i], 1);
-    }
-    mbar_init_n(q_full, kLoadThreads);
-    for (int i = 0; i < 4; ++i) mbar_init_n(&s_full[i], 1);
-    for (int i = 0; i < 4; ++i) {
-      mbar_init_n(&p_full[i], 128);
-      mbar_init_n(&pv_done[i], 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == kLoadWarp) {  // ----------------------------------------------- loader
-    const int lt = lane;  // 0..31
-    const int c = lt & 15;
-    // Q tiles A and B: 256 rows x 16 chunks
-    for (int i = 0; i < 128; ++i) {
-      const int idx = (lt >> 4) + 2 * i;  // 0..255
-      const int x = idx >> 7, row = idx & 127;
-      const int tok = t0A + x * tpt + row / G, gg = row % G;
-      const bool ok = tok < q_len;
-      const char* src = reinterpret_cast<const char*>(g.q) +
-                        (((size_t)rl * q_len + (ok ? tok : 0)) * g.Hq + h * G + gg) * (kD * 2) + c * 16;
-      cp_async16(smem_u32(sQ[x]) + sw_off(row, c), src, ok);
-    }
-    cp_async_arrive(q_full);
-    if (lane == 0) {  // one thread streams K/V: 16 TMA boxes (2 KiB each) per 64-key tile
-      const int2* row_tab = p.req_table + (size_t)handle * p.cap;
-      const long long base_off = g.layer_off + (long long)h * g.head_stride;
-      const int n_blk = (n_keys + kTpb - 1) / kTpb;
-      for (int j = 0; j < n_kt; ++j) {
-        const int st = j % kStagesV3;
-        if (j >= kStagesV3) PF_T(0, mbar_wait(&kv_empty[st], ((j / kStagesV3) - 1) & 1));
-        int2 e[4];
-        int nb = 0;
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const int bi = j * 4 + b;
-          e[b] = bi < n_blk ? row_tab[bi] : make_int2(-1, 0);
-          nb += bi < n_blk;
-        }
-        mbar_expect_tx_v3(&kv_full[st], nb * 4 * 2048);
-        const uint32_t sK = smem_u32(kvbase + st * 2 * kKVBytes), sV = sK + kKVBytes;
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          if (e[b].x < 0) continue;
-          const int row0 = (int)(((long long)e[b].x * p.merged_stride + (long long)e[b].y * g.native_stride +
-                                  base_off) >> 8);
-#pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
-            tma_load_2d(sK + hh * kKVHalf + b * 2048, &p.kv_tmap, hh * 64, row0, &kv_full[st]);
-            tma_load_2d(sV + hh * kKVHalf + b * 2048, &p.kv_tmap, hh * 64, row0 + kTpb, &kv_full[st]);
-          }
-        }
-      }
-    }
-    cp_async_wait<0>();
-  } else if (warp == kMmaWarp) {  // -------------------------------------------- MMA issue
-    if (lane == 0) {
-      const uint32_t idesc_qk = make_idesc_n(p.dtype, 0, kKT);
-      const uint32_t idesc_pv = make_idesc_n(p.dtype, 1, kD);
-      auto qk = [&](int x, int j) {  // S[x][j&1] = Q_x . K_j^T
-        const int st = j % kStagesV3;
-        const uint32_t sK = smem_u32(kvbase + st * 2 * kKVBytes);
-#pragma unroll
-        for (int k = 0; k < kD / 16; ++k) {
-          const uint32_t qoff = (k >> 2) * kHalf + (k & 3) * 32;
-          const uint32_t koff = (k >> 2) * kKVHalf + (k & 3) * 32;
-          mma_f16(tmem + x * 128 + (j & 1) * 64, make_desc(smem_u32(sQ[x]) + qoff, 16, 1024),
-                  make_desc(sK + koff, 16, 1024), idesc_qk, k > 0);
-        }
-        mma_commit(&s_full[x * 2 + (j & 1)]);
-      };
-      auto pv = [&](int x, int j) {  // O[x] += P_x(j) . V_j, P from TMEM (16 keys = 8 columns)
-        const int st = j % kStagesV3;
-        const uint32_t sV = smem_u32(kvbase + st * 2 * kKVBytes + kKVBytes);
-        const uint32_t tP = tmem + x * 128 + (j & 1) * 64;
-#pragma unroll
-        for (int k = 0; k < kKT / 16; ++k)
-          mma_f16_ts(tmem + 256 + x * 128, tP + k * 8, make_desc(sV + k * 2048, kKVHalf, 1024), idesc_pv,
-                     (j > 0 || k > 0) ? 1u : 0u);
-        mma_commit(&pv_done[2 * x + (j & 1)]);
-      };
-      auto wait_kv = [&](int j) {
-        PF_T(1, mbar_wait(&kv_full[j % kStagesV3], (j / kStagesV3) & 1));
-        fence_async_smem();  // cp.async / TMA data -> tensor-core reads
-        tc_fence_after();
-      };
-      // QK runs two tiles ahead of PV (S double-buffered in TMEM), so the softmax of
-      // tile j+1 never waits for PV(j): order QK_A0 QK_B0 QK_A1 QK_B1 | PV_A0 QK_A2 PV_B0 QK_B2 | ...
-      PF_T(0, mbar_wait(q_full, 0));
-      wait_kv(0);
-      qk(0, 0);
-      qk(1, 0);
-      if (n_kt > 1) {
-        wait_kv(1);
-        qk(0, 1);
-        qk(1, 1);
-      }
-      for (int j = 0; j < n_kt; ++j) {
-        PF_T(2, mbar_wait(&p_full[j & 1], (j >> 1) & 1));
-        tc_fence_after();
-        pv(0, j);
-        if (j + 2 < n_kt) {
-          wait_kv(j + 2);
-          qk(0, j + 2);
-        }
-        PF_T(3, mbar_wait(&p_full[2 + (j & 1)], (j >> 1) & 1));
-        tc_fence_after();
-        pv(1, j);
-        mma_commit(&kv_empty[j % kStagesV3]);
-        if (j + 2 < n_kt) qk(1, j + 2);
-      }
-    }
-    __syncwarp();
-  } else {  // ------------------------------------------------------------- softmax warps
-    const int x = warp >> 2;  // 0 = tile A, 1 = tile B; both warpgroups address TMEM lanes 0-127
-    const int row = tid & 127;
-    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-    const uint32_t tS0 = tmem + x * 128 + lane_off, tO = tmem + 256 + x * 128 + lane_off;
-    const int t0 = t0A + x * tpt;
-    const int my_tok = t0 + row / G;
-    const bool row_ok = my_tok < q_len;
-    const int my_pos = start + my_tok;
-    const bool tail_rows = t0 + tpt > q_len;
-    const float c2 = p.scale_log2;
-    float m = -INFINITY, l = 0.f;
-    for (int j = 0; j < n_kt; ++j) {
-      PF_T(0, mbar_wait(&s_full[x * 2 + (j & 1)], (j >> 1) & 1));
-      tc_fence_after();
-      const uint32_t tS = tS0 + (j & 1) * 64;
-      if (x == 0 && j == n_kt - 1 && (j + 1) * kKT > ctx) {
-        // last tile: rows of TMA-loaded blocks past ctx are not this request's K/V (may be NaN)
-        char* sV = kvbase + (j % kStagesV3) * 2 * kKVBytes + kKVBytes;
-        const int c = row & 15;
-        for (int key = row >> 4; key < kKT; key += 8)
-          if (j * kKT + key >= ctx) *reinterpret_cast<uint4*>(sV + sw_kv(key, c)) = make_uint4(0, 0, 0, 0);
-      }
-      float s[64];
-      tmem_ld64(tS, s);
-      const bool masked = (j * kKT + kKT - 1 > start + t0) || tail_rows;
-      if (masked) {
-#pragma unroll
-        for (int k = 0; k < 64; ++k)
-          if (!(row_ok && j * kKT + k <= my_pos)) s[k] = -INFINITY;
-      }
-      float mx4[4] = {s[0], s[1], s[2], s[3]};
-#pragma unroll
-      for (int k = 4; k < 64; ++k) mx4[k & 3] = fmaxf(mx4[k & 3], s[k]);
-      const float mt = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * c2;
-      const bool need = mt > m + kRescale;
-      float alpha = 1.f;
-      if (need) {
-        alpha = ex2(m - mt);
-        l *= alpha;
-        m = mt;
-      }
-      // the O correction needs PV(j-1) done (it cannot have run further: PV(j) needs P(j))
-      if (j > 0 && __any_sync(0xffffffffu, need)) {
-        PF_T(1, mbar_wait(&pv_done[2 * x + ((j - 1) & 1)], ((j - 1) >> 1) & 1));
-        tc_fence_after();
-#pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-          float o[32];
-          tmem_ld32(tO + cc * 32, o);
-#pragma unroll
-          for (int k = 0; k < 32; ++k) o[k] *= alpha;
-          tmem_st32(tO + cc * 32, o);
-        }
-      }
-      const float mu = (m == -INFINITY) ? 0.f : m;
-      float ls[4] = {0.f, 0.f, 0.f, 0.f};
-      uint32_t pk[32];
-#pragma unroll
-      for (int k = 0; k < 64; k += 2) {
-        const float v0 = ex2(fmaf(s[k], c2, -mu));
-        const float v1 = ex2(fmaf(s[k + 1], c2, -mu));
-        ls[(k >> 1) & 3] += v0 + v1;
-        pk[k >> 1] = pack2<T>(v0, v1);
-      }
-      tmem_st32u(tS, pk);  // P(j) over S(j): row = lane, keys (2c, 2c+1) in column c
-      l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
-      fence_async_smem();  // the last tile's V-row zeroing (generic stores) -> tensor core
-      tc_fence_before();
-      mbar_arrive(&p_full[2 * x + (j & 1)]);
-    }
-    PF_T(2, mbar_wait(&pv_done[2 * x + ((n_kt - 1) & 1)], ((n_kt - 1) >> 1) & 1));
-    tc_fence_after();
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-    char* dst = reinterpret_cast<char*>(g.out) +
-                (((size_t)rl * q_len + (row_ok ? my_tok : 0)) * g.Hq + h * G + row % G) * (kD * 2);
-#pragma unroll
-    for (int cc = 0; cc < 4; ++cc) {
-      float o[32];
-      tmem_ld32(tO + cc * 32, o);
-      if (row_ok) {
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {
-          uint4 v;
-          v.x = pack2<T>(o[8 * q4] * inv, o[8 * q4 + 1] * inv);
-          v.y = pack2<T>(o[8 * q4 + 2] * inv, o[8 * q4 + 3] * inv);
-          v.z = pack2<T>(o[8 * q4 + 4] * inv, o[8 * q4 + 5] * inv);
-          v.w = pack2<T>(o[8 * q4 + 6] * inv, o[8 * q4 + 7] * inv);
-          *reinterpret_cast<uint4*>(dst + cc * 64 + q4 * 16) = v;
-        }
-      }
-    }
-  }
-#ifdef SKV_PF_TRACE
-  if (p.trace) {  // [cta][16]: loader 0, mma 1-4, softmax A 5-8, softmax B 9-12, cta 13, n_kt 14
-    unsigned long long* t = p.trace + ((size_t)(blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 16;
-    if (warp == kLoadWarp && lane == 0) t[0] = pf_acc[0];
-    if (warp == kMmaWarp && lane == 0)
-      for (int i = 0; i < 4; ++i) t[1 + i] = pf_acc[i];
-    if (warp < kSoftmaxWarps && (tid & 127) == 0)
-      for (int i = 0; i < 3; ++i) t[5 + 4 * (warp >> 2) + i] = pf_acc[i];
-    if (tid == 0) {
-      t[13] = clock64() - pf_start;
-      t[14] = n_kt;
-    }
-  }
-#endif
-  tc_fence_before();
-  __syncthreads();
-  if (warp == kMmaWarp) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
-  }
-}
-
 // ---------------------------------------------------------------------------------------
-// v7: Q in TMEM.  With Q and K both read from shared memory, a 128x64x16 QK^T MMA moves
-// 6 KiB of operands per 32 tensor-core cycles, above the 128 B/clk shared-memory read
-// rate: it issues at 48 clk instead of 32 (scripts/umma_bench).  Here the softmax warps
-// write their Q rows into TMEM once per CTA (one thread per row, tcgen05.st) and QK^T is
-// the TS form (A = Q from TMEM, B = K from smem): shared memory then feeds only K and V
-// (64 B/clk), the tensor core runs both MMAs at full rate, and the Q buffers' 64 KiB of
-// smem become two more K/V stages (7).  TMEM: Q_A | Q_B (64 cols each) | S_A | S_B (64) |
-// O_A | O_B (128); S is single-buffered per tile (P written over it), so per tile the
-// chain is softmax(j) -> P.V(j) -> QK(j+1) -> softmax(j+1), the other tile's softmax
-// running meanwhile.
+// v9 layout (from v7): Q in TMEM.  With Q and K both read from shared memory, a 128x64x16
+// QK^T MMA moves 6 KiB of operands per 32 tensor-core cycles, above the 128 B/clk
+// shared-memory read rate, and issues at 48 clk instead of 32 (scripts/umma_bench).  The
+// softmax warps write their Q rows into TMEM once per item (tcgen05.st) and QK^T is the TS
+// form; the Q buffers' 64 KiB of smem become two more K/V stages (7).  TMEM: Q_A | Q_B (64
+// cols each) | S_A | S_B (64) | O_A | O_B (128); S is single-buffered per tile (P written
+// over it), so per tile the chain is softmax(j) -> P.V(j) -> QK(j+1) -> softmax(j+1), the
+// other tile's softmax running meanwhile.
 constexpr int kStagesV7 = 7;
 constexpr int kSmemV7 = kStagesV7 * 2 * kKVBytes + 256;
-
-template <typename T>
-__global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v7(const __grid_constant__ DataParams p) {
-  extern __shared__ __align__(1024) char smem[];
-  if (smem_u32(smem) & 1023) __trap();
-#ifdef SKV_PF_TRACE
-  long long pf_acc[4] = {0, 0, 0, 0};
-  const long long pf_start = clock64();
-#endif
-  char* kvbase = smem;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(kvbase + kStagesV7 * 2 * kKVBytes);
-  uint64_t* kv_full = bars;                      // [stages]
-  uint64_t* kv_empty = bars + kStagesV7;         // [stages]
-  uint64_t* q_full = bars + 2 * kStagesV7;       // count 256: every softmax thread stored its Q row
-  uint64_t* s_full = bars + 2 * kStagesV7 + 1;   // [tile]
-  uint64_t* p_full = bars + 2 * kStagesV7 + 3;   // [tile] count 128
-  uint64_t* pv_done = bars + 2 * kStagesV7 + 5;  // [tile]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * kStagesV7 + 7);
-
-  const int r = blockIdx.z, h = blockIdx.y;
-  const int grp = p.req_group[r];
-  const DataGroup& g = p.g[grp];
-  const int G = g.G;
-  const int q_len = p.n_new;
-  const int tileA = 2 * blockIdx.x;
-  if (!g.active || h >= g.Hkv || tileA * kRows >= q_len * G) return;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int handle = p.handles[r];
-  const int ctx = p.req_tokens[handle];
-  const int start = ctx - q_len;
-  const int tpt = kRows / G;
-  const int t0A = tileA * tpt;
-  const int n_keys = min(ctx, start + t0A + 2 * tpt);
-  const int n_kt = (n_keys + kKT - 1) / kKT;
-  const int rl = r - g.req_begin;
-
-  if (warp == kMmaWarp) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  if (tid == 0) {
-    for (int i = 0; i < kStagesV7; ++i) {
-      mbar_init_n(&kv_full[i], 1);
-      mbar_init_n(&kv_empty[i], 1);
-    }
-    mbar_init_n(q_full, 2 * 128);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init_n(&s_full[i], 1);
-      mbar_init_n(&p_full[i], 128);
-      mbar_init_n(&pv_done[i], 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == kLoadWarp) {  // ----------------------------------------------- K/V streaming
-    if (lane == 0) {
-      const int2* row_tab = p.req_table + (size_t)handle * p.cap;
-      const long long base_off = g.layer_off + (long long)h * g.head_stride;
-      const int n_blk = (n_keys + kTpb - 1) / kTpb;
-      for (int j = 0; j < n_kt; ++j) {
-        const int st = j % kStagesV7;
-        if (j >= kStagesV7) PF_T(0, mbar_wait(&kv_empty[st], ((j / kStagesV7) - 1) & 1));
-        int2 e[4];
-        int nb = 0;
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const int bi = j * 4 + b;
-          e[b] = bi < n_blk ? row_tab[bi] : make_int2(-1, 0);
-          nb += bi < n_blk;
-        }
-        mbar_expect_tx_v3(&kv_full[st], nb * 4 * 2048);
-        const uint32_t sK = smem_u32(kvbase + st * 2 * kKVBytes), sV = sK + kKVBytes;
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          if (e[b].x < 0) continue;
-          const int row0 = (int)(((long long)e[b].x * p.merged_stride + (long long)e[b].y * g.native_stride +
-                                  base_off) >> 8);
-#pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
-            tma_load_2d(sK + hh * kKVHalf + b * 2048, &p.kv_tmap, hh * 64, row0, &kv_full[st]);
-            tma_load_2d(sV + hh * kKVHalf + b * 2048, &p.kv_tmap, hh * 64, row0 + kTpb, &kv_full[st]);
-          }
-        }
-      }
-    }
-  } else if (warp == kMmaWarp) {  // -------------------------------------------- MMA issue
-    if (lane == 0) {
-      const uint32_t idesc_qk = make_idesc_n(p.dtype, 0, kKT);
-      const uint32_t idesc_pv = make_idesc_n(p.dtype, 1, kD);
-      auto qk = [&](int x, int j) {  // S_x = Q_x (TMEM, 8 columns per 16 dims) . K_j^T
-        const uint32_t sK = smem_u32(kvbase + (j % kStagesV7) * 2 * kKVBytes);
-#pragma unroll
-        for (int k = 0; k < kD / 16; ++k) {
-          const uint32_t koff = (k >> 2) * kKVHalf + (k & 3) * 32;
-          mma_f16_ts(tmem + 128 + x * 64, tmem + x * 64 + k * 8, make_desc(sK + koff, 16, 1024), idesc_qk, k > 0);
-        }
-        mma_commit(&s_full[x]);
-      };
-      auto pv = [&](int x, int j) {  // O_x += P_x(j) (TMEM, over S_x) . V_j
-        const uint32_t sV = smem_u32(kvbase + (j % kStagesV7) * 2 * kKVBytes + kKVBytes);
-#pragma unroll
-        for (int k = 0; k < kKT / 16; ++k)
-          mma_f16_ts(tmem + 256 + x * 128, tmem + 128 + x * 64 + k * 8, make_desc(sV + k * 2048, kKVHalf, 1024),
-                     idesc_pv, (j > 0 || k > 0) ? 1u : 0u);
-        mma_commit(&pv_done[x]);
-      };
-      auto wait_kv = [&](int j) {
-        PF_T(1, mbar_wait(&kv_full[j % kStagesV7], (j / kStagesV7) & 1));
-        tc_fence_after();
-      };
-      PF_T(0, mbar_wait(q_full, 0));
-      tc_fence_after();
-      wait_kv(0);
-      qk(0, 0);
-      qk(1, 0);
-      for (int j = 0; j < n_kt; ++j) {
-        PF_T(2, mbar_wait(&p_full[0], j & 1));
-        tc_fence_after();
-        pv(0, j);
-        if (j + 1 < n_kt) {
-          wait_kv(j + 1);
-          qk(0, j + 1);  // overwrites S_A / P_A(j) after P.V_A(j) in issue order
-        }
-        PF_T(3, mbar_wait(&p_full[1], j & 1));
-        tc_fence_after();
-        pv(1, j);
-        mma_commit(&kv_empty[j % kStagesV7]);
-        if (j + 1 < n_kt) qk(1, j + 1);
-      }
-    }
-    __syncwarp();
-  } else {  // ------------------------------------------------------------- softmax warps
-    const int x = warp >> 2;
-    const int row = tid & 127;
-    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-    const uint32_t tQ = tmem + x * 64 + lane_off, tS = tmem + 128 + x * 64 + lane_off;
-    const uint32_t tO = tmem + 256 + x * 128 + lane_off;
-    const int t0 = t0A + x * tpt;
-    const int my_tok = t0 + row / G;
-    const bool row_ok = my_tok < q_len;
-    const int my_pos = start + my_tok;
-    const bool tail_rows = t0 + tpt > q_len;
-    const float c2 = p.scale_log2;
-    {  // this thread's Q row -> TMEM lane `row`, 64 columns of packed pairs
-      const uint4* src = reinterpret_cast<const uint4*>(
-          reinterpret_cast<const char*>(g.q) +
-          (((size_t)rl * q_len + (row_ok ? my_tok : 0)) * g.Hq + h * G + row % G) * (kD * 2));
-#pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        uint32_t qv[32];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const uint4 v = row_ok ? src[hh * 8 + i] : make_uint4(0u, 0u, 0u, 0u);
-          qv[4 * i] = v.x;
-          qv[4 * i + 1] = v.y;
-          qv[4 * i + 2] = v.z;
-          qv[4 * i + 3] = v.w;
-        }
-        tmem_st32u(tQ + hh * 32, qv);
-      }
-      tc_fence_before();
-      mbar_arrive(q_full);
-    }
-    float m = -INFINITY, l = 0.f;
-    for (int j = 0; j < n_kt; ++j) {
-      PF_T(0, mbar_wait(&s_full[x], j & 1));
-      tc_fence_after();
-      if (x == 0 && j == n_kt - 1 && (j + 1) * kKT > n_keys) {
-        char* sV = kvbase + (j % kStagesV7) * 2 * kKVBytes + kKVBytes;
-        const int c = row & 15;
-        for (int key = row >> 4; key < kKT; key += 8)
-          if (j * kKT + key >= n_keys) *reinterpret_cast<uint4*>(sV + sw_kv(key, c)) = make_uint4(0, 0, 0, 0);
-      }
-      float s[64];
-      tmem_ld64(tS, s);
-      const bool masked = (j * kKT + kKT - 1 > start + t0) || tail_rows;
-      if (masked) {
-#pragma unroll
-        for (int k = 0; k < 64; ++k)
-          if (!(row_ok && j * kKT + k <= my_pos)) s[k] = -INFINITY;
-      }
-      float mx4[4] = {s[0], s[1], s[2], s[3]};
-#pragma unroll
-      for (int k = 4; k < 64; ++k) mx4[k & 3] = fmaxf(mx4[k & 3], s[k]);
-      const float mt = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * c2;
-      const bool need = mt > m + kRescale;
-      float alpha = 1.f;
-      if (need) {
-        alpha = ex2(m - mt);
-        l *= alpha;
-        m = mt;
-      }
-      // S(j) ready implies P.V(j-1) retired (issued before QK(j)); P.V(j) waits for P(j)
-      if (j > 0 && __any_sync(0xffffffffu, need)) {
-#pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-          float o[32];
-          tmem_ld32(tO + cc * 32, o);
-#pragma unroll
-          for (int k = 0; k < 32; ++k) o[k] *= alpha;
-          tmem_st32(tO + cc * 32, o);
-        }
-      }
-      const float mu = (m == -INFINITY) ? 0.f : m;
-      float ls[4] = {0.f, 0.f, 0.f, 0.f};
-      uint32_t pk[32];
-#pragma unroll
-      for (int k = 0; k < 64; k += 2) {
-        const float v0 = ex2(fmaf(s[k], c2, -mu));
-        const float v1 = ex2(fmaf(s[k + 1], c2, -mu));
-        ls[(k >> 1) & 3] += v0 + v1;
-        pk[k >> 1] = pack2<T>(v0, v1);
-      }
-      tmem_st32u(tS, pk);
-      l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
-      fence_async_smem();
-      tc_fence_before();
-      mbar_arrive(&p_full[x]);
-    }
-    PF_T(2, mbar_wait(&pv_done[x], (n_kt - 1) & 1));
-    tc_fence_after();
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-    char* dst = reinterpret_cast<char*>(g.out) +
-                (((size_t)rl * q_len + (row_ok ? my_tok : 0)) * g.Hq + h * G + row % G) * (kD * 2);
-#pragma unroll
-    for (int cc = 0; cc < 4; ++cc) {
-      float o[32];
-      tmem_ld32(tO + cc * 32, o);
-      if (row_ok) {
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {
-          uint4 v;
-          v.x = pack2<T>(o[8 * q4] * inv, o[8 * q4 + 1] * inv);
-          v.y = pack2<T>(o[8 * q4 + 2] * inv, o[8 * q4 + 3] * inv);
-          v.z = pack2<T>(o[8 * q4 + 4] * inv, o[8 * q4 + 5] * inv);
-          v.w = pack2<T>(o[8 * q4 + 6] * inv, o[8 * q4 + 7] * inv);
-          *reinterpret_cast<uint4*>(dst + cc * 64 + q4 * 16) = v;
-        }
-      }
-    }
-  }
-#ifdef SKV_PF_TRACE
-  if (p.trace) {  // same record layout as v3
-    unsigned long long* t = p.trace + ((size_t)(blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 16;
-    if (warp == kLoadWarp && lane == 0) t[0] = pf_acc[0];
-    if (warp == kMmaWarp && lane == 0)
-      for (int i = 0; i < 4; ++i) t[1 + i] = pf_acc[i];
-    if (warp < kSoftmaxWarps && (tid & 127) == 0)
-      for (int i = 0; i < 3; ++i) t[5 + 4 * (warp >> 2) + i] = pf_acc[i];
-    if (tid == 0) {
-      t[13] = clock64() - pf_start;
-      t[14] = n_kt;
-    }
-  }
-#endif
-  tc_fence_before();
-  __syncthreads();
-  if (warp == kMmaWarp) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
-  }
-}
 
 // ---------------------------------------------------------------------------------------
 // v9: persistent v7 with dynamic scheduling.  One CTA per SM; the TMA warp draws work
@@ -1474,8 +919,9 @@ __device__ __forceinline__ void tmem_ld32_wait(uint32_t (&r)[32]) {
                : "memory");
 }
 
-// 2^x as a degree-3 polynomial on the FMA pipe (2^f on [-1/2, 1/2], max rel. error 7.5e-5), used by
-// v5's dbg bit 1; on v10 a quarter of the exponentials this way measured 952 vs 1025 TFLOP/s at 16K
+// 2^x as a degree-3 polynomial on the FMA pipe (2^f on [-1/2, 1/2], max rel. error 7.5e-5).  Not
+// used: on v10 a quarter of the exponentials this way measured 952 vs 1025 TFLOP/s at 16K (the
+// softmax is not MUFU-bound, profiles/r01_prefill_v10_diagnostics.txt); kept for that record.
 __device__ __forceinline__ float ex2_poly(float x) {
   // clamp: for j <= -127 the exponent add below would underflow into the sign bit
   x = fmaxf(x, -125.f);
@@ -2049,314 +1495,11 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v10(const __grid
   }
 }
 
-// ---------------------------------------------------------------------------------------
-// v5 (experimental, SEAKV_PREFILL_V=5): 128-key tiles.  A 128x64x16 UMMA runs at 2/3 of
-// the tensor core's rate (measured: 48 clk vs 64 clk for N=128, scripts/umma_bench), so
-// S = Q.K^T uses N = 128 keys and P.V uses K = 128 keys.  TMEM: S_A | S_B | O_A | O_B
-// (4 x 128 columns), P(j) written over the first 64 columns of S(j) and read by the
-// TS-form MMA.  Without room for a second S buffer the softmax -> PV -> QK chain of a
-// tile is serial, and on B200 this measured slower than v3 (824 vs 867 TFLOP/s at 16K
-// context, profiles/r01_prefill_probe_v5.txt).  Optional (dbg bit 1): a quarter of the
-// exponentials as a degree-3 polynomial on the FMA pipe (2^f on [-1/2, 1/2], max rel.
-// error 7.5e-5) -- also slower here: the softmax is not exp2-throughput bound.
-// K and V have separate TMA rings (3 and 2 stages of 32 KiB).
-constexpr int kKT5 = 128;
-constexpr int kKStages5 = 3, kVStages5 = 2;
-constexpr int kSmemV5 = 2 * kTileBytes + (kKStages5 + kVStages5) * kTileBytes + 256;
-
-
-
-template <typename T>
-__global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v5(const __grid_constant__ DataParams p) {
-  extern __shared__ __align__(1024) char smem[];
-  if (smem_u32(smem) & 1023) __trap();
-  char* sQ[2] = {smem, smem + kTileBytes};
-  char* kbase = smem + 2 * kTileBytes;                 // [kKStages5] K tiles [128 keys x 128 d]
-  char* vbase = kbase + kKStages5 * kTileBytes;        // [kVStages5] V tiles
-  uint64_t* bars = reinterpret_cast<uint64_t*>(vbase + kVStages5 * kTileBytes);
-  uint64_t* k_full = bars;                              // [3] TMA expect_tx
-  uint64_t* k_empty = bars + 3;                         // [3] commit after QK_B
-  uint64_t* v_full = bars + 6;                          // [2]
-  uint64_t* v_empty = bars + 8;                         // [2] commit after PV_B
-  uint64_t* q_full = bars + 10;                         // count 32
-  uint64_t* s_full = bars + 11;                         // [tile] S(j) ready (=> PV(j-1) done)
-  uint64_t* p_full = bars + 13;                         // [tile] count 128
-  uint64_t* pv_done = bars + 15;                        // [tile]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
-
-  const int r = blockIdx.z, h = blockIdx.y;
-  const int grp = p.req_group[r];
-  const DataGroup& g = p.g[grp];
-  const int G = g.G;
-  const int q_len = p.n_new;
-  const int tileA = 2 * blockIdx.x;
-  if (!g.active || h >= g.Hkv || tileA * kRows >= q_len * G) return;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int handle = p.handles[r];
-  const int ctx = p.req_tokens[handle];
-  const int start = ctx - q_len;
-  const int tpt = kRows / G;
-  const int t0A = tileA * tpt;
-  const int n_keys = min(ctx, start + t0A + 2 * tpt);  // the last row of tile B
-  const int n_kt = (n_keys + kKT5 - 1) / kKT5;
-  const int rl = r - g.req_begin;
-
-  if (warp == kMmaWarp) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  if (tid == 0) {
-    for (int i = 0; i < 3; ++i) {
-      mbar_init_n(&k_full[i], 1);
-      mbar_init_n(&k_empty[i], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init_n(&v_full[i], 1);
-      mbar_init_n(&v_empty[i], 1);
-      mbar_init_n(&s_full[i], 1);
-      mbar_init_n(&p_full[i], 128);
-      mbar_init_n(&pv_done[i], 1);
-    }
-    mbar_init_n(q_full, kLoadThreads);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == kLoadWarp) {  // ----------------------------------------------- loader
-    const int c = lane & 15;
-    for (int i = 0; i < 128; ++i) {  // Q tiles A and B: 256 rows x 16 chunks
-      const int idx = (lane >> 4) + 2 * i;
-      const int x = idx >> 7, row = idx & 127;
-      const int tok = t0A + x * tpt + row / G, gg = row % G;
-      const bool ok = tok < q_len;
-      const char* src = reinterpret_cast<const char*>(g.q) +
-                        (((size_t)rl * q_len + (ok ? tok : 0)) * g.Hq + h * G + gg) * (kD * 2) + c * 16;
-      cp_async16(smem_u32(sQ[x]) + sw_off(row, c), src, ok);
-    }
-    cp_async_arrive(q_full);
-    if (lane == 0) {  // K then V of every 128-key tile: 8 native blocks x 2 d-halves of 2 KiB boxes
-      const int2* row_tab = p.req_table + (size_t)handle * p.cap;
-      const long long base_off = g.layer_off + (long long)h * g.head_stride;
-      const int n_blk = (n_keys + kTpb - 1) / kTpb;
-      for (int j = 0; j < n_kt; ++j) {
-        int2 e[8];
-        int nb = 0;
-#pragma unroll
-        for (int b = 0; b < 8; ++b) {
-          const int bi = j * 8 + b;
-          e[b] = bi < n_blk ? row_tab[bi] : make_int2(-1, 0);
-          nb += bi < n_blk;
-        }
-        const int ks = j % kKStages5, vs = j % kVStages5;
-        if (j >= kKStages5) mbar_wait(&k_empty[ks], ((j / kKStages5) - 1) & 1);
-        mbar_expect_tx_v3(&k_full[ks], nb * 2 * 2048);
-        const uint32_t sK = smem_u32(kbase + ks * kTileBytes), sV = smem_u32(vbase + vs * kTileBytes);
-#pragma unroll
-        for (int b = 0; b < 8; ++b) {
-          if (e[b].x < 0) continue;
-          const int row0 = (int)(((long long)e[b].x * p.merged_stride + (long long)e[b].y * g.native_stride +
-                                  base_off) >> 8);
-          tma_load_2d(sK + b * 2048, &p.kv_tmap, 0, row0, &k_full[ks]);
-          tma_load_2d(sK + kHalf + b * 2048, &p.kv_tmap, 64, row0, &k_full[ks]);
-        }
-        if (j >= kVStages5) mbar_wait(&v_empty[vs], ((j / kVStages5) - 1) & 1);
-        mbar_expect_tx_v3(&v_full[vs], nb * 2 * 2048);
-#pragma unroll
-        for (int b = 0; b < 8; ++b) {
-          if (e[b].x < 0) continue;
-          const int row0 = (int)(((long long)e[b].x * p.merged_stride + (long long)e[b].y * g.native_stride +
-                                  base_off) >> 8) + kTpb;
-          tma_load_2d(sV + b * 2048, &p.kv_tmap, 0, row0, &v_full[vs]);
-          tma_load_2d(sV + kHalf + b * 2048, &p.kv_tmap, 64, row0, &v_full[vs]);
-        }
-      }
-    }
-    cp_async_wait<0>();
-  } else if (warp == kMmaWarp) {  // -------------------------------------------- MMA issue
-    if (lane == 0) {
-      const uint32_t idesc_qk = make_idesc_n(p.dtype, 0, kKT5);
-      const uint32_t idesc_pv = make_idesc_n(p.dtype, 1, kD);
-      auto qk = [&](int x, int j) {  // S[x] = Q_x . K_j^T   (M=128, N=128 keys, K=128 d)
-        const uint32_t sK = smem_u32(kbase + (j % kKStages5) * kTileBytes);
-#pragma unroll
-        for (int k = 0; k < kD / 16; ++k) {
-          const uint32_t off = (k >> 2) * kHalf + (k & 3) * 32;
-          mma_f16(tmem + x * 128, make_desc(smem_u32(sQ[x]) + off, 16, 1024), make_desc(sK + off, 16, 1024),
-                  idesc_qk, k > 0);
-        }
-        mma_commit(&s_full[x]);
-      };
-      auto pv = [&](int x, int j) {  // O[x] += P_x(j) . V_j  (P in TMEM: 16 keys = 8 columns)
-        const uint32_t sV = smem_u32(vbase + (j % kVStages5) * kTileBytes);
-#pragma unroll
-        for (int k = 0; k < kKT5 / 16; ++k)
-          mma_f16_ts(tmem + 256 + x * 128, tmem + x * 128 + k * 8, make_desc(sV + k * 2048, kHalf, 1024), idesc_pv,
-                     (j > 0 || k > 0) ? 1u : 0u);
-        mma_commit(&pv_done[x]);
-      };
-      auto wait_k = [&](int j) {
-        mbar_wait(&k_full[j % kKStages5], (j / kKStages5) & 1);
-        tc_fence_after();
-      };
-      mbar_wait(q_full, 0);
-      fence_async_smem();
-      wait_k(0);
-      qk(0, 0);
-      qk(1, 0);
-      mma_commit(&k_empty[0]);
-      for (int j = 0; j < n_kt; ++j) {
-        mbar_wait(&v_full[j % kVStages5], (j / kVStages5) & 1);
-        mbar_wait(&p_full[0], j & 1);
-        tc_fence_after();
-        pv(0, j);
-        if (j + 1 < n_kt) {
-          wait_k(j + 1);
-          qk(0, j + 1);  // overwrites S_A/P_A(j) after PV_A(j) in issue order
-        }
-        mbar_wait(&p_full[1], j & 1);
-        tc_fence_after();
-        pv(1, j);
-        mma_commit(&v_empty[j % kVStages5]);
-        if (j + 1 < n_kt) {
-          qk(1, j + 1);
-          mma_commit(&k_empty[(j + 1) % kKStages5]);
-        }
-      }
-    }
-    __syncwarp();
-  } else {  // ------------------------------------------------------------- softmax warps
-    const int x = warp >> 2;  // 0 = tile A, 1 = tile B; both warpgroups address TMEM lanes 0-127
-    const int row = tid & 127;
-    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-    const uint32_t tS = tmem + x * 128 + lane_off, tO = tmem + 256 + x * 128 + lane_off;
-    const int t0 = t0A + x * tpt;
-    const int my_tok = t0 + row / G;
-    const bool row_ok = my_tok < q_len;
-    const int my_pos = start + my_tok;
-    const bool tail_rows = t0 + tpt > q_len;
-    const float c2 = p.scale_log2;
-    float m = -INFINITY, l = 0.f;
-    for (int j = 0; j < n_kt; ++j) {
-      mbar_wait(&s_full[x], j & 1);
-      tc_fence_after();
-      if (x == 0 && j == n_kt - 1 && (j + 1) * kKT5 > n_keys) {
-        // rows past the keys this CTA needs: stale smem or another owner's bytes (may be
-        // NaN) -> zero them before P.V (their P is 0 or ~2^-127)
-        const int vs = j % kVStages5;
-        mbar_wait(&v_full[vs], (j / kVStages5) & 1);
-        char* sV = vbase + vs * kTileBytes;
-        const int c = row & 15;
-        for (int key = row >> 4; key < kKT5; key += 8)
-          if (j * kKT5 + key >= n_keys) *reinterpret_cast<uint4*>(sV + sw_off(key, c)) = make_uint4(0, 0, 0, 0);
-      }
-      const bool masked = (j * kKT5 + kKT5 - 1 > start + t0) || tail_rows;
-      const int lim = row_ok ? my_pos - j * kKT5 : -1;  // keys k <= lim are visible
-      // pass 1: tile max
-      float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        float v[64];
-        tmem_ld64(tS + hh * 64, v);
-        if (masked) {
-#pragma unroll
-          for (int k = 0; k < 64; ++k)
-            if (hh * 64 + k > lim) v[k] = -INFINITY;
-        }
-#pragma unroll
-        for (int k = 0; k < 64; ++k) mx4[k & 3] = fmaxf(mx4[k & 3], v[k]);
-      }
-      const float mt = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * c2;
-      const bool need = mt > m + kRescale;
-      float alpha = 1.f;
-      if (need) {
-        alpha = ex2(m - mt);
-        l *= alpha;
-        m = mt;
-      }
-      // O correction: S(j) ready implies PV(j-1) retired (issue order), PV(j) waits for P(j)
-      if (j > 0 && __any_sync(0xffffffffu, need)) {
-#pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-          float o[32];
-          tmem_ld32(tO + cc * 32, o);
-#pragma unroll
-          for (int k = 0; k < 32; ++k) o[k] *= alpha;
-          tmem_st32(tO + cc * 32, o);
-        }
-      }
-      const float mu = (m == -INFINITY) ? 0.f : m;
-      // pass 2: P = 2^(s*c2 - m) (3/4 MUFU, 1/4 polynomial), written over S as packed pairs
-      float ls[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        float v[64];
-        tmem_ld64(tS + hh * 64, v);  // hh = 1 reads columns 64..127, above P of hh = 0 (0..31)
-        if (masked) {
-#pragma unroll
-          for (int k = 0; k < 64; ++k)
-            if (hh * 64 + k > lim) v[k] = -INFINITY;
-        }
-#pragma unroll
-        for (int cc = 0; cc < 2; ++cc) {
-          uint32_t pk[16];
-#pragma unroll
-          for (int k = 0; k < 32; k += 2) {
-            const float a0 = fmaf(v[cc * 32 + k], c2, -mu), a1 = fmaf(v[cc * 32 + k + 1], c2, -mu);
-            const float e0 = ex2(a0);
-            const float e1 = ((k & 2) && (p.dbg & 2)) ? ex2_poly(a1) : ex2(a1);
-            ls[(k >> 1) & 3] += e0 + e1;
-            pk[k >> 1] = pack2<T>(e0, e1);
-          }
-          tmem_st16u(tS + hh * 32 + cc * 16, pk);
-        }
-      }
-      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-      l += (ls[0] + ls[1]) + (ls[2] + ls[3]);
-      fence_async_smem();  // V-row zeroing (generic stores) -> tensor core
-      tc_fence_before();
-      mbar_arrive(&p_full[x]);
-    }
-    mbar_wait(&pv_done[x], (n_kt - 1) & 1);
-    tc_fence_after();
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-    char* dst = reinterpret_cast<char*>(g.out) +
-                (((size_t)rl * q_len + (row_ok ? my_tok : 0)) * g.Hq + h * G + row % G) * (kD * 2);
-#pragma unroll
-    for (int cc = 0; cc < 4; ++cc) {
-      float o[32];
-      tmem_ld32(tO + cc * 32, o);
-      if (row_ok) {
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {
-          uint4 v;
-          v.x = pack2<T>(o[8 * q4] * inv, o[8 * q4 + 1] * inv);
-          v.y = pack2<T>(o[8 * q4 + 2] * inv, o[8 * q4 + 3] * inv);
-          v.z = pack2<T>(o[8 * q4 + 4] * inv, o[8 * q4 + 5] * inv);
-          v.w = pack2<T>(o[8 * q4 + 6] * inv, o[8 * q4 + 7] * inv);
-          *reinterpret_cast<uint4*>(dst + cc * 64 + q4 * 16) = v;
-        }
-      }
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == kMmaWarp) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
-  }
-}
-
 template <typename T>
 void launch_prefill_t(const DataParams& p, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(prefill_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2);
-    cudaFuncSetAttribute(prefill_kernel_v3<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemV3);
-    cudaFuncSetAttribute(prefill_kernel_v5<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemV5);
-    cudaFuncSetAttribute(prefill_kernel_v7<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemV7);
     cudaFuncSetAttribute(prefill_kernel_v9<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemV9);
     cudaFuncSetAttribute(prefill_kernel_v10<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemV10);
     attr = true;
@@ -2368,14 +1511,11 @@ void launch_prefill_t(const DataParams& p, cudaStream_t s) {
   }
   static const int version = [] {
     const char* e = getenv("SEAKV_PREFILL_V");
-    return e ? atoi(e) : 10;  // v10 measured fastest (profiles/r01_prefill_probe_v10.txt); 3, 5, 7, 9 selectable
+    return e ? atoi(e) : 10;  // v10 measured fastest (profiles/r01_prefill_probe_v10_final.txt); 2, 9 selectable
   }();
   if (version == 2 || !p.has_tmap) {
     dim3 grid(tiles, heads, p.nreq);
     prefill_kernel<T><<<grid, kThreads, kSmem2, s>>>(p);
-  } else if (version == 3) {
-    dim3 grid((tiles + 1) / 2, heads, p.nreq);
-    prefill_kernel_v3<T><<<grid, kThreadsV3, kSmemV3, s>>>(p);
   } else if (version == 9) {
     const int npairs = (tiles + 1) / 2;
     int nsm = 148, dev = 0;
@@ -2406,12 +1546,9 @@ void launch_prefill_t(const DataParams& p, cudaStream_t s) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     cudaLaunchKernelEx(&cfg, prefill_kernel_v10<T>, p, npairs, heads);
-  } else if (version == 7) {
-    dim3 grid((tiles + 1) / 2, heads, p.nreq);
-    prefill_kernel_v7<T><<<grid, kThreadsV3, kSmemV7, s>>>(p);
   } else {
-    dim3 grid((tiles + 1) / 2, heads, p.nreq);
-    prefill_kernel_v5<T><<<grid, kThreadsV3, kSmemV5, s>>>(p);
+    std::fprintf(stderr, "SEAKV_PREFILL_V=%d: unknown prefill variant (2, 9, 10)\n", version);
+    std::abort();
   }
 }
 
