@@ -1242,7 +1242,7 @@ skv_status skv_prefill_attention(skv_pool* p, skv_batch* b, const skv_prefill_ar
     const char* e = getenv("SKV_TRACE");
     return e && e[0] == '1';
   }();
-  if (trace_on) {  // prefill_kernel_v3 built with -DSKV_PF_TRACE: 16 u64 per CTA (4 records)
+  if (trace_on) {  // prefill kernels built with -DSKV_PF_TRACE: 16 u64 per CTA (4 records)
     int tiles = 1, heads = 1;
     for (int g = 0; g < b->ngroups; ++g) {
       tiles = std::max(tiles, (a->q_len * dp.g[g].G + 127) / 128);

@@ -1,4 +1,4 @@
-"""Per-role wait profile of prefill_kernel_v3 (build: make SKV_EXTRA=-DSKV_PF_TRACE; run with SKV_TRACE=1).
+"""Per-role wait profile of the warp-specialised prefill kernels (build: make SKV_EXTRA=-DSKV_PF_TRACE; run with SKV_TRACE=1).
 
 usage: SKV_TRACE=1 python scripts/prefill_trace.py R CTX Q
 Prints the mean fraction of each CTA's cycles spent in each wait.
@@ -38,7 +38,7 @@ t = t[t[:, 13] > 0]
 tot = t[:, 13]
 names = ["load:kv_empty", "mma:q_full", "mma:kv_full", "mma:p_full_A", "mma:p_full_B",
          "smA:s_full", "smA:pv_corr", "smA:pv_last", "-", "smB:s_full", "smB:pv_corr", "smB:pv_last"]
-if os.environ.get("SEAKV_PREFILL_V") in ("10", "11"):  # CTA pairs: softmax halves c=0/1 of the same rows
+if os.environ.get("SEAKV_PREFILL_V", "10") == "10":  # CTA pairs: softmax halves c=0/1 of the same rows
     names = ["load:kv_empty", "mma:q_full", "mma:kv_full", "mma:p_full", "mma:issue",
              "sm0:s_full", "sm0:pv_corr", "sm0:pv_last", "sm0:max_xchg", "sm1:s_full", "sm1:pv_corr", "sm1:pv_last",
              "sm1:max_xchg", "-", "-", "mma:descs"]
