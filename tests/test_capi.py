@@ -41,6 +41,15 @@ def test_sass_uses_bulk_async_copies():
     assert "UBLKCP" in out
 
 
+def test_sass_prefill_uses_tcgen05_pair_mma_and_tma():
+    """The default prefill kernel issues 2-CTA tcgen05 MMAs (SASS UTCHMMA.2CTA) on operands
+    staged by TMA tensor loads (UTMALDG), with multicast commits to both CTAs."""
+    out = subprocess.run(["cuobjdump", "-sass", K.LIB_PATH], capture_output=True, text=True).stdout
+    assert "UTCHMMA.2CTA" in out
+    assert "UTMALDG.2D.2CTA" in out
+    assert "UTCBAR.2CTA.MULTICAST" in out
+
+
 def test_version():
     assert b"sm_100a" in K.lib().skv_version()
 
