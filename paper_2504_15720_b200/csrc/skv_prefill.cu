@@ -37,11 +37,9 @@ namespace {
 constexpr int kD = 128;
 constexpr int kTpb = 16;
 constexpr int kRows = 128;                  // M (query rows per CTA)
-constexpr int kKeys = 128;                  // N (keys per tile)
 constexpr int kTileBytes = kRows * kD * 2;  // 32 KiB per operand tile
 constexpr int kHalf = kRows * 128;          // bytes of one 64-element column half
 constexpr int kThreads = 128;
-constexpr int kSmem = 6 * kTileBytes + 1024 + 64;  // Q, K[2], V[2], P + alignment + barrier/tmem slot
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -83,17 +81,6 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint
   return d;
 }
 
-// kind::f16 instruction descriptor: fp32 accumulate, M=128, N=128.
-__device__ __forceinline__ uint32_t make_idesc(int bf16, int b_mn_major) {
-  uint32_t d = 0;
-  d |= 1u << 4;                   // D format f32
-  d |= (uint32_t)bf16 << 7;       // A format (0 f16, 1 bf16)
-  d |= (uint32_t)bf16 << 10;      // B format
-  d |= (uint32_t)b_mn_major << 16;  // B major (0 K, 1 MN); A is K-major
-  d |= (uint32_t)(kKeys >> 3) << 17;  // N >> 3
-  d |= (uint32_t)(kRows >> 4) << 24;  // M >> 4
-  return d;
-}
 
 __device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                         uint32_t accumulate) {
@@ -227,13 +214,6 @@ __device__ __forceinline__ void tmem_st32u(uint32_t taddr, const uint32_t (&v)[3
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
-__device__ __forceinline__ void tmem_st16u(uint32_t taddr, const uint32_t (&v)[16]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
-      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
-      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
-      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]));
-}
 
 __device__ __forceinline__ float ex2(float x) {
 #ifdef SKV_PF_NOMUFU  // diagnostic build only (wrong results): exponentials off the MUFU
@@ -509,7 +489,6 @@ constexpr int kSoftmaxWarps = 8;             // 4 per query tile, one thread per
 constexpr int kMmaWarp = kSoftmaxWarps;      // warp 8
 constexpr int kLoadWarp = kSoftmaxWarps + 1; // warp 9
 constexpr int kThreadsV3 = (kSoftmaxWarps + 2) * 32;
-constexpr int kLoadThreads = 32;
 
 __device__ __forceinline__ void mbar_init_n(uint64_t* b, uint32_t n) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(n));
@@ -526,9 +505,6 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* tmap, int 
 }
 __device__ __forceinline__ void mbar_expect_tx_v3(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void cp_async_arrive(uint64_t* b) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(b)) : "memory");
 }
 
 // Build with SKV_EXTRA=-DSKV_PF_TRACE to record, per CTA, clock64 cycles spent in each
@@ -919,19 +895,6 @@ __device__ __forceinline__ void tmem_ld32_wait(uint32_t (&r)[32]) {
                : "memory");
 }
 
-// 2^x as a degree-3 polynomial on the FMA pipe (2^f on [-1/2, 1/2], max rel. error 7.5e-5).  Not
-// used: on v10 a quarter of the exponentials this way measured 952 vs 1025 TFLOP/s at 16K (the
-// softmax is not MUFU-bound, profiles/r01_prefill_v10_diagnostics.txt); kept for that record.
-__device__ __forceinline__ float ex2_poly(float x) {
-  // clamp: for j <= -127 the exponent add below would underflow into the sign bit
-  x = fmaxf(x, -125.f);
-  const float t = x + 12582912.f;  // 1.5 * 2^23: round to nearest integer in the low bits
-  const float f = x - (t - 12582912.f);
-  float p = fmaf(0.05517166207399859f, f, 0.2426111584161752f);
-  p = fmaf(p, f, 0.6932609899481472f);
-  p = fmaf(p, f, 0.9999280714420054f);
-  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
-}
 
 constexpr int kStagesV10 = 6;
 constexpr int kKV10 = 2 * kKVHalf * 2;  // per CTA per stage: K half-tile 16 KiB + V half-tile 16 KiB
