@@ -27,7 +27,8 @@ __device__ __forceinline__ void mma_ts_lo(uint32_t d, uint32_t a, uint32_t blo, 
       "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], bd, %3, p;\n\t}" ::"r"(d),
       "r"(a), "r"(blo), "r"(idesc), "r"(acc), "n"(kDescHi));
 }
-__global__ void __launch_bounds__(128, 1) bench(int iters, int variant, long long* out) {
+template <int variant>
+__global__ void __launch_bounds__(128, 1) bench(int iters, long long* out) {
   extern __shared__ __align__(1024) char smem[];
   __shared__ uint32_t slot;
   __shared__ __align__(8) uint64_t bar;
@@ -61,16 +62,25 @@ __global__ void __launch_bounds__(128, 1) bench(int iters, int variant, long lon
       for (int kk = 0; kk < 8; ++kk) {
         const uint32_t off = st + (kk >> 2) * 8192 + (kk & 3) * 32;
         const uint32_t d = tmem + (kk & 1) * 128, a = tmem + 384 + kk * 8;
-        if (variant == 0) {
+        if constexpr (variant == 0) {
           asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                        "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d), "r"(a),
                        "l"(make_desc(sb + off, 16, 1024)), "r"(idesc), "r"(1));
-        } else if (variant == 1) {
+        } else if constexpr (variant == 1) {
           asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                        "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d), "r"(a),
                        "l"(db + (uint64_t)(off >> 4)), "r"(idesc), "r"(1));
-        } else {
+        } else if constexpr (variant == 2) {
           mma_ts_lo(d, a, dlo + (off >> 4), idesc, 1);
+        } else {
+          asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                       "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem),
+                       "r"(tmem + 384), "l"(db), "r"(idesc), "r"(1));
+        }
+      }
+      if (variant >= 3 && (i & 15) == 8) {  // after every 16 MMAs: a gap of busy work
+        const long long g0 = clock64();
+        while (clock64() - g0 < (long long)(variant - 3) * 200) {
         }
       }
     }
@@ -101,9 +111,19 @@ __global__ void __launch_bounds__(128, 1) bench(int iters, int variant, long lon
 int main() {
   long long* d;
   cudaMalloc(&d, 74 * sizeof(long long));
-  cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-  const char* names[3] = {"make_desc per MMA      ", "64-bit base + offset   ", "lo word + imm hi in asm"};
-  for (int v = 0; v < 3; ++v)
+  cudaFuncSetAttribute(bench<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  cudaFuncSetAttribute(bench<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  cudaFuncSetAttribute(bench<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  cudaFuncSetAttribute(bench<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  cudaFuncSetAttribute(bench<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  cudaFuncSetAttribute(bench<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  cudaFuncSetAttribute(bench<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  cudaFuncSetAttribute(bench<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  cudaFuncSetAttribute(bench<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  const char* names[9] = {"make_desc per MMA      ", "64-bit base + offset   ", "lo word + imm hi in asm",
+                          "fixed, gap 0/16 MMAs   ", "fixed, gap 200/16 MMAs ", "fixed, gap 400/16 MMAs ",
+                          "fixed, gap 600/16 MMAs ", "fixed, gap 800/16 MMAs ", "fixed, gap 1000/16 MMAs"};
+  for (int v = 0; v < 9; ++v)
     for (int rep = 0; rep < 2; ++rep) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(148);
@@ -117,7 +137,17 @@ int main() {
       cfg.attrs = at;
       cfg.numAttrs = 1;
       const int iters = 4096;
-      cudaLaunchKernelEx(&cfg, bench, iters, v, d);
+      switch (v) {
+        case 0: cudaLaunchKernelEx(&cfg, bench<0>, iters, d); break;
+        case 1: cudaLaunchKernelEx(&cfg, bench<1>, iters, d); break;
+        case 2: cudaLaunchKernelEx(&cfg, bench<2>, iters, d); break;
+        case 3: cudaLaunchKernelEx(&cfg, bench<3>, iters, d); break;
+        case 4: cudaLaunchKernelEx(&cfg, bench<4>, iters, d); break;
+        case 5: cudaLaunchKernelEx(&cfg, bench<5>, iters, d); break;
+        case 6: cudaLaunchKernelEx(&cfg, bench<6>, iters, d); break;
+        case 7: cudaLaunchKernelEx(&cfg, bench<7>, iters, d); break;
+        default: cudaLaunchKernelEx(&cfg, bench<8>, iters, d); break;
+      }
       if (cudaDeviceSynchronize() != cudaSuccess) { printf("err\n"); return 1; }
       long long h[74];
       cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
