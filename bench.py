@@ -152,7 +152,13 @@ def make_workload(P, args):
     nreq = args.requests or 256
     ctx = args.ctx or 2048
     ctxs = [[ctx] * nreq for _ in SERVICES]
-    return Workload("config2", SERVICES, ctxs, args.phys_layers, _blocks(P, SERVICES, ctxs, grow),
+    blocks = _blocks(P, SERVICES, ctxs, grow)
+    if args.phys_layers == 0:  # SURVEY §8d run (B): every layer stored, requests cut to fit one B200
+        return Workload("config2", SERVICES, ctxs, 0, blocks,
+                        f"config2-capacity-faithful: 4 services (llama-3-8b, mistral-7b, llama-2-13b, opt-6.7b) x "
+                        f"{nreq} decode requests, ctx {ctx}+, one unified all-layer pool of {blocks} merged blocks, "
+                        f"40 layer-index launches per step")
+    return Workload("config2", SERVICES, ctxs, args.phys_layers, blocks,
                     f"config2-layer-sliced: 4 services (llama-3-8b, mistral-7b, llama-2-13b, opt-6.7b) x {nreq} "
                     f"decode requests, ctx {ctx}+, one unified pool; {args.phys_layers} physical layers per native "
                     f"block (logical l -> l % {args.phys_layers}), 40 layer-index launches per step")
