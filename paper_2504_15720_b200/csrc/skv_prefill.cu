@@ -920,6 +920,11 @@ __device__ __forceinline__ void cluster_sync_all() {
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
+// TMEM-only handoffs (tcgen05.st -> fence::before_thread_sync -> arrive; the waiter issues
+// fence::after_thread_sync before its MMAs): no generic-memory ordering needed, so no MEMBAR
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_cluster_rel(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
@@ -1251,7 +1256,7 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v10(const __grid
         tmem_st32u(tQ, qv);
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(q_full_l);
+        if (lane == 0) mbar_arrive_cluster_relaxed(q_full_l);
       }
       float m = -INFINITY, l = 0.f;
       const uint32_t j0 = jt;
@@ -1398,7 +1403,10 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v10(const __grid
         if (last_partial) fence_async_smem();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(p_full_l + 8 * (gj & 1));
+        if (lane == 0) {
+          if (last_partial) mbar_arrive_cluster(p_full_l + 8 * (gj & 1));  // orders the V-row zeroing
+          else mbar_arrive_cluster_relaxed(p_full_l + 8 * (gj & 1));
+        }
       }
       const uint32_t gl = j0 + e.n_kt - 1;
       xl[c * 128 + row] = l;
