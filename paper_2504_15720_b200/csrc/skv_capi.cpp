@@ -359,6 +359,8 @@ skv_status queue_free(skv_pool* p, const skv::FreeOp& op) {
 }
 
 // try_allocate (kv_cache.hpp:104-123) on the host mirror; queues the claims.
+skv_status grow_handle_impl(skv_pool* p, int h, uint64_t id, int m, long long tokens);
+
 skv_status try_allocate_impl(skv_pool* p, uint64_t id, int m, long long tokens) {
   if (tokens < 0) return fail(p, SKV_ERR_VALIDATION, "allocate: negative tokens_needed");
   if (m < 0 || m >= p->M) return fail(p, SKV_ERR_ARG, "allocate: model index out of range");
@@ -379,6 +381,12 @@ skv_status try_allocate_impl(skv_pool* p, uint64_t id, int m, long long tokens) 
   } else {
     h = it->second;
   }
+  return grow_handle_impl(p, h, id, m, tokens);
+}
+
+// try_allocate for a registered request whose handle is known (the batch path skips the
+// id -> handle lookup)
+skv_status grow_handle_impl(skv_pool* p, int h, uint64_t id, int m, long long tokens) {
   ReqHost& r = p->req[h];
   if (r.nslots == 0) r.model = m;
   if (r.model != m) return fail(p, SKV_ERR_LOGIC, "allocate: request changed model");
@@ -959,8 +967,11 @@ skv_status skv_batch_grow(skv_pool* p, skv_batch* b, int64_t delta, int32_t* n_g
   for (int g = 0; g < b->ngroups; ++g) {
     for (int i = 0; i < b->gsize[g]; ++i) {
       const int r = b->gbegin[g] + i;
-      const ReqHost& rh = p->req[b->handles[r]];
-      st = try_allocate_impl(p, b->ids[r], b->gmodel[g], rh.tokens + delta);
+      const int h = b->handles[r];
+      const ReqHost& rh = p->req[h];
+      if (!rh.live || rh.id != b->ids[r]) return fail(p, SKV_ERR_LOGIC, "batch grow: request no longer registered");
+      if (delta < 0) return fail(p, SKV_ERR_VALIDATION, "allocate: negative tokens_needed");
+      st = grow_handle_impl(p, h, b->ids[r], b->gmodel[g], rh.tokens + delta);
       if (st == SKV_OK) granted++;
       else if (st != SKV_CACHE_FULL) return st;
     }
