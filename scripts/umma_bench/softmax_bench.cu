@@ -99,6 +99,13 @@ __global__ void __launch_bounds__(288, 1) bench(int iters, int mode, int nwarps,
         float mx = s[0];
 #pragma unroll
         for (int k = 1; k < COLS; ++k) mx = fmaxf(mx, s[k]);
+        if (mode >= 3) {  // v10-style row-max exchange between warps w and w+4 (same TMEM lanes)
+          __shared__ float xm[2][2][128];
+          const int row = (warp & 3) * 32 + (tid & 31), c = (warp >> 2) & 1;
+          xm[it & 1][c][row] = mx;
+          asm volatile("bar.sync %0, %1;" ::"r"(1 + (warp & 3)), "r"(64) : "memory");
+          mx = fmaxf(xm[it & 1][0][row], xm[it & 1][1][row]);
+        }
         m = fmaxf(m, mx);
       }
       if (mode >= 2) {
@@ -139,9 +146,9 @@ int main() {
   cudaMalloc(&sink, 148 * 256 * sizeof(float));
   const int iters = 2000;
   for (int mma = 1; mma < 2; ++mma)
-  for (int cols : {128})
-    for (int mode = 0; mode < 3; ++mode)
-      for (int nw : {0, 4, 8}) {
+  for (int cols : {64})
+    for (int mode = 2; mode < 4; ++mode)
+      for (int nw : {8}) {
         if (cols == 64) bench<64><<<148, 288>>>(iters, mode, nw, d, sink, mma);
         else bench<128><<<148, 288>>>(iters, mode, nw, d, sink, mma);
         cudaError_t err = cudaDeviceSynchronize();
@@ -154,7 +161,7 @@ int main() {
         double cyc = 0;
         for (int i = 0; i < 148; ++i) cyc += h[i];
         cyc /= 148;
-        const char* mn[3] = {"ld only", "ld+max", "ld+max+exp+st"};
+        const char* mn[4] = {"ld only", "ld+max", "ld+max+exp+st", "ld+max+xchg+exp+st"};
         printf("%s cols %d, %d warps, %s: %.0f clk/iter (TMEM read %.1f B/clk/SM)\n", mma ? "with MMA" : "no MMA  ", cols, nw, mn[mode], cyc / iters,
                (double)nw * 32 * cols * 4 * iters / cyc);
       }
