@@ -10,6 +10,8 @@
   allocator, K/V contents from the SplitMix64 synthetic generator (the formula of
   skv_synth_fill, recomputed here in numpy), fp16 queries, and decode outputs from
   an independent float64 numpy implementation of softmax(q·Kᵀ/√d)·V.
+* prefill_golden.npz — causal chunked prefill (the last 32 tokens of every request
+  with at least 32) on the same pool and tables, float64 numpy.
 
     python tests/golden/make_golden.py
 """
@@ -128,10 +130,60 @@ def make_attn():
     np.savez_compressed(os.path.join(HERE, "attn_golden.npz"), **res)
 
 
+def make_prefill():
+    """prefill_golden.npz: causal chunked-prefill attention (the last Q_LEN tokens of each
+    request attend to every key at or before their position) on the attn_golden pool and
+    tables, float64 numpy."""
+    a = np.load(os.path.join(HERE, "attn_golden.npz"))
+    shapes = [tuple(int(x) for x in r) for r in a["shapes"]]
+    seed, pool, layer = int(a["seed"]), int(a["pool"]), int(a["layer"])
+    models = [(L, H, 128, 2) for L, H, _ in shapes]
+    merged = int(O.plan_merged_shape(models))
+    stride = (merged + 255) // 256 * 256
+    img = synth_fp16(seed, pool * stride // 2).view(np.uint8)
+    q_len = 32
+    rng = np.random.default_rng(9)
+    res = {"q_len": np.int64(q_len)}
+    for m, (L, H, Hq) in enumerate(shapes):
+        layer_stride = H * 2 * 16 * 128 * 2
+        native = L * layer_stride
+        G = Hq // H
+        ids = [int(i) for i in a[f"m{m}_ids"]]
+        ctxs = [int(c) for c in a[f"m{m}_ctx"]]
+        keep = [k for k, c in enumerate(ctxs) if c >= q_len]
+        tabs = a[f"m{m}_tables"][keep]
+        q = (rng.standard_normal((len(keep), q_len, Hq, 128)) * 0.7).astype(np.float16)
+        out = np.zeros((len(keep), q_len, Hq, 128), np.float64)
+        for kk, k in enumerate(keep):
+            n = ctxs[k]
+            K = np.zeros((H, n, 128))
+            V = np.zeros((H, n, 128))
+            for t in range(n):
+                b, sl = tabs[kk][t // 16]
+                base = int(b) * stride + int(sl) * native + layer * layer_stride + (t % 16) * 256
+                for h in range(H):
+                    ko = base + h * 2 * 16 * 256
+                    K[h, t] = img[ko:ko + 256].view(np.float16).astype(np.float64)
+                    V[h, t] = img[ko + 16 * 256:ko + 16 * 256 + 256].view(np.float16).astype(np.float64)
+            for i in range(q_len):
+                pos = n - q_len + i
+                for hq in range(Hq):
+                    s_ = K[hq // G, :pos + 1] @ q[kk, i, hq].astype(np.float64) / np.sqrt(128.0)
+                    pr = np.exp(s_ - s_.max())
+                    out[kk, i, hq] = (pr / pr.sum()) @ V[hq // G, :pos + 1]
+        res[f"m{m}_ids"] = np.array([ids[k] for k in keep], np.uint64)
+        res[f"m{m}_ctx"] = np.array([ctxs[k] for k in keep], np.int64)
+        res[f"m{m}_tables"] = tabs
+        res[f"m{m}_q"] = q.view(np.uint16)
+        res[f"m{m}_out"] = out.astype(np.float32)
+    np.savez_compressed(os.path.join(HERE, "prefill_golden.npz"), **res)
+
+
 if __name__ == "__main__":
     if not O.ref_available():
         O.build()
     make_alloc()
     make_attn()
-    for f in ("alloc_golden.npz", "attn_golden.npz"):
+    make_prefill()
+    for f in ("alloc_golden.npz", "attn_golden.npz", "prefill_golden.npz"):
         print(f, os.path.getsize(os.path.join(HERE, f)), "bytes")
