@@ -94,3 +94,22 @@ def test_prefill_gqa8_llama70b_ratio():
 
 def test_prefill_long_prefix_many_tiles():
     run_prefill_check([(2, 2, 2)], [[4100]], q_len=300, layer=0)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3, 4, 5, 6])
+def test_prefill_randomised_services(seed):
+    """Randomised mixes: 1-3 services with random layer counts, KV heads and GQA ratios
+    (1, 2, 4, 8), ragged contexts, a random chunk length (1-300), fp16 or bf16."""
+    rng = np.random.default_rng(100 + seed)
+    n_svc = int(rng.integers(1, 4))
+    q_len = int(rng.choice([1, 7, 64, 100, 129, 256, 300]))
+    shapes, ctxs = [], []
+    for _ in range(n_svc):
+        L = int(rng.integers(1, 4))
+        H = int(rng.choice([1, 2, 4]))
+        G = int(rng.choice([1, 2, 4, 8]))
+        shapes.append((L, H, H * G))
+        ctxs.append([int(q_len + rng.integers(0, 900)) for _ in range(int(rng.integers(1, 4)))])
+    layer = int(rng.integers(0, min(L for L, _, _ in shapes)))
+    dtype = P.BF16 if seed % 3 == 0 else P.FP16
+    run_prefill_check(shapes, ctxs, q_len=q_len, layer=layer, dtype=dtype, seed=seed)
