@@ -315,3 +315,23 @@ def test_back_to_back_fused_launches_match_serialised(split):
             for layer, (a_l, b_l) in enumerate(zip(a_step, b_step)):
                 # groups whose model has <= layer layers are skipped (output untouched)
                 assert all(torch.equal(x, y) for x, y, (L, _, _) in zip(a_l, b_l, shapes) if layer < L), mode
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3, 4, 5, 6, 7, 8])
+def test_decode_randomised_services(seed):
+    """Randomised mixes: 1-4 services with random layer counts, KV heads and GQA ratios
+    (1, 2, 4, 8), 1-40 requests each with ragged contexts (1-3000 tokens, some split-KV),
+    fp16 or bf16, sliced or faithful pool."""
+    rng = np.random.default_rng(200 + seed)
+    shapes, ctxs = [], []
+    for _ in range(int(rng.integers(1, 5))):
+        L = int(rng.integers(1, 5))
+        H = int(rng.choice([1, 2, 4, 8]))
+        G = int(rng.choice([1, 2, 4, 8]))
+        shapes.append((L, H, H * G))
+        ctxs.append([int(rng.integers(1, 3000)) for _ in range(int(rng.integers(1, 41)))])
+    layer = int(rng.integers(0, max(L for L, _, _ in shapes)))
+    dtype = P.BF16 if seed % 4 == 0 else P.FP16
+    phys = 2 if seed % 3 == 0 else 0
+    run_decode_check(shapes, ctxs, layer=layer, dtype=dtype, phys_layers=phys, seed=seed,
+                     split=int(rng.choice([0, 0, 64])))
