@@ -203,8 +203,9 @@ class ChurnEngine:
             r = Req(self.next_id, a.svc, p.model_idx, a.in_len, a.out_len)
             self.next_id += 1
             gen = 1 + int(rng.next_double() * max(0, a.out_len - 1))
-            need = cache.native_blocks_for(r.in_len + gen) / max(1, cache.sub_slots_per_merged(r.model))
-            if cache.allocated_blocks() + need > target or not self._grow(r, r.in_len + gen):
+            # gen tokens generated, gen - 1 of them already fed back (their K/V cached)
+            need = cache.native_blocks_for(r.in_len + gen - 1) / max(1, cache.sub_slots_per_merged(r.model))
+            if cache.allocated_blocks() + need > target or not self._grow(r, r.in_len + gen - 1):
                 self.waiting.append(r)
                 continue
             r.phase, r.done, r.generated = "decode", r.in_len, gen
@@ -231,11 +232,12 @@ class ChurnEngine:
             self.running[r.rid] = r
             prefill.append(r)
             st["admitted"] += 1
-        # decode growth (+1 token); CacheFull -> preempt (free + re-queue for re-prefill)
+        # decode growth: the last generated token is fed back, so the cache holds prompt +
+        # generated tokens (+1 per step); CacheFull -> preempt (free + re-queue for re-prefill)
         decode = [r for r in self.running.values() if r.phase == "decode"][: self.max_decode]
         dec_ok = []
         for r in decode:
-            if self._grow(r, r.in_len + r.generated + 1):
+            if self._grow(r, r.in_len + r.generated):
                 dec_ok.append(r)
             else:
                 st["cache_full"] += 1
