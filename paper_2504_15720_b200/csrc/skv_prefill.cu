@@ -1298,6 +1298,8 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v10(const __grid
           // the path between the tile barrier and the MUFU work.
           uint32_t ra[32], rb[32];
           float mxa = -INFINITY, mxb = -INFINITY;
+          const float2 c2v = make_float2(c2, c2), nmv = make_float2(-m, -m);  // packed (FFMA2 / FADD2)
+          float2 ls2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
           tmem_ld32_issue(tS + 64 * c, ra);
           tmem_ld32_wait(ra);
           tmem_ld32_issue(tS + 64 * c + 32, rb);
@@ -1306,8 +1308,9 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v10(const __grid
             const float x0 = __uint_as_float(ra[kk]), x1 = __uint_as_float(ra[kk + 1]);
             mxa = fmaxf(mxa, x0);
             mxb = fmaxf(mxb, x1);
-            const float v0 = ex2(fmaf(x0, c2, -m)), v1 = ex2(fmaf(x1, c2, -m));
-            ls[(kk >> 1) & 3] += v0 + v1;
+            const float2 a = __ffma2_rn(make_float2(x0, x1), c2v, nmv);
+            const float v0 = ex2(a.x), v1 = ex2(a.y);
+            ls2[(kk >> 1) & 1] = __fadd2_rn(ls2[(kk >> 1) & 1], make_float2(v0, v1));
             pk[kk >> 1] = pack2<T>(v0, v1);
           }
           tmem_ld32_wait(rb);
@@ -1316,10 +1319,15 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v10(const __grid
             const float x0 = __uint_as_float(rb[kk]), x1 = __uint_as_float(rb[kk + 1]);
             mxa = fmaxf(mxa, x0);
             mxb = fmaxf(mxb, x1);
-            const float v0 = ex2(fmaf(x0, c2, -m)), v1 = ex2(fmaf(x1, c2, -m));
-            ls[(kk >> 1) & 3] += v0 + v1;
+            const float2 a = __ffma2_rn(make_float2(x0, x1), c2v, nmv);
+            const float v0 = ex2(a.x), v1 = ex2(a.y);
+            ls2[(kk >> 1) & 1] = __fadd2_rn(ls2[(kk >> 1) & 1], make_float2(v0, v1));
             pk[16 + (kk >> 1)] = pack2<T>(v0, v1);
           }
+          ls[0] = ls2[0].x;
+          ls[1] = ls2[0].y;
+          ls[2] = ls2[1].x;
+          ls[3] = ls2[1].y;
           xmb[c * 128 + row] = fmaxf(mxa, mxb);
           PF_T(3, named_bar(nbar, 64));
           const float mt = fmaxf(xmb[row], xmb[128 + row]) * c2;
