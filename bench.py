@@ -779,6 +779,124 @@ def run_config5(args):
         dist.destroy_process_group()
 
 
+def run_prefill(args):
+    """Chunked-prefill attention on tcgen05, one line in the bench format:
+    the four config-2 services, R requests each, the last C tokens of a CTX-token context
+    attending causally (layer 0), default R=4, CTX=16384, C=2048.  value = useful causal
+    TFLOP/s, roofline against the measured dense bf16 peak; e2e copies q from pinned host
+    memory and the output back every step."""
+    import numpy as np
+    import torch
+
+    import paper_2504_15720_b200 as P
+
+    torch.cuda.set_device(0)
+    R = args.requests or 4
+    ctx = args.ctx or 16384
+    C = args.chunk
+    models = [P.ModelSpec(n, L, H, 128, 2, Hq) for n, L, H, Hq in SERVICES]
+    cache = P.UnifiedKvCache(models, 16, 1, 4 * R * (ctx // 16 + 2) + 64, phys_layers=2, allocate_storage=True)
+    groups, rid = [], 1
+    for m in range(len(SERVICES)):
+        ids = []
+        for _ in range(R):
+            assert cache.try_allocate(rid, m, ctx)
+            ids.append(rid)
+            rid += 1
+        groups.append((m, ids))
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    cache.set_stream(stream)
+    cache.synth_fill(1, 1.0, stream)
+    b = cache.batch(groups)
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    qs = [torch.randn((R, C, Hq, 128), generator=gen, device="cuda").half() for _, _, _, Hq in SERVICES]
+    outs = [torch.empty_like(x) for x in qs]
+    p0 = ctx - C
+    flops = sum(4.0 * 128 * Hq * R * (C * p0 + C * (C + 1) / 2) for _, _, _, Hq in SERVICES)
+    launches0 = cache.kernel_launches()
+    for _ in range(args.warmup):
+        b.prefill(qs, outs, 0, C, stream=stream)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(0) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            b.prefill(qs, outs, 0, C, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    tflops = flops / (ms * 1e-3) / 1e12
+    launches = cache.kernel_launches() - launches0 - args.warmup
+    # e2e: q from pinned host memory in, output back, every step
+    hq = [x.cpu().pin_memory() for x in qs]
+    ho = [torch.empty(x.shape, dtype=x.dtype).pin_memory() for x in outs]
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        for d, h in zip(qs, hq):
+            d.copy_(h, non_blocking=True)
+        b.prefill(qs, outs, 0, C, stream=stream)
+        for h, d in zip(ho, outs):
+            h.copy_(d, non_blocking=True)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = t0.elapsed_time(t1) / args.steps
+    io_bytes = sum(x.numel() * 2 for x in qs)
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peak, peak_kind = float(json.load(f)["bf16_tflops"]), "measured (burst, cuBLAS bf16)"
+    except Exception:
+        peak, peak_kind = 2250.0, "fallback (nominal dense bf16)"
+    # CPU baseline: the fp32 oracle on a bounded sample (first request of each service, 32 q tokens)
+    cpu = None
+    if not args.no_cpu_baseline:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle_py as O
+        cores = os.cpu_count() or 1
+        img = cache.read_blocks(np.arange(cache.pool_size(), dtype=np.int32))
+        qn_tok = 32
+        done, cflops, t_start = 0, 0.0, time.perf_counter()
+        while time.perf_counter() - t_start < args.cpu_seconds / 2 or done == 0:
+            for (m, ids), q in zip(groups, qs):
+                Lh = cache.layout(m)
+                lay = O.layout(Lh.merged_stride, Lh.native_stride, Lh.layer_stride, Lh.head_stride, Lh.kv_stride,
+                               16, 128, Lh.kv_heads, Lh.q_heads, Lh.phys_layers, 0)
+                tab = np.array([cache.block_table(ids[0])], np.int32)
+                qh = q[0, C - qn_tok:].contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+                qh = qh.reshape(qn_tok, -1, 128)
+                O.prefill_attention(lay, img, 0, tab, np.array([ctx - qn_tok], np.int64),
+                                    np.array([qn_tok], np.int64), qh, 1.0 / np.sqrt(128.0), nthreads=cores)
+                Hq = SERVICES[m][3]
+                cflops += 4.0 * 128 * Hq * (qn_tok * (ctx - qn_tok) + qn_tok * (qn_tok + 1) / 2)
+            done += 1
+        dt = time.perf_counter() - t_start
+        cpu = {"value": round(cflops / dt / 1e12, 6), "unit": "TFLOP/s", "cores": cores, "kind": "port",
+               "sample": f"fp32 oracle causal prefill of the last {qn_tok} tokens of one request per service at "
+                         f"ctx {ctx}, {done} reps in {dt:.1f} s (oracle/attn_oracle.c; the reference has no attention)"}
+    res = {
+        "metric": "chunked-prefill attention TFLOP/s (unified pool, tcgen05)", "value": round(tflops, 1),
+        "unit": "TFLOP/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp16",
+        "data": "synthetic (SplitMix64 K/V pool, randn q)",
+        "config": {"workload": f"prefill: 4 services (config-2 shapes) x {R} requests, last {C} tokens of a "
+                               f"{ctx}-token context, causal, layer 0; useful (causal) flops only",
+                   "l2": "K/V per step larger than L2; no flush"},
+        "e2e": {"value": round(flops / (e2e_ms * 1e-3) / 1e12, 1), "unit": "TFLOP/s",
+                "h2d_bytes_per_step": int(io_bytes), "d2h_bytes_per_step": int(io_bytes),
+                "ms_per_step": round(e2e_ms, 4)},
+        "roofline": {"bound": "tensor", "kernel": "skv prefill_kernel_v10 (cta_group::2 tcgen05.mma)",
+                     "achieved": round(tflops, 1), "peak": peak, "peak_kind": peak_kind, "unit": "TFLOP/s",
+                     "frac": round(tflops / peak, 4), "traffic": None,
+                     "ncu": "profiles/r01_ncu_prefill_v10_final.txt (tensor pipe active % of cycles)"},
+        "gpu_launches": int(launches), "clocks": clk.summary(),
+    }
+    if cpu:
+        res["cpu_baseline"] = cpu
+    print(json.dumps(res), flush=True)
+
+
 def run_reference(args):
     """Reference arm: the reference's own CPU path for this workload on the host cores —
     the reference has no attention, so the fp32 oracle port stands in for decode and the
@@ -881,7 +999,9 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="config2", choices=["config1", "config2", "config3", "config4", "config5"])
+    ap.add_argument("--workload", default="config2",
+                    choices=["config1", "config2", "config3", "config4", "config5", "prefill"])
+    ap.add_argument("--chunk", type=int, default=2048, help="prefill workload: chunk length")
     ap.add_argument("--rate", type=float, default=20.0, help="config3 arrival rate (requests/s)")
     ap.add_argument("--pool-gb", dest="pool_gb", type=float, default=100.0, help="config3 pool size")
     ap.add_argument("--requests", type=int, default=0, help="decode requests per service (0 = workload default)")
@@ -900,6 +1020,8 @@ def main():
         run_churn(args)
     elif args.workload == "config5":
         run_config5(args)
+    elif args.workload == "prefill":
+        run_prefill(args)
     else:
         run_gpu(args)
 
