@@ -1,0 +1,33 @@
+"""bench.py workloads at small sizes: each prints one JSON line with the contract's keys
+(guards the benchmark paths themselves; the numbers are not checked)."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _run(*args):
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "2", "--warmup", "1",
+                          "--no-cpu-baseline", *args], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    return json.loads(lines[0])
+
+
+def test_bench_decode_small():
+    d = _run("--workload", "config2", "--requests", "8", "--ctx", "512")
+    for key in ("metric", "value", "unit", "e2e", "roofline", "gpu_launches", "clocks", "config"):
+        assert key in d, key
+    assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
+    assert d["roofline"]["bound"] == "hbm"
+
+
+def test_bench_prefill_small():
+    d = _run("--workload", "prefill", "--requests", "1", "--ctx", "1024", "--chunk", "256")
+    assert d["value"] > 0 and d["roofline"]["bound"] == "tensor" and d["gpu_launches"] == 2
