@@ -108,6 +108,18 @@ __global__ void __launch_bounds__(288, 1) bench(int iters, int mode, int nwarps,
         }
         m = fmaxf(m, mx);
       }
+      if (mode >= 4) {  // v10 per-tile protocol: fences, syncwarp, mbarrier arrive + wait (a completed phase)
+        if (mode != 5) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        __shared__ __align__(8) uint64_t pb[8];
+        const uint32_t ba = smem_u32(&pb[warp]);
+        if (it == 0 && (tid & 31) == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(ba));
+        __syncwarp();
+        if (mode != 6 && (tid & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(ba) : "memory");
+        uint32_t ok = mode == 6;
+        while (!ok)
+          asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                       : "=r"(ok) : "r"(ba), "r"((uint32_t)(it & 1)) : "memory");
+      }
       if (mode >= 2) {
 #pragma unroll
         for (int c = 0; c < COLS; c += 32) {
@@ -122,6 +134,10 @@ __global__ void __launch_bounds__(288, 1) bench(int iters, int mode, int nwarps,
           st16(tS + c / 2, pk);
         }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        if (mode >= 4) {
+          if (mode != 5) asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+        }
       } else {
 #pragma unroll
         for (int k = 0; k < COLS; ++k) acc += s[k];
@@ -147,7 +163,7 @@ int main() {
   const int iters = 2000;
   for (int mma = 1; mma < 2; ++mma)
   for (int cols : {64})
-    for (int mode = 2; mode < 4; ++mode)
+    for (int mode = 3; mode < 7; ++mode)
       for (int nw : {8}) {
         if (cols == 64) bench<64><<<148, 288>>>(iters, mode, nw, d, sink, mma);
         else bench<128><<<148, 288>>>(iters, mode, nw, d, sink, mma);
@@ -161,7 +177,7 @@ int main() {
         double cyc = 0;
         for (int i = 0; i < 148; ++i) cyc += h[i];
         cyc /= 148;
-        const char* mn[4] = {"ld only", "ld+max", "ld+max+exp+st", "ld+max+xchg+exp+st"};
+        const char* mn[7] = {"ld only", "ld+max", "ld+max+exp+st", "ld+max+xchg+exp+st", "+fences+mbarrier round trip", "+mbarrier only", "+fences only"};
         printf("%s cols %d, %d warps, %s: %.0f clk/iter (TMEM read %.1f B/clk/SM)\n", mma ? "with MMA" : "no MMA  ", cols, nw, mn[mode], cyc / iters,
                (double)nw * 32 * cols * 4 * iters / cyc);
       }
