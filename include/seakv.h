@@ -57,8 +57,12 @@ typedef struct {
   int32_t phys_layers;            /* 0: every layer stored (faithful merged-block layout).
                                      k>0: layer-sliced pool, k physical layers per native
                                      block, logical layer l -> l % k */
-  int32_t max_requests;           /* capacity of the device request table */
-  int32_t max_blocks_per_request; /* block-table row capacity (native blocks) */
+  int32_t max_requests;           /* initial capacity of the device request table (grows on
+                                     demand: the reference has no limit, kv_cache.hpp:104-106) */
+  int32_t max_blocks_per_request; /* initial block-table row capacity in native blocks (0: min(
+                                     pool_blocks * max sub-slots, 4096)); grows on demand.  A
+                                     growth re-allocates the device table: CUDA graphs captured
+                                     before it must be re-captured.  Fixed for the split scheme. */
   int32_t allocate_storage;       /* 1: allocate the KV bytes in HBM; 0: allocator only */
 } skv_pool_opts;
 

@@ -155,6 +155,9 @@ class UnifiedKvCache {
     for (const auto& m : models_) d.push_back(seakv_detail::to_desc(m));
     skv_pool_opts opts;
     skv_default_opts(&opts);
+    // max_requests / max_blocks_per_request are only initial capacities: the device request
+    // table grows on demand, so like the reference there is no limit on live requests or on a
+    // request's length other than the pool itself (kv_cache.hpp:104-123).
     opts.device = seakv_detail::default_device();
     skv_pool* p = nullptr;
     seakv_detail::check(skv_pool_create(d.data(), static_cast<int32_t>(d.size()), tokens_per_block, tp_size,

@@ -728,6 +728,18 @@ __global__ void __launch_bounds__(1024) plan_kernel(DataParams p) {
     __syncthreads();
   }
   const int N1 = carry[1], N2 = carry[2];
+  // Capacity guard: a CUDA graph replays this plan with the token counts of the replay, which
+  // may need more pieces than the host sized the buffers for at capture time.  Never write
+  // past them: flag the pool (skv_synchronize reports it) and run an empty launch instead.
+  if ((long long)N1 + N2 + carry[3] > p.items_cap || carry[4] > p.slots_cap) {
+    if (tid == 0) {
+      *p.n_items = 0;
+      p.counter[0] = 0;
+      p.counter[1] = 0;
+      if (p.status) atomicExch(p.status, 3);
+    }
+    return;
+  }
   // pass B: one warp per request, lanes over its kv heads
   for (int r = wid; r < n; r += 32) {
     const int grp = p.req_group[r];
@@ -812,12 +824,11 @@ __global__ void synth_kernel(uint4* pool, size_t n16, unsigned long long seed, f
 }
 
 bool pdl_enabled() {
-  static int on = -1;
-  if (on < 0) {
+  static const bool on = [] {  // environment read once (thread-safe static init)
     const char* e = getenv("SKV_NO_PDL");
-    on = (e && e[0] == '1') ? 0 : 1;
-  }
-  return on == 1;
+    return !(e && e[0] == '1');
+  }();
+  return on;
 }
 
 // Launch with the programmatic-stream-serialization attribute (see pdl_wait).
@@ -837,29 +848,29 @@ void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cu
   cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
-int g_num_sms = 0;
-int num_sms() {
-  if (!g_num_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
-  }
-  return g_num_sms;
-}
-
 template <typename T, int MAXG>
 void launch_decode_t(const DataParams& p, int grid, cudaStream_t s) {
   const int smem = kWarps * kStages * kTile + kWarps * kStages * 8 + kWarps * kRing * 4;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(decode_kernel<T, MAXG>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  ensure_smem_attr(decode_kernel<T, MAXG>, smem, attr);
   launch_pdl(decode_kernel<T, MAXG>, dim3(grid), dim3(kWarps * 32), smem, s, p);
 }
 
 }  // namespace
+
+int num_sms() {
+  static std::atomic<int> cached[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::atomic<int>& c = cached[dev & 63];
+  int n = c.load(std::memory_order_relaxed);
+  if (n <= 0) {
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+    c.store(n, std::memory_order_relaxed);
+  }
+  return n;
+}
 
 int decode_ctas_per_sm() { return 1; }
 int decode_warps_per_cta() { return kWarps; }

@@ -358,6 +358,53 @@ skv_status queue_free(skv_pool* p, const skv::FreeOp& op) {
   return SKV_OK;
 }
 
+// Grows the device request table on demand.  The reference has no limit on live requests
+// or on a request's length beyond the pool itself (kv_cache.hpp:104-123, simulation.hpp:248),
+// so opts.max_requests / max_blocks_per_request are initial capacities: the handle count and
+// the per-request row capacity double until `rows` handles / `cap` native blocks fit.  The
+// copy is stream-ordered after all work already on the pool stream (queued claims are
+// launched later against the new layout); CUDA graphs captured before a growth still point at
+// the old table and must be re-captured.
+skv_status grow_tables(skv_pool* p, long long rows, long long cap) {
+  if (rows <= p->R && cap <= p->cap) return SKV_OK;
+  if (cap > 0x7fffffffLL) return fail(p, SKV_ERR_ARG, "allocate: request longer than 2^31 native blocks");
+  DeviceGuard g(p->device);
+  int nR = p->R, ncap = p->cap;
+  while (nR < rows) nR *= 2;
+  while (ncap < cap) ncap = (int)std::min<long long>(2LL * ncap, 0x7fffffffLL);
+  skv::DevAlloc& d = p->dev;
+  int2* tab = nullptr;
+  int32_t *ns = nullptr, *tk = nullptr, *md = nullptr;
+  SKV_CUDA(p, cudaMalloc(&tab, (size_t)nR * ncap * sizeof(int2)));
+  SKV_CUDA(p, cudaMalloc(&ns, (size_t)nR * sizeof(int32_t)));
+  SKV_CUDA(p, cudaMalloc(&tk, (size_t)nR * sizeof(int32_t)));
+  SKV_CUDA(p, cudaMalloc(&md, (size_t)nR * sizeof(int32_t)));
+  SKV_CUDA(p, cudaMemcpy2DAsync(tab, (size_t)ncap * sizeof(int2), d.req_table, (size_t)p->cap * sizeof(int2),
+                                (size_t)p->cap * sizeof(int2), (size_t)p->R, cudaMemcpyDeviceToDevice, p->stream));
+  SKV_CUDA(p, cudaMemsetAsync(ns + p->R, 0, (size_t)(nR - p->R) * sizeof(int32_t), p->stream));
+  SKV_CUDA(p, cudaMemsetAsync(tk + p->R, 0, (size_t)(nR - p->R) * sizeof(int32_t), p->stream));
+  SKV_CUDA(p, cudaMemsetAsync(md + p->R, 0xff, (size_t)(nR - p->R) * sizeof(int32_t), p->stream));
+  SKV_CUDA(p, cudaMemcpyAsync(ns, d.req_nslots, (size_t)p->R * sizeof(int32_t), cudaMemcpyDeviceToDevice, p->stream));
+  SKV_CUDA(p, cudaMemcpyAsync(tk, d.req_tokens, (size_t)p->R * sizeof(int32_t), cudaMemcpyDeviceToDevice, p->stream));
+  SKV_CUDA(p, cudaMemcpyAsync(md, d.req_model, (size_t)p->R * sizeof(int32_t), cudaMemcpyDeviceToDevice, p->stream));
+  SKV_CUDA(p, cudaStreamSynchronize(p->stream));  // other streams may still read the old table
+  SKV_CUDA(p, cudaDeviceSynchronize());
+  cudaFree(d.req_table);
+  cudaFree(d.req_nslots);
+  cudaFree(d.req_tokens);
+  cudaFree(d.req_model);
+  d.req_table = tab;
+  d.req_nslots = ns;
+  d.req_tokens = tk;
+  d.req_model = md;
+  p->req.resize(nR);
+  for (int h = nR - 1; h >= p->R; --h) p->free_handles.push_back(h);  // lowest new handle on top
+  p->R = nR;
+  p->cap = ncap;
+  p->prm.cap = ncap;
+  return SKV_OK;
+}
+
 // try_allocate (kv_cache.hpp:104-123) on the host mirror; queues the claims.
 skv_status grow_handle_impl(skv_pool* p, int h, uint64_t id, int m, long long tokens);
 
@@ -369,8 +416,10 @@ skv_status try_allocate_impl(skv_pool* p, uint64_t id, int m, long long tokens) 
   int h;
   auto it = p->id2h.find(id);
   if (it == p->id2h.end()) {  // registers on first touch (:106), even if it then fails (Q3)
-    if (p->free_handles.empty())
-      return fail(p, SKV_ERR_ARG, "allocate: device request table full (max_requests)");
+    if (p->free_handles.empty()) {
+      skv_status st = grow_tables(p, (long long)p->R + 1, p->cap);
+      if (st) return st;
+    }
     h = p->free_handles.back();
     p->free_handles.pop_back();
     p->id2h.emplace(id, h);
@@ -399,7 +448,10 @@ skv_status grow_handle_impl(skv_pool* p, int h, uint64_t id, int m, long long to
     c = need - r.nslots;
     const long long avail = p->open[m] + p->free_count * mi.sub;  // :88-90
     if (avail < c) return SKV_CACHE_FULL;                           // :110-112
-    if (need > p->cap) return fail(p, SKV_ERR_ARG, "allocate: request exceeds max_blocks_per_request");
+    if (need > p->cap) {
+      skv_status st = grow_tables(p, p->R, need);
+      if (st) return st;
+    }
   }
   const long long w0 = entry_waste(p, r);
   const int have = r.nslots;
@@ -721,6 +773,10 @@ size_t skv_available_slots(skv_pool* p, int32_t m) {
 skv_status skv_can_grow_to(skv_pool* p, uint64_t id, int32_t m, int64_t tokens, int32_t* out) {
   if (m < 0 || m >= p->M) return fail(p, SKV_ERR_ARG, "model index out of range");
   const long long need = ceil_div_ll(tokens, p->tpb);
+  if (need < 0) {  // the reference's size_t need wraps to a huge count: never satisfiable (:93-98)
+    *out = 0;
+    return SKV_OK;
+  }
   long long have = 0;
   auto it = p->id2h.find(id);
   if (it != p->id2h.end()) have = p->req[it->second].nslots;
@@ -755,6 +811,9 @@ skv_status skv_synchronize(skv_pool* p) {
   SKV_CUDA(p, cudaStreamSynchronize(p->stream));
   int32_t status = 0;
   SKV_CUDA(p, cudaMemcpy(&status, p->dev.status, sizeof(status), cudaMemcpyDeviceToHost));
+  if (status == 3)
+    return fail(p, SKV_ERR_CUDA, "decode plan exceeded the work-list capacity sized at capture time "
+                                 "(a CUDA graph replayed at longer contexts): re-capture the graph");
   if (status) return fail(p, SKV_ERR_CUDA, "device allocator invariant violated (code " + std::to_string(status) + ")");
   return SKV_OK;
 }
@@ -1099,8 +1158,7 @@ skv_status skv_decode_attention(skv_pool* p, skv_batch* b, const skv_decode_args
   // pieces (4 per warp slot: enough small work to even out the launch's tail); leading
   // parts are cut to <= split tokens only when there are too few (request, kv head)s to
   // keep every warp slot busy (~4 pieces per slot).
-  int nsm = 148;
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, p->device);
+  const int nsm = skv::num_sms();  // current device = the pool's (DeviceGuard)
   const long long slots8 = (long long)nsm * skv::decode_warps_per_cta() * skv::decode_ctas_per_sm();
   int split = a->split_tokens;
   if (split < 0) return fail(p, SKV_ERR_ARG, "decode: split_tokens must be >= 0");
@@ -1163,6 +1221,9 @@ skv_status skv_decode_attention(skv_pool* p, skv_batch* b, const skv_decode_args
   dp.counter = b->d_counter + 2 * parity;
   dp.itemx = b->d_itemx;
   dp.rscr = b->d_rscr;
+  dp.items_cap = (int)std::min<size_t>(b->items_cap, 0x7fffffff);
+  dp.slots_cap = (int)std::min<size_t>(b->slots_cap, 0x7fffffff);
+  dp.status = p->dev.status;
   dp.arrive = b->d_arrive + parity * b->items_cap;
   dp.ws_o = b->d_ws_o;
   dp.ws_ml = b->d_ws_ml;

@@ -5,7 +5,26 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 namespace skv {
+
+// Kernel function attributes are per device: the dynamic shared-memory opt-in of a kernel is
+// applied once per (kernel, device) — `done` is the kernel's own device bitmask — so a pool on
+// a second device (or another thread) never launches without it.
+template <typename K>
+inline cudaError_t ensure_smem_attr(K kernel, int bytes, std::atomic<uint64_t>& done) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
+
+// SM count of the current device (cached per device ordinal, thread-safe).
+int num_sms();
 
 constexpr int kMaxModels = 16;   // services sharing one pool
 constexpr int kMaxGroups = 16;   // groups in one data-path batch
@@ -111,6 +130,8 @@ struct DataParams {
   int4* itemx;               // [max_items] {pieces of the (request, kv head), partial-slot base,
                              //  piece index, arrival counter index}
   int* rscr;                 // [5*nreq] plan scratch
+  int items_cap, slots_cap;  // capacities of items/itemx/arrive and ws_o/ws_ml (plan guard)
+  int32_t* status;           // device invariant flag (DevAlloc::status): plan overflow -> code 3
   int* arrive;               // [items] pieces finished per (request, kv head) (self-resetting)
   int dbg;                   // debug knobs (prefill v5: bit1 = polynomial exp2 for 1/4)
   // split scheme (skv_split.cpp): split_L > 0 -> req_table rows are per (request, layer,

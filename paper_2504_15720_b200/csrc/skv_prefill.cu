@@ -1476,13 +1476,10 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel_v10(const __grid
 
 template <typename T>
 void launch_prefill_t(const DataParams& p, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(prefill_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2);
-    cudaFuncSetAttribute(prefill_kernel_v9<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemV9);
-    cudaFuncSetAttribute(prefill_kernel_v10<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemV10);
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr2{0}, attr9{0}, attr10{0};
+  ensure_smem_attr(prefill_kernel<T>, kSmem2, attr2);
+  ensure_smem_attr(prefill_kernel_v9<T>, kSmemV9, attr9);
+  ensure_smem_attr(prefill_kernel_v10<T>, kSmemV10, attr10);
   int tiles = 1, heads = 1;
   for (int i = 0; i < p.ngroups; ++i) {
     tiles = max(tiles, (p.n_new * p.g[i].G + kRows - 1) / kRows);
@@ -1497,18 +1494,14 @@ void launch_prefill_t(const DataParams& p, cudaStream_t s) {
     prefill_kernel<T><<<grid, kThreads, kSmem2, s>>>(p);
   } else if (version == 9) {
     const int npairs = (tiles + 1) / 2;
-    int nsm = 148, dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int nsm = num_sms();
     const long long items = (long long)npairs * heads * p.nreq;
     const int grid = (int)std::min<long long>(items, nsm);
     cudaMemsetAsync(p.counter, 0, sizeof(int), s);
     prefill_kernel_v9<T><<<grid, kThreadsV3, kSmemV9, s>>>(p, npairs, heads);
   } else if (version == 10) {
     const int npairs = (tiles + 1) / 2;
-    int nsm = 148, dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int nsm = num_sms();
     const long long items = (long long)npairs * heads * p.nreq;
     const int clusters = (int)std::min<long long>(items, nsm / 2);
     cudaMemsetAsync(p.counter, 0, sizeof(int), s);

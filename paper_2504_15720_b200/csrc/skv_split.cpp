@@ -202,23 +202,41 @@ uint64_t skv_split_kernel_launches(const skv_split* s) { return s->launches; }
 
 skv_status skv_split_grow(skv_split* s, const uint64_t* ids, const int32_t* models, const int64_t* tokens, int32_t n,
                           int32_t* granted) {
+  // Validate every op before any state changes: an early error return must not leave
+  // queued claims behind (they would be replayed by the next launch_ops as releases).
+  {
+    std::unordered_map<uint64_t, int> seen;  // model of ids first seen in this call
+    for (int i = 0; i < n; ++i) {
+      const int m = models[i];
+      if (m < 0 || m >= s->M) return sfail(s, SKV_ERR_ARG, "split grow: model index out of range");
+      if (tokens[i] < 0) return sfail(s, SKV_ERR_VALIDATION, "split grow: negative tokens");
+      auto it = s->live.find(ids[i]);
+      const int prev = it != s->live.end() ? it->second.model : (seen.count(ids[i]) ? seen[ids[i]] : m);
+      if (prev != m) return sfail(s, SKV_ERR_LOGIC, "split grow: model changed");
+      seen[ids[i]] = m;
+      if (it == s->live.end() && s->live.size() + seen.size() > (size_t)s->R)
+        return sfail(s, SKV_ERR_ARG, "split grow: more live requests than max_requests");
+      if ((tokens[i] + 15) / 16 > s->cap)
+        return sfail(s, SKV_ERR_ARG, "split grow: request exceeds max_blocks_per_request");
+    }
+  }
   for (int i = 0; i < n; ++i) {
     const int m = models[i];
-    if (m < 0 || m >= s->M) return sfail(s, SKV_ERR_ARG, "split grow: model index out of range");
-    if (tokens[i] < 0) return sfail(s, SKV_ERR_VALIDATION, "split grow: negative tokens");
     auto it = s->live.find(ids[i]);
     const long long have = it == s->live.end() ? 0 : it->second.blocks;
-    if (it != s->live.end() && it->second.model != m) return sfail(s, SKV_ERR_LOGIC, "split grow: model changed");
     const long long need = (tokens[i] + 15) / 16;
     const SplitModel& sm = s->models[m];
     const long long claims = need > have ? (need - have) * sm.L * sm.H : 0;
-    if (need > s->cap) return sfail(s, SKV_ERR_ARG, "split grow: request exceeds max_blocks_per_request");
     if (claims > s->top) {  // all-or-nothing, no change (as kv_cache.hpp:110-112)
       if (granted) granted[i] = 0;
       continue;
     }
     skv_status st = skv_try_allocate(s->reg, ids[i], m, tokens[i]);
-    if (st != SKV_OK) return sfail(s, st, std::string("split grow: registry: ") + skv_last_error(s->reg));
+    if (st != SKV_OK) {  // registry capacity: keep what was already granted consistent on the GPU
+      const std::string msg = std::string("split grow: registry: ") + skv_last_error(s->reg);
+      launch_ops(s, 0);
+      return sfail(s, st == SKV_CACHE_FULL ? SKV_ERR_LOGIC : st, msg);
+    }
     if (granted) granted[i] = 1;
     if (claims > 0) {
       skv::SplitOp op{};
@@ -250,6 +268,12 @@ skv_status skv_split_grow(skv_split* s, const uint64_t* ids, const int32_t* mode
 }
 
 skv_status skv_split_free(skv_split* s, const uint64_t* ids, int32_t n) {
+  {  // validate first (unknown or repeated id -> error, nothing changed)
+    std::unordered_map<uint64_t, int> seen;
+    for (int i = 0; i < n; ++i)
+      if (!s->live.count(ids[i]) || seen[ids[i]]++)
+        return sfail(s, SKV_ERR_LOGIC, "split free: unknown request");
+  }
   for (int i = 0; i < n; ++i) {  // SplitCacheCounter::free (kv_cache.hpp:304-309)
     auto it = s->live.find(ids[i]);
     if (it == s->live.end()) return sfail(s, SKV_ERR_LOGIC, "split free: unknown request");

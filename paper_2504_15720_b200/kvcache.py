@@ -454,12 +454,38 @@ class UnifiedKvCache:
         return Batch(self, groups)
 
 
+def _check_tensors(ts, shapes, dtype: int, device: int, what: str):
+    """Raises ArgError unless every torch tensor in ``ts`` is a contiguous CUDA tensor on
+    ``device`` of the pool's dtype with the expected shape (the C-ABI takes raw pointers, so
+    a mismatch would otherwise read or write out of bounds).  Raw integer addresses are
+    passed through unchecked."""
+    if len(ts) != len(shapes):
+        raise ArgError(f"{what}: expected {len(shapes)} tensors (one per group), got {len(ts)}")
+    for g, (t, shp) in enumerate(zip(ts, shapes)):
+        if isinstance(t, int):
+            continue
+        if not hasattr(t, "data_ptr"):
+            raise ArgError(f"{what}[{g}]: expected a torch tensor or a device address")
+        if not t.is_cuda or (t.device.index or 0) != device:
+            raise ArgError(f"{what}[{g}]: tensor on {t.device}, pool on cuda:{device}")
+        want = "float16" if dtype == FP16 else "bfloat16"
+        if str(t.dtype).split(".")[-1] != want:
+            raise ArgError(f"{what}[{g}]: dtype {t.dtype}, pool stores {want}")
+        if tuple(t.shape) != tuple(shp):
+            raise ArgError(f"{what}[{g}]: shape {tuple(t.shape)}, expected {tuple(shp)}")
+        if not t.is_contiguous():
+            raise ArgError(f"{what}[{g}]: tensor must be contiguous")
+
+
 class Batch:
     """Requests covered by one data-path launch, grouped by service (model index)."""
 
     def __init__(self, cache: UnifiedKvCache, groups: Sequence[tuple[int, Sequence[int]]]):
         self.cache = cache
         self.groups = [(int(m), [int(i) for i in ids]) for m, ids in groups]
+        lay = {m: cache.layout(m) for m in {m for m, _ in self.groups}}
+        # per group (B_g, Hq/tp, Hkv/tp, head_dim) for argument validation
+        self._shapes = [(len(ids), lay[m].q_heads, lay[m].kv_heads, lay[m].head_dim) for m, ids in self.groups]
         gm = (C.c_int32 * len(self.groups))(*[m for m, _ in self.groups])
         gs = (C.c_int32 * len(self.groups))(*[len(ids) for _, ids in self.groups])
         flat = [i for _, ids in self.groups for i in ids]
@@ -471,6 +497,8 @@ class Batch:
     def reset(self, groups: Sequence[tuple[int, Sequence[int]]]):
         """Re-point this batch at new requests, reusing its device buffers."""
         self.groups = [(int(m), [int(i) for i in ids]) for m, ids in groups]
+        lay = {m: self.cache.layout(m) for m in {m for m, _ in self.groups}}
+        self._shapes = [(len(ids), lay[m].q_heads, lay[m].kv_heads, lay[m].head_dim) for m, ids in self.groups]
         gm = (C.c_int32 * len(self.groups))(*[m for m, _ in self.groups])
         gs = (C.c_int32 * len(self.groups))(*[len(ids) for _, ids in self.groups])
         flat = [i for _, ids in self.groups for i in ids]
@@ -504,6 +532,18 @@ class Batch:
         """Paged decode attention of every group for ``layer``.  With ``k``/``v`` (each
         [B_g, 1, Hkv, d]) the step's new token is appended at position tokens-1 inside the
         same launch (fused ``append(k, v, layer, 1)``)."""
+        self.cache._chk(self.cache._lib.skv_decode_attention(self.cache._h, self._h,
+                                                             C.byref(self._decode_args(q, out, layer, softmax_scale,
+                                                                                       split_tokens, k, v)),
+                                                             _stream_ptr(stream)))
+
+    def _decode_args(self, q, out, layer, softmax_scale, split_tokens, k, v):
+        dt, dev = self.cache.dtype, self.cache.device
+        _check_tensors(q, [(B, Hq, d) for B, Hq, _, d in self._shapes], dt, dev, "decode q")
+        _check_tensors(out, [(B, Hq, d) for B, Hq, _, d in self._shapes], dt, dev, "decode out")
+        if k is not None and v is not None:
+            _check_tensors(k, [(B, 1, Hkv, d) for B, _, Hkv, d in self._shapes], dt, dev, "decode k")
+            _check_tensors(v, [(B, 1, Hkv, d) for B, _, Hkv, d in self._shapes], dt, dev, "decode v")
         n = len(self.groups)
         qa = (C.c_void_p * n)(*[_ptr(t) for t in q])
         oa = (C.c_void_p * n)(*[_ptr(t) for t in out])
@@ -516,8 +556,8 @@ class Batch:
             va = (C.c_void_p * n)(*[_ptr(t) for t in v])
             a.k = C.cast(ka, C.POINTER(C.c_void_p))
             a.v = C.cast(va, C.POINTER(C.c_void_p))
-        self.cache._chk(self.cache._lib.skv_decode_attention(self.cache._h, self._h, C.byref(a),
-                                                             _stream_ptr(stream)))
+        a._keep = (qa, oa) + ((ka, va) if k is not None else ())
+        return a
 
     def decode_trace(self, max_records: int = 4096) -> np.ndarray:
         """Debug (SKV_TRACE=1): per-warp [start_ns, after_wait_ns, end_ns, tiles<<32|items]
@@ -530,14 +570,26 @@ class Batch:
         return buf[: n.value]
 
     def append(self, k: Sequence, v: Sequence, layer: int, n_new: int = 1, stream=None):
+        self.cache._chk(self.cache._lib.skv_append_kv(self.cache._h, self._h, C.byref(self._append_args(k, v, layer,
+                                                                                                       n_new)),
+                                                      _stream_ptr(stream)))
+
+    def _append_args(self, k, v, layer, n_new):
+        dt, dev = self.cache.dtype, self.cache.device
+        _check_tensors(k, [(B, n_new, Hkv, d) for B, _, Hkv, d in self._shapes], dt, dev, "append k")
+        _check_tensors(v, [(B, n_new, Hkv, d) for B, _, Hkv, d in self._shapes], dt, dev, "append v")
         n = len(self.groups)
         ka = (C.c_void_p * n)(*[_ptr(t) for t in k])
         va = (C.c_void_p * n)(*[_ptr(t) for t in v])
         a = _AppendArgs(C.cast(ka, C.POINTER(C.c_void_p)), C.cast(va, C.POINTER(C.c_void_p)), layer, n_new)
-        self.cache._chk(self.cache._lib.skv_append_kv(self.cache._h, self._h, C.byref(a), _stream_ptr(stream)))
+        a._keep = (ka, va)
+        return a
 
     def prefill(self, q: Sequence, out: Sequence, layer: int, q_len: int, softmax_scale: float = 0.0,
                 stream=None):
+        dt, dev = self.cache.dtype, self.cache.device
+        _check_tensors(q, [(B, q_len, Hq, d) for B, Hq, _, d in self._shapes], dt, dev, "prefill q")
+        _check_tensors(out, [(B, q_len, Hq, d) for B, Hq, _, d in self._shapes], dt, dev, "prefill out")
         n = len(self.groups)
         qa = (C.c_void_p * n)(*[_ptr(t) for t in q])
         oa = (C.c_void_p * n)(*[_ptr(t) for t in out])
@@ -664,23 +716,13 @@ class SplitBatch(Batch):
         return int(self.split.grow(ids, models, toks).sum())
 
     def decode(self, q, out, layer, softmax_scale=0.0, split_tokens=0, stream=None, k=None, v=None):
-        n = len(self.groups)
-        qa = (C.c_void_p * n)(*[_ptr(t) for t in q])
-        oa = (C.c_void_p * n)(*[_ptr(t) for t in out])
-        a = _DecodeArgs(C.cast(qa, C.POINTER(C.c_void_p)), C.cast(oa, C.POINTER(C.c_void_p)), softmax_scale,
-                        layer, split_tokens)
-        if k is not None:
-            ka = (C.c_void_p * n)(*[_ptr(t) for t in k])
-            va = (C.c_void_p * n)(*[_ptr(t) for t in v])
-            a.k = C.cast(ka, C.POINTER(C.c_void_p))
-            a.v = C.cast(va, C.POINTER(C.c_void_p))
+        if (k is None) != (v is None):
+            raise ValueError("decode: pass both k and v for the fused append, or neither")
+        a = self._decode_args(q, out, layer, softmax_scale, split_tokens, k, v)
         self.split._chk(self.split._lib.skv_split_decode(self.split._s, self._h, C.byref(a), _stream_ptr(stream)))
 
     def append(self, k, v, layer, n_new=1, stream=None):
-        n = len(self.groups)
-        ka = (C.c_void_p * n)(*[_ptr(t) for t in k])
-        va = (C.c_void_p * n)(*[_ptr(t) for t in v])
-        a = _AppendArgs(C.cast(ka, C.POINTER(C.c_void_p)), C.cast(va, C.POINTER(C.c_void_p)), layer, n_new)
+        a = self._append_args(k, v, layer, n_new)
         self.split._chk(self.split._lib.skv_split_append(self.split._s, self._h, C.byref(a), _stream_ptr(stream)))
 
     def prefill(self, *a, **k):
