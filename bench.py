@@ -491,12 +491,75 @@ def run_gpu(args):
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
+    cache.synchronize()  # surfaces any device-side invariant flag raised during the runs
+    if not args.no_parity:
+        result["parity"] = headline_parity(torch, cache, batch, q, k, v, stream, NLAYERS)
     if rank == 0 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(cache, batch, q, args)
     if rank == 0:
         print(json.dumps(result), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def headline_parity(torch, cache, batch, q, k, v, stream, nlayers, per_end=2, tol=2e-3):
+    """Oracle check of the measured code path at the measured size (run after the timed
+    regions): the same fused append+decode launch over the WHOLE batch at layers 0, 31 and the
+    last layer, then the fp32 CPU oracle (oracle/attn_oracle.c; checker only) on a sample of
+    its rows — the first and last `per_end` requests of every service, which covers both
+    (request, kv head)s that were run as one piece and the last n_cut ones that were cut into
+    pieces merged in-kernel."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle_py as O
+
+    layers = sorted({0, min(31, nlayers - 1), nlayers - 1})
+    outs = {}
+    for layer in layers:
+        o = [torch.full_like(x, float("nan")) for x in q]
+        batch.decode(q, o, layer, stream=stream, k=k, v=v)
+        outs[layer] = o
+    info = batch.plan_info()
+    torch.cuda.synchronize()
+    groups = batch.groups
+    picks = [sorted(set(range(min(per_end, len(ids)))) | set(range(max(0, len(ids) - per_end), len(ids))))
+             for _, ids in groups]
+    hkv = [cache.layout(m).kv_heads for m, _ in groups]
+    # (request, kv head) index in batch order: the last n_cut of them were cut
+    first_rh, acc = [], 0
+    for (m, ids), h in zip(groups, hkv):
+        first_rh.append(acc)
+        acc += len(ids) * h
+    cut_from = info["sum_hkv"] - info["n_cut"]
+    blocks = sorted({int(b) for (m, ids), pk in zip(groups, picks) for i in pk
+                     for b in cache.block_table_np(ids[i])[:, 0]})
+    remap = {b: j for j, b in enumerate(blocks)}
+    img = cache.read_blocks(np.array(blocks, dtype=np.int32))
+    worst, n_rows, cut_rows = 0.0, 0, 0
+    for gi, ((m, ids), pk) in enumerate(zip(groups, picks)):
+        lay = cache.layout(m)
+        olay = O.layout(lay.merged_stride, lay.native_stride, lay.layer_stride, lay.head_stride, lay.kv_stride,
+                        lay.tpb, lay.head_dim, lay.kv_heads, lay.q_heads, lay.phys_layers, lay.dtype)
+        tabs = [cache.block_table_np(ids[i]) for i in pk]
+        tt = np.zeros((len(pk), max(len(t) for t in tabs), 2), np.int32)
+        for j, t in enumerate(tabs):
+            tt[j, :len(t), 0] = [remap[int(b)] for b in t[:, 0]]
+            tt[j, :len(t), 1] = t[:, 1]
+        ctx = np.array([cache.request_tokens(ids[i]) for i in pk], np.int64)
+        qh = q[gi][pk].contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+        G = lay.q_heads // lay.kv_heads
+        for layer in layers:
+            if layer >= cache.models[m].num_layers:
+                continue
+            ref = O.decode_attention(olay, img, layer, tt, ctx, qh, 1.0 / np.sqrt(lay.head_dim))
+            got = outs[layer][gi][pk].float().cpu().numpy()
+            worst = max(worst, float(np.abs(got - ref).max()) if not np.isnan(got).any() else float("inf"))
+            n_rows += got.shape[0] * got.shape[1]
+            cut_rows += sum(G for i in pk for h in range(lay.kv_heads)
+                            if first_rh[gi] + i * lay.kv_heads + h >= cut_from)
+    return {"max_abs": worst, "tol": tol, "ok": bool(worst <= tol), "n_rows": n_rows, "rows_in_cut_pieces": cut_rows,
+            "layers": layers, "requests_per_service": [len(pk) for pk in picks],
+            "schedule": info, "oracle": "oracle/attn_oracle.c (fp32, OpenMP)",
+            "note": "fused append+decode launch over the whole measured batch; first/last requests of each service"}
 
 
 def _sample_image(cache, batch_groups, per_group):
@@ -1031,6 +1094,8 @@ def main():
                     help="CPU-baseline sample duration (bounded sample of the workload)")
     ap.add_argument("--cpu-requests", dest="cpu_requests", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", dest="no_cpu_baseline", action="store_true")
+    ap.add_argument("--no-parity", dest="no_parity", action="store_true",
+                    help="skip the post-timing oracle check of a sample of the measured launch")
     ap.add_argument("--no-graph", dest="no_graph", action="store_true",
                     help="eager launches instead of a CUDA graph per step")
     args = ap.parse_args()

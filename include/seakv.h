@@ -180,6 +180,13 @@ typedef struct {
 skv_status skv_decode_attention(skv_pool* p, skv_batch* b, const skv_decode_args* args,
                                 void* stream);
 
+/* Work-list schedule chosen by the batch's last decode launch: split_tokens (max tokens of a
+ * (request, kv head)'s leading piece; >= 2^30 = no chunking), n_cut (the last n_cut
+ * (request, kv head)s of the batch get two trailing pieces, merged in-kernel) and sum_hkv
+ * (the (request, kv head)s of the launch).  For tests and the bench's parity sample. */
+skv_status skv_batch_plan_info(skv_pool* p, skv_batch* b, int32_t* split_tokens, int64_t* n_cut,
+                               int64_t* sum_hkv);
+
 typedef struct {
   const void* const* k; /* [host array of n_groups dev ptrs] each [B_g][n_new][Hkv/tp][d] */
   const void* const* v;

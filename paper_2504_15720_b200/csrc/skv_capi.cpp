@@ -149,6 +149,7 @@ struct skv_batch {
   uint64_t plan_epoch = ~0ull;
   uint64_t launch_seq = 0;
   int plan_split = 0;
+  long long last_sum_hkv = 0, last_ncut = 0;  // schedule of the last decode launch (skv_batch_plan_info)
   unsigned long long* d_trace = nullptr;  // SKV_TRACE=1: per-warp timing of the last decode
   size_t trace_n = 0;
 };
@@ -1183,6 +1184,8 @@ skv_status skv_decode_attention(skv_pool* p, skv_batch* b, const skv_decode_args
   const long long piece_tiles = std::min<long long>(ceil_div_ll(work, std::max(1LL, sum_hkv) * 16), split / 16);
   const long long ncut = ncut_x4 >= 0 ? ncut_x4 * slots8 / 4 : (piece_tiles < 64 ? slots8 / 2 : 2 * slots8);
   dp.n_cut = (int)std::min<long long>(ncut, sum_hkv);
+  b->last_sum_hkv = sum_hkv;
+  b->last_ncut = dp.n_cut;
   // capacities: an upper bound on pieces and partial slots (every head cut)
   long long items = 0, slots = 0;
   const long long maxt = std::max(1, split / 16);
@@ -1261,6 +1264,15 @@ skv_status skv_decode_attention(skv_pool* p, skv_batch* b, const skv_decode_args
   skv::launch_decode(dp, maxg, 0, s);
   p->launches++;
   return after_data(p, s);
+}
+
+skv_status skv_batch_plan_info(skv_pool* p, skv_batch* b, int32_t* split_tokens, int64_t* n_cut,
+                               int64_t* sum_hkv) {
+  if (!b || b->pool != p) return fail(p, SKV_ERR_ARG, "batch belongs to another pool");
+  if (split_tokens) *split_tokens = b->plan_split;
+  if (n_cut) *n_cut = b->last_ncut;
+  if (sum_hkv) *sum_hkv = b->last_sum_hkv;
+  return SKV_OK;
 }
 
 skv_status skv_append_kv(skv_pool* p, skv_batch* b, const skv_append_args* a, void* stream) {

@@ -183,6 +183,7 @@ def lib() -> C.CDLL:
         "skv_batch_grow": (S, [P, P, C.c_int64, C.POINTER(C.c_int32)]),
         "skv_batch_decode_bytes": (S, [P, P, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
         "skv_decode_attention": (S, [P, P, C.POINTER(_DecodeArgs), P]),
+        "skv_batch_plan_info": (S, [P, P, C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
         "skv_append_kv": (S, [P, P, C.POINTER(_AppendArgs), P]),
         "skv_prefill_attention": (S, [P, P, C.POINTER(_PrefillArgs), P]),
         "skv_model_layout": (S, [P, C.c_int32, C.POINTER(Layout)]),
@@ -558,6 +559,14 @@ class Batch:
             a.v = C.cast(va, C.POINTER(C.c_void_p))
         a._keep = (qa, oa) + ((ka, va) if k is not None else ())
         return a
+
+    def plan_info(self) -> dict:
+        """Schedule of the last decode launch: split_tokens, n_cut (the last n_cut (request,
+        kv head)s of the batch, in batch order, were cut into pieces merged in-kernel), sum_hkv."""
+        s, n, h = C.c_int32(), C.c_int64(), C.c_int64()
+        self.cache._chk(self.cache._lib.skv_batch_plan_info(self.cache._h, self._h, C.byref(s), C.byref(n),
+                                                            C.byref(h)))
+        return {"split_tokens": s.value, "n_cut": n.value, "sum_hkv": h.value}
 
     def decode_trace(self, max_records: int = 4096) -> np.ndarray:
         """Debug (SKV_TRACE=1): per-warp [start_ns, after_wait_ns, end_ns, tiles<<32|items]
