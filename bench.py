@@ -164,8 +164,31 @@ def make_workload(P, args):
                     f"block (logical l -> l % {args.phys_layers}), 40 layer-index launches per step")
 
 
-def setup(P, torch, args, device):
+def add_tp_shard(P, wl, args, tp):
+    """N >= 2: one 70B-shape service (reference llama2-70b: 80 layers, 64 KV heads, Q7) is
+    head-sharded over tp = min(N, 4) ranks.  Each rank's pool holds its 64/tp KV heads as one
+    more service — native block = 16*80*2*(64/tp)*128*2 B, exactly native_block_bytes(70B, tp)
+    (kv_cache.hpp:17-22) — and replays the same op stream, so block tables are identical on the
+    tp ranks with no communication.  16*tp requests per group keep the per-rank bytes constant
+    as N grows (weak scaling)."""
+    h = 64 // tp
+    nreq = 16 * tp
+    ctx = args.ctx or 2048
+    wl.services = list(wl.services) + [(f"llama2-70b/tp{tp}", 80, h, h)]
+    wl.ctxs = list(wl.ctxs) + [[ctx] * nreq]
+    grow = args.warmup * 2 + args.steps * 2 + 8
+    wl.pool_blocks = _blocks(P, wl.services, wl.ctxs, grow)
+    wl.nlayers = 80
+    wl.desc += (f"; plus a llama2-70b-shape service head-sharded over tp={tp} ranks ({nreq} requests per tp group, "
+                f"{h} KV/Q heads per rank, W_o row slice + NCCL AllReduce of the [B, 8192] output per layer; "
+                f"80 layer-index launches per step)")
+    return wl
+
+
+def setup(P, torch, args, device, tp_shard=0):
     wl = make_workload(P, args)
+    if tp_shard:
+        add_tp_shard(P, wl, args, tp_shard)
     models = [P.ModelSpec(n, L, H, 128, 2, Hq) for n, L, H, Hq in wl.services]
     ctx_max = max(max(c) for c in wl.ctxs if c) + args.warmup * 2 + args.steps * 2 + 8
     nreq_total = sum(len(c) for c in wl.ctxs)
@@ -203,12 +226,15 @@ def setup(P, torch, args, device):
     return wl, cache, batch, q, out, k, v, stream
 
 
-def step_device(batch, q, out, k, v, stream, nlayers):
+def step_device(batch, q, out, k, v, stream, nlayers, epilogue=None, timed=False):
     """One decode step: allocator grow (+1 token per request), then per layer one fused
-    launch that appends the new K/V token and runs paged decode attention."""
+    launch that appends the new K/V token and runs paged decode attention (then, with a
+    head-sharded service, its output projection + AllReduce)."""
     batch.grow(1)
     for layer in range(nlayers):
         batch.decode(q, out, layer, stream=stream, k=k, v=v)
+        if epilogue:
+            epilogue(layer, out, timed)
 
 
 def capture_step_graph(torch, cache, batch, q, out, k, v, stream, nlayers):
@@ -281,9 +307,42 @@ def run_gpu(args):
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
-    wl, cache, batch, q, out, k, v, stream = setup(P, torch, args, local)
+    # N >= 2: a 70B-shape service head-sharded over tp = min(N, 4) ranks joins every rank's
+    # pool; its per-layer output reduction is the data path's only collective
+    tp = min(world, 4) if world > 1 and not args.no_tp_group else 0
+    if tp and world % tp:
+        raise SystemExit(f"--gpus {world}: not a multiple of the tp group size {tp}")
+    pg = None
+    if tp:
+        for g0 in range(0, world, tp):  # every rank creates every subgroup, same order
+            grp = dist.new_group(list(range(g0, g0 + tp)))
+            if g0 <= rank < g0 + tp:
+                pg = grp
+    wl, cache, batch, q, out, k, v, stream = setup(P, torch, args, local, tp_shard=tp)
     NLAYERS = wl.nlayers
     red_dev = "cuda" if backend == "nccl" else "cpu"
+    shard_g = len(wl.services) - 1 if tp else None
+    ar_events = []
+    if tp:
+        L70 = wl.services[shard_g][1]
+        B70 = len(wl.ctxs[shard_g])
+        gen = torch.Generator(device=local).manual_seed(70)
+        w_o = (torch.randn((q[shard_g].shape[1] * 128, 8192), generator=gen, device=local) / 90).half()
+        y70 = torch.empty((B70, 8192), device=local, dtype=torch.float16)
+
+    def tp_epilogue(layer, outs, timed=False, y=None):
+        """70B shard: row-parallel W_o slice (cuBLAS) and NCCL AllReduce over the tp group."""
+        if not tp or layer >= L70:
+            return
+        y = y70 if y is None else y
+        torch.matmul(outs[shard_g].view(B70, -1), w_o, out=y)
+        if timed:
+            e = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            e[0].record(stream)
+        dist.all_reduce(y, op=dist.ReduceOp.SUM, group=pg)
+        if timed:
+            e[1].record(stream)
+            ar_events.append(e)
 
     def barrier():
         torch.cuda.synchronize()
@@ -306,9 +365,10 @@ def run_gpu(args):
 
     # ---- device-resident timed region (value) ------------------------------------------
     for _ in range(args.warmup):
-        step_device(batch, q, out, k, v, stream, NLAYERS)
+        step_device(batch, q, out, k, v, stream, NLAYERS, tp_epilogue)
     barrier()
-    graph = None if args.no_graph else capture_step_graph(torch, cache, batch, q, out, k, v, stream, NLAYERS)
+    # the collective is not captured: with a tp group the step runs eagerly
+    graph = None if (args.no_graph or tp) else capture_step_graph(torch, cache, batch, q, out, k, v, stream, NLAYERS)
     kv_total = all_total = 0.0
     launches0 = cache.kernel_launches()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -321,7 +381,7 @@ def run_gpu(args):
                 cache.flush(stream)
                 graph.replay()
             else:
-                step_device(batch, q, out, k, v, stream, NLAYERS)
+                step_device(batch, q, out, k, v, stream, NLAYERS, tp_epilogue, timed=True)
             kvb, totb = step_bytes(batch, NLAYERS)  # host mirror: exact context of this step
             kv_total += kvb
             all_total += totb
@@ -354,7 +414,10 @@ def run_gpu(args):
     elapsed_ms = max_over_ranks(t0.elapsed_time(t1))
     kv_all = sum_over_ranks(kv_total)
     value = kv_all / (elapsed_ms / 1e3) / 1e9
-    tokens_s = sum_over_ranks(float(sum(len(c) for c in wl.ctxs) * args.steps)) / (elapsed_ms / 1e3)
+    # a head-sharded request is served by its tp ranks together: count it once per group
+    n_tok = sum(len(c) for c in wl.ctxs) - (len(wl.ctxs[shard_g]) * (tp - 1) / tp if tp else 0)
+    tokens_s = sum_over_ranks(float(n_tok * args.steps)) / (elapsed_ms / 1e3)
+    ar_ms = sum(a.elapsed_time(b) for a, b in ar_events)
     hbm, peak_kind = peaks()
     achieved = dec_bytes / (dec_ms / 1e3) / 1e9  # algorithmic bytes / decode launch time
     traffic, traffic_src = profiled_traffic(wl, args)
@@ -382,18 +445,23 @@ def run_gpu(args):
     # outputs go back (d2h stream) while chunk c+1 runs; within a chunk the launches stay
     # back to back (no event between them, so programmatic dependent launch still
     # overlaps them).  Device buffers are double-buffered by step parity.
-    def pinned_like(x):
-        return torch.empty((NLAYERS,) + tuple(x.shape), dtype=x.dtype, pin_memory=True)
+    glayers = [wl.services[m][1] for m, _ in batch.groups]  # each service copies only its own layers
 
-    hq = [pinned_like(x) for x in q]
-    hk = [pinned_like(x) for x in k]
-    hv = [pinned_like(x) for x in v]
-    ho = [pinned_like(x) for x in out]
+    def pinned_like(x, nl):
+        return torch.empty((nl,) + tuple(x.shape), dtype=x.dtype, pin_memory=True)
+
+    hq = [pinned_like(x, nl) for x, nl in zip(q, glayers)]
+    hk = [pinned_like(x, nl) for x, nl in zip(k, glayers)]
+    hv = [pinned_like(x, nl) for x, nl in zip(v, glayers)]
+    ho = [pinned_like(x, nl) for x, nl in zip(out, glayers)]
+    if tp:  # the reduced 70B output of every layer comes back too
+        ho.append(torch.empty((L70, B70, 8192), dtype=torch.float16, pin_memory=True))
     for hs, ds in ((hq, q), (hk, k), (hv, v)):
         for a, b in zip(hs, ds):
             a.copy_(b.unsqueeze(0).expand_as(a).cpu())
     h2d = sum(x.numel() * x.element_size() for x in hq + hk + hv)
     d2h = sum(x.numel() * x.element_size() for x in ho)
+    glayers_o = glayers + ([L70] if tp else [])
     h2d_stream = torch.cuda.Stream(device=local)
     d2h_stream = torch.cuda.Stream(device=local)
     dq = [[torch.empty(x.shape, dtype=x.dtype, device=local) for x in hq] for _ in range(2)]
@@ -416,21 +484,27 @@ def run_gpu(args):
         with torch.cuda.stream(h2d_stream):
             h2d_stream.wait_event(comp_ev[j])  # step i-2 is done with buffer set j
             for ci, ls in enumerate(chunks):
-                for a, b in zip(dq[j] + dk[j] + dv[j], hq + hk + hv):
-                    a[ls.start:ls.stop].copy_(b[ls.start:ls.stop], non_blocking=True)
+                for a, b, nl in zip(dq[j] + dk[j] + dv[j], hq + hk + hv, glayers * 3):
+                    if ls.start < nl:
+                        a[ls.start:min(ls.stop, nl)].copy_(b[ls.start:min(ls.stop, nl)], non_blocking=True)
                 in_ev[ci].record(h2d_stream)
         batch.grow(1)
         stream.wait_event(d2h_ev[j])  # output set j drained to host
         for ci, ls in enumerate(chunks):
             stream.wait_event(in_ev[ci])
             for layer in ls:
-                batch.decode([x[layer] for x in dq[j]], [x[layer] for x in do[j]], layer, stream=stream,
-                             k=[x[layer] for x in dk[j]], v=[x[layer] for x in dv[j]])
+                sel = [min(layer, nl - 1) for nl in glayers]  # groups past their last layer are skipped
+                outs = [x[s] for x, s in zip(do[j], sel)]
+                batch.decode([x[s] for x, s in zip(dq[j], sel)], outs, layer, stream=stream,
+                             k=[x[s] for x, s in zip(dk[j], sel)], v=[x[s] for x, s in zip(dv[j], sel)])
+                if tp and layer < L70:
+                    tp_epilogue(layer, outs, y=do[j][-1][layer])
             out_ev[ci].record(stream)
             with torch.cuda.stream(d2h_stream):
                 d2h_stream.wait_event(out_ev[ci])
-                for a, b in zip(ho, do[j]):
-                    a[ls.start:ls.stop].copy_(b[ls.start:ls.stop], non_blocking=True)
+                for a, b, nl in zip(ho, do[j], glayers_o):
+                    if ls.start < nl:
+                        a[ls.start:min(ls.stop, nl)].copy_(b[ls.start:min(ls.stop, nl)], non_blocking=True)
         comp_ev[j].record(stream)
         d2h_ev[j].record(d2h_stream)
 
@@ -471,7 +545,9 @@ def run_gpu(args):
             "merged_block_bytes": cache.merged_block_bytes(),
             "pool_gb": round(cache.storage()[1] / 1e9, 2),
             "l2": "inputs larger than L2 (>= 0.6 GB K/V per layer launch vs 126 MB L2); no flush",
-            "parallelism": f"placement-sharded replicas x{world} (tp=1 groups, no collective)",
+            "parallelism": (f"placement-sharded replicas x{world} (tp=1 groups, no collective)" if not tp else
+                            f"config-2 replica per rank (tp=1, no collective) + llama2-70b shape head-sharded in "
+                            f"{world // tp} tp={tp} group(s) (NCCL AllReduce of its output per layer)"),
             "cuda_graph": graph is not None,
         },
         "e2e": {"value": round(e2e_value, 1), "unit": "GB/s", "h2d_bytes_per_step": int(h2d),
@@ -491,8 +567,15 @@ def run_gpu(args):
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
+    if tp:
+        result["allreduce"] = {"group_size": tp, "groups": world // tp, "backend": backend,
+                               "bytes_per_layer": int(y70.numel() * 2), "layers_per_step": L70,
+                               "ms_per_step_rank0": round(ar_ms / args.steps, 4),
+                               "per_layer_ms_rank0": round(ar_ms / max(1, len(ar_events)), 4),
+                               "note": "CUDA events around dist.all_reduce on the compute stream (rank 0), "
+                                       "timed steps only"}
     cache.synchronize()  # surfaces any device-side invariant flag raised during the runs
-    if not args.no_parity:
+    if rank == 0 and not args.no_parity:
         result["parity"] = headline_parity(torch, cache, batch, q, k, v, stream, NLAYERS)
     if rank == 0 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(cache, batch, q, args)
@@ -1076,6 +1159,34 @@ def run_reference(args):
     print(json.dumps(res), flush=True)
 
 
+def spawn_ranks(args) -> int:
+    """`bench.py --gpus N` outside torchrun: re-launch this script as N ranks (one process per
+    GPU, torch.distributed.run on 127.0.0.1); rank 0 prints the JSON line."""
+    import socket
+
+    env = dict(os.environ)
+    if args.share_gpu:
+        env["SKV_BENCH_SHARE_GPU"] = "1"
+        env.setdefault("SKV_BENCH_BACKEND", "gloo")
+    elif args.impl == "ours":
+        try:
+            import torch
+            have = torch.cuda.device_count()
+        except Exception:  # noqa: BLE001
+            have = 0
+        if have < args.gpus:
+            print(json.dumps({"error": f"--gpus {args.gpus} but this box has {have} GPU(s); use --share-gpu "
+                                       "for a functional dry run"}), flush=True)
+            return 2
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -1094,11 +1205,23 @@ def main():
                     help="CPU-baseline sample duration (bounded sample of the workload)")
     ap.add_argument("--cpu-requests", dest="cpu_requests", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", dest="no_cpu_baseline", action="store_true")
+    ap.add_argument("--no-tp-group", dest="no_tp_group", action="store_true",
+                    help="N>1: run config-2 replicas only (no head-sharded 70B service)")
+    ap.add_argument("--share-gpu", dest="share_gpu", action="store_true",
+                    help="dry run of the N-rank path on a box with fewer GPUs: every rank on GPU 0, gloo "
+                         "(functional only; the numbers are meaningless)")
     ap.add_argument("--no-parity", dest="no_parity", action="store_true",
                     help="skip the post-timing oracle check of a sample of the measured launch")
     ap.add_argument("--no-graph", dest="no_graph", action="store_true",
                     help="eager launches instead of a CUDA graph per step")
     args = ap.parse_args()
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is not None and int(env_world) != args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={env_world}: launch one rank per GPU "
+                                   f"(torchrun --nproc-per-node {args.gpus}) or drop --gpus"}), flush=True)
+        sys.exit(2)
+    if env_world is None and args.gpus > 1:
+        sys.exit(spawn_ranks(args))
     if args.impl == "reference":
         run_reference(args)
     elif args.workload == "config3":

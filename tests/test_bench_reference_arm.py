@@ -22,3 +22,25 @@ def test_reference_arm_prints_contract_line():
         assert key in d, key
     assert d["value"] > 0 and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+
+
+def test_gpus_mismatch_with_world_size_is_refused():
+    env = dict(os.environ, WORLD_SIZE="3", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--impl", "reference"],
+                         capture_output=True, text=True, timeout=120, cwd=ROOT, env=env)
+    assert out.returncode == 2
+    assert "WORLD_SIZE=3" in json.loads(out.stdout.strip().splitlines()[-1])["error"]
+
+
+def test_gpus_n_spawns_ranks_without_torchrun():
+    """`bench.py --gpus 2` with no WORLD_SIZE re-launches itself as 2 ranks (torch.distributed.run
+    on 127.0.0.1); rank 0 alone prints the reference arm's line."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--impl", "reference",
+                          "--steps", "1", "--warmup", "0", "--cpu-requests", "1", "--ctx", "256"],
+                         capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2

@@ -31,3 +31,12 @@ def test_bench_decode_small():
 def test_bench_prefill_small():
     d = _run("--workload", "prefill", "--requests", "1", "--ctx", "1024", "--chunk", "256")
     assert d["value"] > 0 and d["roofline"]["bound"] == "tensor" and d["gpu_launches"] == 2
+
+
+def test_bench_gpus2_dry_run_without_torchrun():
+    """`bench.py --gpus 2 --share-gpu` on a 1-GPU box: spawns 2 ranks itself, both on GPU 0
+    with gloo; the line reports n_gpus 2 and the head-sharded service's AllReduce."""
+    d = _run("--gpus", "2", "--share-gpu", "--workload", "config2", "--requests", "4", "--ctx", "256")
+    assert d["n_gpus"] == 2 and d["value"] > 0
+    assert d["allreduce"]["group_size"] == 2 and d["allreduce"]["per_layer_ms_rank0"] > 0
+    assert d["parity"]["ok"], d["parity"]
