@@ -26,9 +26,9 @@ namespace skv {
 
 namespace {
 
-constexpr int kD = 128;                       // head_dim handled by the kernels
 constexpr int kTpb = 16;                      // tokens per native block
-constexpr int kTile = 2 * kTpb * kD * 2;      // K + V tile bytes (8 KiB)
+constexpr int kTile = 8192;                   // ring slot: a d=128 K|V run, a d=64 run, or half a d=256 run
+constexpr int kWsRow = 256;                   // floats per partial-output slot (any head_dim <= 256)
 #ifndef SKV_DEC_WARPS
 #define SKV_DEC_WARPS 8
 #endif
@@ -157,95 +157,124 @@ struct MixFma<__nv_bfloat16> {
   }
 };
 
-// Sum of 8 per-lane partials over the 16 lanes of a half-warp, scattered so lane
-// (c = lane&15) ends up with the total of index (c>>1)&7 (8 shuffles, not 32).
-__device__ __forceinline__ float reduce_scatter16(const float (&v)[8], int lane) {
-  const bool b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
-  float v4[4];
+// Lane geometry of a 16-token K/V tile for head dim D.  A lane always holds 8 dims (16 B) of a
+// token row: CPR = D/8 lanes cover one row, so a warp pass reads TPP = 32/CPR tokens and a
+// tile takes NP = 16/TPP passes.  D = 64, 128: one ring unit = the native block's whole K|V
+// run of this (layer, kv head) (64*D B: 4 / 8 KiB).  D = 256: the 16 KiB run is two ring
+// units of 8 KiB (K, then V), each read by all 32 lanes, one token per pass.
+template <int D>
+struct Lanes {
+  static constexpr int CPR = D / 8;
+  static constexpr int TPP = CPR >= 32 ? 1 : 32 / CPR;
+  static constexpr int NP = kTpb / TPP;
+  static constexpr int ROW = 2 * D;                                    // bytes of one token row
+  static constexpr int USH = D == 256 ? 1 : 0;                         // log2(ring units per block)
+  static constexpr int UNIT = D == 256 ? kTpb * ROW : 2 * kTpb * ROW;  // bytes of one ring unit
+  static_assert(D == 64 || D == 128 || D == 256, "head_dim 64, 128 or 256");
+  static_assert(UNIT <= kTile, "a ring unit must fit a ring slot");
+};
+
+// Sum of W per-lane partials over 2W lanes (xor distances W .. 1), scattered so lane c ends
+// up with the total of index (c >> 1) & (W - 1) (2W - 1 shuffles, not W * log2(2W)).
+template <int W>
+__device__ __forceinline__ float reduce_scatter(float (&v)[W], int lane) {
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const float send = b3 ? v[k] : v[k + 4];
-    const float keep = b3 ? v[k + 4] : v[k];
-    v4[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-  }
-  float v2[2];
+  for (int w = W; w >= 2; w >>= 1) {
+    const bool hi = lane & w;
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const float send = b2 ? v4[k] : v4[k + 2];
-    const float keep = b2 ? v4[k + 2] : v4[k];
-    v2[k] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    for (int k = 0; k < w / 2; ++k) {
+      const float send = hi ? v[k] : v[k + w / 2];
+      const float keep = hi ? v[k + w / 2] : v[k];
+      v[k] = keep + __shfl_xor_sync(0xffffffffu, send, w);
+    }
   }
-  const float send = b1 ? v2[0] : v2[1];
-  const float keep = b1 ? v2[1] : v2[0];
-  float s = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-  s += __shfl_xor_sync(0xffffffffu, s, 1);
-  return s;
+  return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
 }
 
-// One 16-token K/V tile for G query heads sharing a KV head.
-// Lane (c = lane&15, hf = lane>>4) reads dims [8c, 8c+8) of tokens 2i+hf.
-template <typename T, int G, bool PARTIAL>
+// max over the warp (lanes c and c^1 hold the same value)
+__device__ __forceinline__ float warp_max_pairs(float x) {
+  x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, 2));
+  x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, 4));
+  x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, 8));
+  return fmaxf(x, __shfl_xor_sync(0xffffffffu, x, 16));
+}
+
+// q . k over this lane's 8 dims for G heads: packed fp32 FMA (FFMA2), 4 + 1 instructions
+template <int G>
+__device__ __forceinline__ void dot8(const float (&q)[G][8], const float (&kf)[8], float (&out)[G]) {
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    float2 a = __fmul2_rn(make_float2(q[g][0], q[g][1]), make_float2(kf[0], kf[1]));
+#pragma unroll
+    for (int j = 2; j < 8; j += 2) a = __ffma2_rn(make_float2(q[g][j], q[g][j + 1]), make_float2(kf[j], kf[j + 1]), a);
+    out[g] = a.x + a.y;
+  }
+}
+
+// o += p * v over this lane's 8 dims (FFMA2)
+__device__ __forceinline__ void axpy8(float pt, const float (&vf)[8], float (&o)[8]) {
+  const float2 pt2 = make_float2(pt, pt);
+#pragma unroll
+  for (int j = 0; j < 8; j += 2) {
+    const float2 r = __ffma2_rn(pt2, make_float2(vf[j], vf[j + 1]), make_float2(o[j], o[j + 1]));
+    o[j] = r.x;
+    o[j + 1] = r.y;
+  }
+}
+
+__device__ __forceinline__ void scale8(float alpha, float (&o)[8]) {
+  const float2 a2 = make_float2(alpha, alpha);
+#pragma unroll
+  for (int j = 0; j < 8; j += 2) {
+    const float2 r = __fmul2_rn(make_float2(o[j], o[j + 1]), a2);
+    o[j] = r.x;
+    o[j + 1] = r.y;
+  }
+}
+
+// One 16-token K/V tile (D = 64 / 128) for G query heads sharing a KV head (GQA path: K/V
+// converted once, reused for the G heads).  Lane (c = lane % CPR, hf = lane / CPR) reads
+// dims [8c, 8c+8) of tokens TPP*i + hf.
+template <typename T, int G, int D, bool PARTIAL>
 __device__ __forceinline__ void consume_tile(const char* tile, int lane, int valid,
                                              const float (&q)[G][8], float (&o)[G][8],
                                              float (&mx)[G], float (&l)[G]) {
-  const int c = lane & 15, hf = lane >> 4;
-  float part[G][8];
+  using LG = Lanes<D>;
+  const int c = lane % LG::CPR, hf = lane / LG::CPR;
+  float part[G][LG::NP];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const uint4 raw = *reinterpret_cast<const uint4*>(tile + (2 * i + hf) * (kD * 2) + c * 16);
+  for (int i = 0; i < LG::NP; ++i) {
+    const uint4 raw = *reinterpret_cast<const uint4*>(tile + (LG::TPP * i + hf) * LG::ROW + c * 16);
     float kf[8];
     Cvt<T>::to_f32(raw, kf);
+    float d[G];
+    dot8<G>(q, kf, d);
 #pragma unroll
-    for (int g = 0; g < G; ++g) {  // packed fp32 FMA (FFMA2): 4 + 1 instructions per 8 dims
-      float2 a = __fmul2_rn(make_float2(q[g][0], q[g][1]), make_float2(kf[0], kf[1]));
-#pragma unroll
-      for (int j = 2; j < 8; j += 2) a = __ffma2_rn(make_float2(q[g][j], q[g][j + 1]), make_float2(kf[j], kf[j + 1]), a);
-      part[g][i] = a.x + a.y;
-    }
+    for (int g = 0; g < G; ++g) part[g][i] = d[g];
   }
-  const int tok = 2 * ((c >> 1) & 7) + hf;
+  const int tok = LG::TPP * ((c >> 1) & (LG::NP - 1)) + hf;
   float p[G];
 #pragma unroll
   for (int g = 0; g < G; ++g) {
-    float s = reduce_scatter16(part[g], lane);
+    float s = reduce_scatter<LG::NP>(part[g], lane);
     if (tok >= valid) s = -INFINITY;
-    float bm = s;
-    bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 2));
-    bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 4));
-    bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 8));
-    bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 16));
-    const float mnew = fmaxf(mx[g], bm);
+    const float mnew = fmaxf(mx[g], warp_max_pairs(s));
     const float alpha = exp2f(mx[g] - mnew);
     p[g] = exp2f(s - mnew);
     l[g] = l[g] * alpha + p[g];
-    const float2 a2 = make_float2(alpha, alpha);
-#pragma unroll
-    for (int j = 0; j < 8; j += 2) {
-      const float2 r = __fmul2_rn(make_float2(o[g][j], o[g][j + 1]), a2);
-      o[g][j] = r.x;
-      o[g][j + 1] = r.y;
-    }
+    scale8(alpha, o[g]);
     mx[g] = mnew;
   }
-  const char* vt = tile + kTpb * kD * 2;
+  const char* vt = tile + kTpb * LG::ROW;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    uint4 raw = *reinterpret_cast<const uint4*>(vt + (2 * i + hf) * (kD * 2) + c * 16);
-    if (PARTIAL && 2 * i + hf >= valid) raw = make_uint4(0u, 0u, 0u, 0u);  // unwritten slots may hold NaN
+  for (int i = 0; i < LG::NP; ++i) {
+    uint4 raw = *reinterpret_cast<const uint4*>(vt + (LG::TPP * i + hf) * LG::ROW + c * 16);
+    if (PARTIAL && LG::TPP * i + hf >= valid) raw = make_uint4(0u, 0u, 0u, 0u);  // unwritten slots may hold NaN
     float vf[8];
     Cvt<T>::to_f32(raw, vf);
-    const int src = (hf << 4) | (i << 1);
+    const int src = hf * LG::CPR + 2 * i;
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const float pt = __shfl_sync(0xffffffffu, p[g], src);
-      const float2 pt2 = make_float2(pt, pt);
-#pragma unroll
-      for (int j = 0; j < 8; j += 2) {
-        const float2 r = __ffma2_rn(pt2, make_float2(vf[j], vf[j + 1]), make_float2(o[g][j], o[g][j + 1]));
-        o[g][j] = r.x;
-        o[g][j + 1] = r.y;
-      }
-    }
+    for (int g = 0; g < G; ++g) axpy8(__shfl_sync(0xffffffffu, p[g], src), vf, o[g]);
   }
 }
 
@@ -256,62 +285,156 @@ __device__ __forceinline__ const int2* table_row(const DataParams& p, int handle
                    : p.req_table + (size_t)handle * p.cap;
 }
 
-// G = 1 (MHA) variant of consume_tile: q stays in 16-bit (qraw, this lane's 8 dims) and
+// G = 1 (MHA) variant of consume_tile: q stays in 16-bit (qraw, this lane's 8 raw dims) and
 // both dot products run as mixed-precision FMAs (fp32 accumulate, 16-bit operands), so
 // neither K nor V is converted; P is rounded to the 16-bit type for P.V, as the tensor-core
 // prefill does.  About 30 % fewer instructions per tile than the converting path.
-template <typename T, bool PARTIAL>
+template <typename T, int D, bool PARTIAL>
 __device__ __forceinline__ void consume_tile_mha(const char* tile, int lane, int valid, const uint4& qraw,
                                                  float scale_log2, float (&o)[8], float& mx, float& l) {
-  const int c = lane & 15, hf = lane >> 4;
+  using LG = Lanes<D>;
+  const int c = lane % LG::CPR, hf = lane / LG::CPR;
   const unsigned short* qh = reinterpret_cast<const unsigned short*>(&qraw);
-  float part[8];
+  float part[LG::NP];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const uint4 raw = *reinterpret_cast<const uint4*>(tile + (2 * i + hf) * (kD * 2) + c * 16);
+  for (int i = 0; i < LG::NP; ++i) {
+    const uint4 raw = *reinterpret_cast<const uint4*>(tile + (LG::TPP * i + hf) * LG::ROW + c * 16);
     const unsigned short* kh = reinterpret_cast<const unsigned short*>(&raw);
     float a = 0.f;
 #pragma unroll
     for (int j = 0; j < 8; ++j) a = MixFma<T>::f(a, qh[j], kh[j]);
     part[i] = a;
   }
-  const int tok = 2 * ((c >> 1) & 7) + hf;
-  float sc = reduce_scatter16(part, lane) * scale_log2;
+  const int tok = LG::TPP * ((c >> 1) & (LG::NP - 1)) + hf;
+  float sc = reduce_scatter<LG::NP>(part, lane) * scale_log2;
   if (tok >= valid) sc = -INFINITY;
-  float bm = sc;
-  bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 2));
-  bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 4));
-  bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 8));
-  bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, 16));
-  const float mnew = fmaxf(mx, bm);
+  const float mnew = fmaxf(mx, warp_max_pairs(sc));
   const float alpha = exp2f(mx - mnew);
   const float pr = exp2f(sc - mnew);
   l = l * alpha + pr;
-  const float2 a2 = make_float2(alpha, alpha);
-#pragma unroll
-  for (int j = 0; j < 8; j += 2) {
-    const float2 r = __fmul2_rn(make_float2(o[j], o[j + 1]), a2);
-    o[j] = r.x;
-    o[j + 1] = r.y;
-  }
+  scale8(alpha, o);
   mx = mnew;
-  const char* vt = tile + kTpb * kD * 2;
+  const char* vt = tile + kTpb * LG::ROW;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    uint4 raw = *reinterpret_cast<const uint4*>(vt + (2 * i + hf) * (kD * 2) + c * 16);
-    if (PARTIAL && 2 * i + hf >= valid) raw = make_uint4(0u, 0u, 0u, 0u);  // unwritten slots may hold NaN
+  for (int i = 0; i < LG::NP; ++i) {
+    uint4 raw = *reinterpret_cast<const uint4*>(vt + (LG::TPP * i + hf) * LG::ROW + c * 16);
+    if (PARTIAL && LG::TPP * i + hf >= valid) raw = make_uint4(0u, 0u, 0u, 0u);  // unwritten slots may hold NaN
     const unsigned short* vh = reinterpret_cast<const unsigned short*>(&raw);
-    const unsigned short ph = Cvt<T>::one(__shfl_sync(0xffffffffu, pr, (hf << 4) | (i << 1)));
+    const unsigned short ph = Cvt<T>::one(__shfl_sync(0xffffffffu, pr, hf * LG::CPR + 2 * i));
 #pragma unroll
     for (int j = 0; j < 8; ++j) o[j] = MixFma<T>::f(o[j], ph, vh[j]);
   }
 }
 
-// Per-warp producer: walks the same item sequence as the consumer, kStages tiles ahead.
+// D = 256, K unit (16 tokens x 512 B, one token per pass, lane = dims [8*lane, 8*lane+8)):
+// scores of tokens 0-7 and 8-15 as two reduce-scatters of 8 values over 16 lanes plus the
+// other 16 lanes' dims (xor 16), so a lane holds tokens (lane>>1)&7 and 8 + that; then the
+// online-softmax update.  p0 / p1 are the lane's two probabilities.
+template <typename T, int G>
+__device__ __forceinline__ void scores_256(const char* kt, int lane, int valid, const float (&q)[G][8],
+                                           float (&o)[G][8], float (&mx)[G], float (&l)[G], float (&p0)[G],
+                                           float (&p1)[G]) {
+  float s[2][G];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    float part[G][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint4 raw = *reinterpret_cast<const uint4*>(kt + (8 * h + i) * 512 + lane * 16);
+      float kf[8];
+      Cvt<T>::to_f32(raw, kf);
+      float d[G];
+      dot8<G>(q, kf, d);
+#pragma unroll
+      for (int g = 0; g < G; ++g) part[g][i] = d[g];
+    }
+    const int tok = 8 * h + ((lane >> 1) & 7);
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      float x = reduce_scatter<8>(part[g], lane);
+      x += __shfl_xor_sync(0xffffffffu, x, 16);
+      s[h][g] = tok >= valid ? -INFINITY : x;
+    }
+  }
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const float mnew = fmaxf(mx[g], warp_max_pairs(fmaxf(s[0][g], s[1][g])));
+    const float alpha = exp2f(mx[g] - mnew);
+    p0[g] = exp2f(s[0][g] - mnew);
+    p1[g] = exp2f(s[1][g] - mnew);
+    l[g] = l[g] * alpha + (p0[g] + p1[g]);
+    scale8(alpha, o[g]);
+    mx[g] = mnew;
+  }
+}
+
+// D = 256, V unit: o += p . V; token i's probability sits in lane 2*(i&7) (p0 for i < 8, p1 after)
+template <typename T, int G, bool PARTIAL>
+__device__ __forceinline__ void pv_256(const char* vt, int lane, int valid, const float (&p0)[G],
+                                       const float (&p1)[G], float (&o)[G][8]) {
+#pragma unroll
+  for (int i = 0; i < kTpb; ++i) {
+    uint4 raw = *reinterpret_cast<const uint4*>(vt + i * 512 + lane * 16);
+    if (PARTIAL && i >= valid) raw = make_uint4(0u, 0u, 0u, 0u);  // unwritten slots may hold NaN
+    float vf[8];
+    Cvt<T>::to_f32(raw, vf);
+#pragma unroll
+    for (int g = 0; g < G; ++g) axpy8(__shfl_sync(0xffffffffu, i < 8 ? p0[g] : p1[g], 2 * (i & 7)), vf, o[g]);
+  }
+}
+
+// D = 256 MHA variants (16-bit q, mixed-precision FMAs, P rounded to 16 bits for P.V)
+template <typename T>
+__device__ __forceinline__ void scores_256_mha(const char* kt, int lane, int valid, const uint4& qraw,
+                                               float scale_log2, float (&o)[8], float& mx, float& l, float& p0,
+                                               float& p1) {
+  const unsigned short* qh = reinterpret_cast<const unsigned short*>(&qraw);
+  float s[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    float part[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint4 raw = *reinterpret_cast<const uint4*>(kt + (8 * h + i) * 512 + lane * 16);
+      const unsigned short* kh = reinterpret_cast<const unsigned short*>(&raw);
+      float a = 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) a = MixFma<T>::f(a, qh[j], kh[j]);
+      part[i] = a;
+    }
+    float x = reduce_scatter<8>(part, lane);
+    x = (x + __shfl_xor_sync(0xffffffffu, x, 16)) * scale_log2;
+    s[h] = 8 * h + ((lane >> 1) & 7) >= valid ? -INFINITY : x;
+  }
+  const float mnew = fmaxf(mx, warp_max_pairs(fmaxf(s[0], s[1])));
+  const float alpha = exp2f(mx - mnew);
+  p0 = exp2f(s[0] - mnew);
+  p1 = exp2f(s[1] - mnew);
+  l = l * alpha + (p0 + p1);
+  scale8(alpha, o);
+  mx = mnew;
+}
+
+template <typename T, bool PARTIAL>
+__device__ __forceinline__ void pv_256_mha(const char* vt, int lane, int valid, float p0, float p1, float (&o)[8]) {
+#pragma unroll
+  for (int i = 0; i < kTpb; ++i) {
+    uint4 raw = *reinterpret_cast<const uint4*>(vt + i * 512 + lane * 16);
+    if (PARTIAL && i >= valid) raw = make_uint4(0u, 0u, 0u, 0u);  // unwritten slots may hold NaN
+    const unsigned short* vh = reinterpret_cast<const unsigned short*>(&raw);
+    const unsigned short ph = Cvt<T>::one(__shfl_sync(0xffffffffu, i < 8 ? p0 : p1, 2 * (i & 7)));
+#pragma unroll
+    for (int j = 0; j < 8; ++j) o[j] = MixFma<T>::f(o[j], ph, vh[j]);
+  }
+}
+
+// Per-warp producer: walks the same item sequence as the consumer, kStages ring units ahead.
 struct Producer {
   int idx;         // current item, -1 before the first
-  int blk, bend;   // next block to issue / end (native block indices)
-  int cbase;       // first block of the cached table chunk (-1 = none)
+  int blk, bend;   // next ring unit to issue / end (unit = native block << ush, + K/V half)
+  int ush;         // log2(ring units per native block) of the current item (1 for D = 256)
+  int ubytes;      // bytes of one ring unit of the current item
+  int cbase;       // first native block of the cached table chunk (-1 = none)
   int2 tc;         // lane-held table chunk entry
   const int2* row;
   const char* base;  // pool + layer/head offset of the current item
@@ -347,27 +470,30 @@ __device__ __forceinline__ bool produce_one(const DataParams& p, Producer& P, co
     __syncwarp();
     P.pushed++;
     P.idx = idx;
-    P.blk = it.z / kTpb;
-    P.bend = (it.w + kTpb - 1) / kTpb;
+    P.ush = g.D == 256 ? 1 : 0;
+    P.ubytes = g.D == 256 ? kTpb * 512 : 64 * g.D;
+    P.blk = (it.z / kTpb) << P.ush;
+    P.bend = ((it.w + kTpb - 1) / kTpb) << P.ush;
     P.row = table_row(p, p.handles[it.x], it.y & 0xffff);
     P.base = p.pool + g.layer_off + (long long)(it.y & 0xffff) * g.head_stride;
     P.nstride = g.native_stride;
     P.cbase = -1;
   }
   if (P.done || P.blk >= P.bend) return false;
-  if (P.cbase < 0 || P.blk - P.cbase >= 32) {
-    P.cbase = P.blk;
-    const int b = P.blk + w.lane;
-    P.tc = b < P.bend ? P.row[b] : make_int2(0, 0);
+  const int blk = P.blk >> P.ush;
+  if (P.cbase < 0 || blk - P.cbase >= 32) {
+    P.cbase = blk;
+    const int b = blk + w.lane;
+    P.tc = b < (P.bend >> P.ush) ? P.row[b] : make_int2(0, 0);
   }
-  const int rel = P.blk - P.cbase;
+  const int rel = blk - P.cbase;
   const int bx = __shfl_sync(0xffffffffu, P.tc.x, rel);
   const int by = __shfl_sync(0xffffffffu, P.tc.y, rel);
   const int stage = P.issued % kStages;
   if (w.lane == 0) {
-    const char* src = P.base + (long long)bx * p.merged_stride + (long long)by * P.nstride;
-    mbar_expect_tx(&w.bars[stage], kTile);
-    bulk_g2s(w.tiles + stage * kTile, src, kTile, &w.bars[stage], w.policy);
+    const char* src = P.base + (long long)bx * p.merged_stride + (long long)by * P.nstride + (P.blk & P.ush) * (kTpb * 512);
+    mbar_expect_tx(&w.bars[stage], P.ubytes);
+    bulk_g2s(w.tiles + stage * kTile, src, P.ubytes, &w.bars[stage], w.policy);
   }
   P.issued++;
   P.blk++;
@@ -380,10 +506,48 @@ __device__ __forceinline__ void fill(const DataParams& p, Producer& P, const War
   }
 }
 
-template <typename T, int G>
+// Waits for the next ring unit of the current item; returns its shared-memory tile.
+__device__ __forceinline__ char* next_unit(const DataParams& p, Producer& P, const WarpCtx& w) {
+  if (P.issued == P.consumed) fill(p, P, w);
+  const int stage = P.consumed % kStages;
+  mbar_wait(&w.bars[stage], (P.consumed / kStages) & 1u);
+  return w.tiles + stage * kTile;
+}
+
+__device__ __forceinline__ void release_unit(const DataParams& p, Producer& P, const WarpCtx& w) {
+  __syncwarp();
+  P.consumed++;
+  fill(p, P, w);
+}
+
+// Fused append (n_new == 1): writes the step's new K (kv 0) and/or V (kv 1) row of token apos
+// into the pool and patches it into the staged unit, which holds the K|V run (D <= 128) or just
+// the K or V half (D = 256).  16 B per lane, as append_kernel.
+template <int D>
+__device__ __forceinline__ void patch_new_token(const DataParams& p, const DataGroup& g, int handle, int head, int rl,
+                                                int b, int apos, char* unit, int kv_first, int kv_last, int lane) {
+  using LG = Lanes<D>;
+  const int2 e = table_row(p, handle, head)[b];
+  char* run = p.pool + g.layer_off + (long long)head * g.head_stride + (long long)e.x * p.merged_stride +
+              (long long)e.y * g.native_stride;
+  for (int ch = lane + kv_first * LG::CPR; ch < (kv_last + 1) * LG::CPR; ch += 32) {
+    const int kv = ch / LG::CPR, c = ch % LG::CPR;
+    const uint4 val = *reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(kv ? g.v : g.k) +
+                                                      ((size_t)rl * g.Hkv + head) * LG::ROW + c * 16);
+    const int off = (apos % kTpb) * LG::ROW + c * 16;
+    *reinterpret_cast<uint4*>(run + kv * (kTpb * LG::ROW) + off) = val;
+    *reinterpret_cast<uint4*>(unit + (D == 256 ? 0 : kv * (kTpb * LG::ROW)) + off) = val;
+  }
+  // the slot is refilled by TMA (async proxy) later: order this generic write first
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+}
+
+template <typename T, int G, int D>
 __device__ __forceinline__ void process_item(const DataParams& p, Producer& P, const WarpCtx& w,
                                              const int4 it, int idx) {
-  const int lane = w.lane, c = lane & 15, hf = lane >> 4;
+  using LG = Lanes<D>;
+  const int lane = w.lane, c = lane % LG::CPR, hf = lane / LG::CPR;
   const int grp = it.y >> 16, head = it.y & 0xffff;
   const DataGroup& g = p.g[grp];
   const int rl = it.x - g.req_begin;
@@ -391,70 +555,72 @@ __device__ __forceinline__ void process_item(const DataParams& p, Producer& P, c
   uint4 qraw = make_uint4(0u, 0u, 0u, 0u);  // G = 1: this lane's 8 raw query dims
 #pragma unroll
   for (int gg = 0; gg < G; ++gg) {
-    const T* qp = reinterpret_cast<const T*>(g.q) + ((size_t)rl * g.Hq + head * G + gg) * kD;
+    const T* qp = reinterpret_cast<const T*>(g.q) + ((size_t)rl * g.Hq + head * G + gg) * D;
     const uint4 raw = *reinterpret_cast<const uint4*>(qp + c * 8);
     if (G == 1) qraw = raw;
     Cvt<T>::to_f32(raw, q[gg]);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      q[gg][j] *= p.scale_log2;
+      q[gg][j] *= g.scale_log2;
       o[gg][j] = 0.f;
     }
     mx[gg] = -INFINITY;
     l[gg] = 0.f;
   }
-  // fused append (n_new == 1): the item holding position ctx-1 writes the step's new
-  // K/V token into the pool and patches it into the staged tile before attending
+  // fused append (n_new == 1): the item holding position ctx-1 writes the step's new K/V
+  // token into the pool and patches it into the staged unit(s) before attending
   int apos = -1;
+  const int handle = p.handles[it.x];
   if (p.n_new == 1 && g.k != nullptr) {
-    const int pos = p.req_tokens[p.handles[it.x]] - 1;
+    const int pos = p.req_tokens[handle] - 1;
     if (pos >= it.z && pos < it.w) apos = pos;
   }
   const int b0 = it.z / kTpb, b1 = (it.w + kTpb - 1) / kTpb;
   for (int b = b0; b < b1; ++b) {
-    if (P.issued == P.consumed) fill(p, P, w);
-    const int stage = P.consumed % kStages;
-    const uint32_t phase = (P.consumed / kStages) & 1u;
-    mbar_wait(&w.bars[stage], phase);
-    if (apos >= 0 && b == apos / kTpb) {
-      // lanes 0-15 move the K row, 16-31 the V row (16 B each), as append_kernel
-      const int kv = lane >> 4;
-      const int2 e = table_row(p, p.handles[it.x], head)[b];
-      const uint4 val = *reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(kv ? g.v : g.k) +
-                                                        ((size_t)rl * g.Hkv + head) * (kD * 2) + c * 16);
-      const int off = kv * (kTpb * kD * 2) + (apos % kTpb) * (kD * 2) + c * 16;
-      *reinterpret_cast<uint4*>(p.pool + g.layer_off + (long long)head * g.head_stride +
-                                (long long)e.x * p.merged_stride + (long long)e.y * g.native_stride + off) = val;
-      *reinterpret_cast<uint4*>(w.tiles + stage * kTile + off) = val;
-      // the slot is refilled by TMA (async proxy) later: order this generic write first
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-    }
     const int valid = min(kTpb, it.w - b * kTpb);
-    if constexpr (G == 1) {
-      if (valid == kTpb)
-        consume_tile_mha<T, false>(w.tiles + stage * kTile, lane, valid, qraw, p.scale_log2, o[0], mx[0], l[0]);
-      else
-        consume_tile_mha<T, true>(w.tiles + stage * kTile, lane, valid, qraw, p.scale_log2, o[0], mx[0], l[0]);
+    const bool patch = apos >= 0 && b == apos / kTpb;
+    char* unit = next_unit(p, P, w);
+    if constexpr (D != 256) {
+      if (patch) patch_new_token<D>(p, g, handle, head, rl, b, apos, unit, 0, 1, lane);
+      if constexpr (G == 1) {
+        if (valid == kTpb) consume_tile_mha<T, D, false>(unit, lane, valid, qraw, g.scale_log2, o[0], mx[0], l[0]);
+        else consume_tile_mha<T, D, true>(unit, lane, valid, qraw, g.scale_log2, o[0], mx[0], l[0]);
+      } else {
+        if (valid == kTpb) consume_tile<T, G, D, false>(unit, lane, valid, q, o, mx, l);
+        else consume_tile<T, G, D, true>(unit, lane, valid, q, o, mx, l);
+      }
+      release_unit(p, P, w);
     } else {
-      if (valid == kTpb) consume_tile<T, G, false>(w.tiles + stage * kTile, lane, valid, q, o, mx, l);
-      else consume_tile<T, G, true>(w.tiles + stage * kTile, lane, valid, q, o, mx, l);
+      float p0[G], p1[G];
+      if (patch) patch_new_token<D>(p, g, handle, head, rl, b, apos, unit, 0, 0, lane);
+      if constexpr (G == 1) scores_256_mha<T>(unit, lane, valid, qraw, g.scale_log2, o[0], mx[0], l[0], p0[0], p1[0]);
+      else scores_256<T, G>(unit, lane, valid, q, o, mx, l, p0, p1);
+      release_unit(p, P, w);
+      unit = next_unit(p, P, w);
+      if (patch) patch_new_token<D>(p, g, handle, head, rl, b, apos, unit, 1, 1, lane);
+      if constexpr (G == 1) {
+        if (valid == kTpb) pv_256_mha<T, false>(unit, lane, valid, p0[0], p1[0], o[0]);
+        else pv_256_mha<T, true>(unit, lane, valid, p0[0], p1[0], o[0]);
+      } else {
+        if (valid == kTpb) pv_256<T, G, false>(unit, lane, valid, p0, p1, o);
+        else pv_256<T, G, true>(unit, lane, valid, p0, p1, o);
+      }
+      release_unit(p, P, w);
     }
-    __syncwarp();
-    P.consumed++;
-    fill(p, P, w);
   }
-  // finalize: l over the 16 distinct token lanes, o over the two token halves
+  // finalize: l over the lanes holding distinct tokens, o over the TPP token lanes
 #pragma unroll
   for (int gg = 0; gg < G; ++gg) {
     float s = l[gg];
     s += __shfl_xor_sync(0xffffffffu, s, 2);
     s += __shfl_xor_sync(0xffffffffu, s, 4);
     s += __shfl_xor_sync(0xffffffffu, s, 8);
-    s += __shfl_xor_sync(0xffffffffu, s, 16);
+    if (D != 256) s += __shfl_xor_sync(0xffffffffu, s, 16);  // D = 256: lanes c, c^16 hold the same tokens
     l[gg] = s;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) o[gg][j] += __shfl_xor_sync(0xffffffffu, o[gg][j], 16);
+    for (int x = LG::CPR; x < 32; x <<= 1)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[gg][j] += __shfl_xor_sync(0xffffffffu, o[gg][j], x);
   }
   const int4 x = p.itemx[idx];  // {pieces, partial-slot base, piece, arrival index}
   const int ns = x.x;
@@ -466,7 +632,7 @@ __device__ __forceinline__ void process_item(const DataParams& p, Producer& P, c
         float r[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) r[j] = o[gg][j] * inv;
-        T* op = reinterpret_cast<T*>(g.out) + ((size_t)rl * g.Hq + head * G + gg) * kD + c * 8;
+        T* op = reinterpret_cast<T*>(g.out) + ((size_t)rl * g.Hq + head * G + gg) * D + c * 8;
         *reinterpret_cast<uint4*>(op) = Cvt<T>::from_f32(r);
       }
     }
@@ -478,7 +644,7 @@ __device__ __forceinline__ void process_item(const DataParams& p, Producer& P, c
   for (int gg = 0; gg < G; ++gg) {
     const size_t slot = (size_t)x.y + (size_t)x.z * G + gg;
     if (hf == 0) {
-      float4* dst = reinterpret_cast<float4*>(p.ws_o + slot * kD + c * 8);
+      float4* dst = reinterpret_cast<float4*>(p.ws_o + slot * kWsRow + c * 8);
       __stcg(dst, make_float4(o[gg][0], o[gg][1], o[gg][2], o[gg][3]));
       __stcg(dst + 1, make_float4(o[gg][4], o[gg][5], o[gg][6], o[gg][7]));
     }
@@ -499,42 +665,56 @@ __device__ __forceinline__ void process_item(const DataParams& p, Producer& P, c
     for (int s = lane; s < ns; s += 32) M = fmaxf(M, __ldcg(p.ws_ml + x.y + (size_t)s * G + gg).x);
 #pragma unroll
     for (int o2 = 16; o2 >= 1; o2 >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o2));
-    // lane (c, hf): dims [8c, 8c+8) over pieces hf, hf+2, ...
+    // lane (c, hf): dims [8c, 8c+8) over pieces hf, hf + TPP, ...
     float L = 0.f, acc[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[j] = 0.f;
 #pragma unroll 2
-    for (int s = hf; s < ns; s += 2) {
+    for (int s = hf; s < ns; s += LG::TPP) {
       const size_t slot = (size_t)x.y + (size_t)s * G + gg;
       const float2 ml = __ldcg(p.ws_ml + slot);
-      const float4* src = reinterpret_cast<const float4*>(p.ws_o + slot * kD + c * 8);
-      const float4 a = __ldcg(src), b = __ldcg(src + 1);
+      const float4* src = reinterpret_cast<const float4*>(p.ws_o + slot * kWsRow + c * 8);
+      const float4 a = __ldcg(src), bb = __ldcg(src + 1);
       const float wgt = ml.y > 0.f ? exp2f(ml.x - M) : 0.f;
       L += ml.y * wgt;
       acc[0] += a.x * wgt;
       acc[1] += a.y * wgt;
       acc[2] += a.z * wgt;
       acc[3] += a.w * wgt;
-      acc[4] += b.x * wgt;
-      acc[5] += b.y * wgt;
-      acc[6] += b.z * wgt;
-      acc[7] += b.w * wgt;
+      acc[4] += bb.x * wgt;
+      acc[5] += bb.y * wgt;
+      acc[6] += bb.z * wgt;
+      acc[7] += bb.w * wgt;
     }
-    L += __shfl_xor_sync(0xffffffffu, L, 16);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], 16);
+    for (int xo = LG::CPR; xo < 32; xo <<= 1) {
+      L += __shfl_xor_sync(0xffffffffu, L, xo);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], xo);
+    }
     if (hf == 0) {
       const float inv = L > 0.f ? 1.f / L : 0.f;
 #pragma unroll
       for (int j = 0; j < 8; ++j) acc[j] *= inv;
-      T* op = reinterpret_cast<T*>(g.out) + ((size_t)rl * g.Hq + head * G + gg) * kD + c * 8;
+      T* op = reinterpret_cast<T*>(g.out) + ((size_t)rl * g.Hq + head * G + gg) * D + c * 8;
       *reinterpret_cast<uint4*>(op) = Cvt<T>::from_f32(acc);
     }
   }
   if (lane == 0) p.arrive[x.w] = 0;  // ready for the launch after next (same counter set)
 }
 
-template <typename T, int MAXG>
+template <typename T, int MAXG, int D>
+__device__ __forceinline__ void run_item(const DataParams& p, Producer& P, const WarpCtx& w, const int4 it, int idx,
+                                         int G) {
+  if (G == 1) process_item<T, 1, D>(p, P, w, it, idx);
+  else if (MAXG >= 2 && G == 2) process_item<T, (MAXG >= 2 ? 2 : 1), D>(p, P, w, it, idx);
+  else if (MAXG >= 4 && G == 4) process_item<T, (MAXG >= 4 ? 4 : 1), D>(p, P, w, it, idx);
+  else if (MAXG >= 8 && G == 8) process_item<T, (MAXG >= 8 ? 8 : 1), D>(p, P, w, it, idx);
+}
+
+// DMASK: head dims present in the launch (1: 64, 2: 128, 4: 256); a d = 128-only launch
+// compiles just that path.
+template <typename T, int MAXG, int DMASK>
 __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const __grid_constant__ DataParams p) {
   extern __shared__ __align__(128) char smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -556,6 +736,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const __grid_con
   Producer P;
   P.idx = -1;
   P.blk = P.bend = 0;
+  P.ush = 0;
+  P.ubytes = kTile;
   P.cbase = -1;
   P.tc = make_int2(0, 0);
   P.row = nullptr;
@@ -565,7 +747,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const __grid_con
   P.pushed = P.popped = 0;
   P.issued = P.consumed = 0;
   // Everything before pdl_wait() overlaps the previous launch's tail.  With prefetch the
-  // first kStages K/V tiles of this warp are already in flight: the cache bytes of this
+  // first kStages K/V units of this warp are already in flight: the cache bytes of this
   // layer do not depend on the previous launch (see DataParams::prefetch).
   if (p.prefetch) {
     w.n_items = *p.n_items;
@@ -587,11 +769,23 @@ __global__ void __launch_bounds__(kWarps * 32, 1) decode_kernel(const __grid_con
     P.popped++;
     ++n_done;
     const int4 it = p.items[idx];
-    const int G = p.g[it.y >> 16].G;
-    if (G == 1) process_item<T, 1>(p, P, w, it, idx);
-    else if (MAXG >= 2 && G == 2) process_item<T, (MAXG >= 2 ? 2 : 1)>(p, P, w, it, idx);
-    else if (MAXG >= 4 && G == 4) process_item<T, (MAXG >= 4 ? 4 : 1)>(p, P, w, it, idx);
-    else if (MAXG >= 8 && G == 8) process_item<T, (MAXG >= 8 ? 8 : 1)>(p, P, w, it, idx);
+    const DataGroup& gi = p.g[it.y >> 16];
+    const int G = gi.G;
+    if constexpr ((DMASK & 2) != 0) {
+      if (DMASK == 2 || gi.D == 128) {
+        run_item<T, MAXG, 128>(p, P, w, it, idx, G);
+        continue;
+      }
+    }
+    if constexpr ((DMASK & 1) != 0) {
+      if (gi.D == 64) {
+        run_item<T, MAXG, 64>(p, P, w, it, idx, G);
+        continue;
+      }
+    }
+    if constexpr ((DMASK & 4) != 0) {
+      if (gi.D == 256) run_item<T, MAXG, 256>(p, P, w, it, idx, G);
+    }
   }
   if (p.trace && lane == 0) {
     unsigned long long* t = p.trace + ((size_t)blockIdx.x * kWarps + wid) * 4;
@@ -796,13 +990,16 @@ __global__ void append_kernel(const __grid_constant__ DataParams p) {
   const int pos = p.req_tokens[handle] - p.n_new + i;
   if (pos < 0) return;
   const int2 e = table_row(p, handle, h)[pos / kTpb];
-  const int kv = lane >> 4, c = lane & 15;
-  char* dst = p.pool + (long long)e.x * p.merged_stride + (long long)e.y * g.native_stride + g.layer_off +
-              (long long)h * g.head_stride + kv * (kTpb * kD * 2) + (pos % kTpb) * (kD * 2) + c * 16;
+  const int row = 2 * g.D, cpr = g.D / 8;  // bytes of a token row, 16-B chunks per row
+  char* run = p.pool + (long long)e.x * p.merged_stride + (long long)e.y * g.native_stride + g.layer_off +
+              (long long)h * g.head_stride + (pos % kTpb) * row;
   const int rl = r - g.req_begin;
-  const char* src = reinterpret_cast<const char*>(kv ? g.v : g.k) +
-                    (((size_t)rl * p.n_new + i) * g.Hkv + h) * (kD * 2) + c * 16;
-  *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(src);
+  const size_t src_row = (((size_t)rl * p.n_new + i) * g.Hkv + h) * row;
+  for (int ch = lane; ch < 2 * cpr; ch += 32) {  // K row then V row, 16 B per lane
+    const int kv = ch >= cpr, c = ch - kv * cpr;
+    const char* src = reinterpret_cast<const char*>(kv ? g.v : g.k) + src_row + c * 16;
+    *reinterpret_cast<uint4*>(run + kv * (kTpb * row) + c * 16) = *reinterpret_cast<const uint4*>(src);
+  }
 }
 
 __device__ __forceinline__ float synth_u(unsigned long long seed, unsigned long long i) {
@@ -848,12 +1045,20 @@ void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cu
   cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
-template <typename T, int MAXG>
+template <typename T, int MAXG, int DMASK>
 void launch_decode_t(const DataParams& p, int grid, cudaStream_t s) {
   const int smem = kWarps * kStages * kTile + kWarps * kStages * 8 + kWarps * kRing * 4;
   static std::atomic<uint64_t> attr{0};
-  ensure_smem_attr(decode_kernel<T, MAXG>, smem, attr);
-  launch_pdl(decode_kernel<T, MAXG>, dim3(grid), dim3(kWarps * 32), smem, s, p);
+  ensure_smem_attr(decode_kernel<T, MAXG, DMASK>, smem, attr);
+  launch_pdl(decode_kernel<T, MAXG, DMASK>, dim3(grid), dim3(kWarps * 32), smem, s, p);
+}
+
+template <typename T, int DMASK>
+void launch_decode_g(const DataParams& p, int max_g, int grid, cudaStream_t s) {
+  if (max_g <= 1) launch_decode_t<T, 1, DMASK>(p, grid, s);
+  else if (max_g <= 2) launch_decode_t<T, 2, DMASK>(p, grid, s);
+  else if (max_g <= 4) launch_decode_t<T, 4, DMASK>(p, grid, s);
+  else launch_decode_t<T, 8, DMASK>(p, grid, s);
 }
 
 }  // namespace
@@ -881,16 +1086,14 @@ void launch_decode_plan(const DataParams& p, cudaStream_t s) {
 
 void launch_decode(const DataParams& p, int max_g, int grid, cudaStream_t s) {
   if (grid <= 0) grid = num_sms() * decode_ctas_per_sm();
+  int dmask = 0;
+  for (int i = 0; i < p.ngroups; ++i) dmask |= p.g[i].D == 64 ? 1 : p.g[i].D == 128 ? 2 : 4;
   if (p.dtype == 0) {
-    if (max_g <= 1) launch_decode_t<__half, 1>(p, grid, s);
-    else if (max_g <= 2) launch_decode_t<__half, 2>(p, grid, s);
-    else if (max_g <= 4) launch_decode_t<__half, 4>(p, grid, s);
-    else launch_decode_t<__half, 8>(p, grid, s);
+    if (dmask == 2) launch_decode_g<__half, 2>(p, max_g, grid, s);
+    else launch_decode_g<__half, 7>(p, max_g, grid, s);
   } else {
-    if (max_g <= 1) launch_decode_t<__nv_bfloat16, 1>(p, grid, s);
-    else if (max_g <= 2) launch_decode_t<__nv_bfloat16, 2>(p, grid, s);
-    else if (max_g <= 4) launch_decode_t<__nv_bfloat16, 4>(p, grid, s);
-    else launch_decode_t<__nv_bfloat16, 8>(p, grid, s);
+    if (dmask == 2) launch_decode_g<__nv_bfloat16, 2>(p, max_g, grid, s);
+    else launch_decode_g<__nv_bfloat16, 7>(p, max_g, grid, s);
   }
 }
 

@@ -638,7 +638,8 @@ skv_status skv_pool_create(const skv_model_desc* models, int32_t n, int32_t tpb,
     delete p;
     return fail(nullptr, SKV_ERR_ARG, "more than 64 sub-slots per merged block");
   }
-  p->merged_stride = round_up(p->phys_layers > 0 ? phys_merged : merged, 256);
+  // 1 KiB aligned: every model's K/V rows (2*head_dim B) start on a TMA row boundary
+  p->merged_stride = round_up(p->phys_layers > 0 ? phys_merged : merged, 1024);
   p->R = opts.max_requests > 0 ? opts.max_requests : 4096;
   long long cap = opts.max_blocks_per_request > 0 ? opts.max_blocks_per_request
                                                   : std::min<long long>((long long)pool_blocks * p->maxsub, 4096);
@@ -1074,7 +1075,8 @@ static skv_status make_params(skv_pool* p, skv_batch* b, int layer, skv::DataPar
   dp->merged_stride = p->merged_stride;
   dp->tpb = p->tpb;
   dp->dtype = p->dtype;
-  dp->head_dim = 128;
+  dp->head_dim = 0;  // per group (DataGroup::D); this is the largest in the batch
+  for (int g = 0; g < b->ngroups; ++g) dp->head_dim = std::max(dp->head_dim, p->models[b->gmodel[g]].d);
   dp->layer = layer;
   if (p->split) {  // split scheme: per (request, layer, head) rows of 8 KiB block ids
     dp->req_table = p->split->table;
@@ -1087,9 +1089,12 @@ static skv_status make_params(skv_pool* p, skv_batch* b, int layer, skv::DataPar
   }
   for (int g = 0; g < b->ngroups; ++g) {
     const ModelInfo& mi = p->models[b->gmodel[g]];
-    if (mi.d != 128 || mi.e != 2 || p->tpb != 16)
-      return fail(p, SKV_ERR_ARG, "data path kernels need head_dim 128, 2-byte dtype, tokens_per_block 16");
+    if ((mi.d != 64 && mi.d != 128 && mi.d != 256) || mi.e != 2 || p->tpb != 16)
+      return fail(p, SKV_ERR_ARG, "data path kernels need head_dim 64, 128 or 256, 2-byte dtype, tokens_per_block 16");
+    if (p->split && mi.d != 128) return fail(p, SKV_ERR_ARG, "split scheme: head_dim 128 only (8 KiB split blocks)");
     skv::DataGroup& dg = dp->g[g];
+    dg.D = mi.d;
+    dg.scale_log2 = 1.4426950408889634f / std::sqrt((float)mi.d);
     dg.native_stride = p->split ? 0 : mi.native_stride;
     dg.layer_off = p->split ? 0 : (long long)(layer % mi.phys_L) * mi.layer_stride;
     dg.head_stride = p->split ? 0 : mi.head_stride;
@@ -1149,12 +1154,13 @@ skv_status skv_decode_attention(skv_pool* p, skv_batch* b, const skv_decode_args
     for (int i = 0; i < b->gsize[g]; ++i) {
       const long long ctx = p->req[b->handles[b->gbegin[g] + i]].tokens;
       sum_hkv += dp.g[g].Hkv;
-      work += ctx * dp.g[g].Hkv;
+      work += ctx * dp.g[g].Hkv * dp.g[g].D / 128;  // in d=128 token-head units (bytes / 512)
       max_ctx = std::max(max_ctx, ctx);
     }
   }
-  const float scale = a->softmax_scale > 0.f ? a->softmax_scale : 1.0f / std::sqrt(128.0f);
-  dp.scale_log2 = scale * 1.4426950408889634f;
+  if (a->softmax_scale > 0.f)  // else 1/sqrt(head_dim) of each group (make_params)
+    for (int g = 0; g < b->ngroups; ++g) dp.g[g].scale_log2 = a->softmax_scale * 1.4426950408889634f;
+  dp.scale_log2 = dp.g[0].scale_log2;
   // Work list (plan_kernel): the last n_cut (request, kv head)s get two small trailing
   // pieces (4 per warp slot: enough small work to even out the launch's tail); leading
   // parts are cut to <= split tokens only when there are too few (request, kv head)s to
@@ -1212,7 +1218,7 @@ skv_status skv_decode_attention(skv_pool* p, skv_batch* b, const skv_decode_args
     if (b->d_ws_o) cudaFree(b->d_ws_o);
     if (b->d_ws_ml) cudaFree(b->d_ws_ml);
     b->slots_cap = (size_t)slots * 2;
-    SKV_CUDA(p, cudaMalloc(&b->d_ws_o, b->slots_cap * 128 * sizeof(float)));
+    SKV_CUDA(p, cudaMalloc(&b->d_ws_o, b->slots_cap * 256 * sizeof(float)));  // up to head_dim 256 per slot
     SKV_CUDA(p, cudaMalloc(&b->d_ws_ml, b->slots_cap * sizeof(float2)));
   }
   dp.items = b->d_items;
@@ -1313,8 +1319,11 @@ skv_status skv_prefill_attention(skv_pool* p, skv_batch* b, const skv_prefill_ar
     dp.g[g].q = a->q[g];
     dp.g[g].out = a->out[g];
   }
-  const float scale = a->softmax_scale > 0.f ? a->softmax_scale : 1.0f / std::sqrt(128.0f);
-  dp.scale_log2 = scale * 1.4426950408889634f;
+  for (int g = 0; g < b->ngroups; ++g) {
+    if (p->models[b->gmodel[g]].d != 128) return fail(p, SKV_ERR_ARG, "prefill: head_dim 128 only");
+    if (a->softmax_scale > 0.f) dp.g[g].scale_log2 = a->softmax_scale * 1.4426950408889634f;
+  }
+  dp.scale_log2 = dp.g[0].scale_log2;
   dp.n_new = a->q_len;
   static const int dbg = [] {
     const char* e = getenv("SKV_PREFILL_DBG");

@@ -99,6 +99,8 @@ struct DataGroup {
   long long head_stride;    // bytes between kv heads
   int Hq, Hkv, G, active;   // active = num_layers > layer
   int req_begin, nreq;      // slice of the batch
+  int D;                    // head_dim (64, 128, 256)
+  float scale_log2;         // softmax scale * log2(e) (default 1/sqrt(D))
 };
 
 struct DataParams {
