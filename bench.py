@@ -97,6 +97,9 @@ class Clocks:
 
 
 SERVICES_C1 = [("llama-2-7b", 32, 32, 32), ("llama-2-13b", 40, 40, 40)]
+# (name, layers, kv heads, q heads, head dim): config 2 with four different head-dim / GQA mixes
+SERVICES_MIXED_D = [("llama-3.2-1b", 16, 8, 32, 64), ("llama-3-8b", 32, 8, 32, 128), ("llama-2-13b", 40, 40, 40, 128),
+                    ("gemma-7b", 28, 16, 16, 256)]
 
 
 class Workload:
@@ -106,11 +109,20 @@ class Workload:
     def __init__(self, name, services, ctxs, phys_layers, pool_blocks, desc):
         self.name, self.services, self.ctxs = name, services, ctxs
         self.phys_layers, self.pool_blocks, self.desc = phys_layers, pool_blocks, desc
-        self.nlayers = max(L for _, L, _, _ in services)
+        self.nlayers = max(s[1] for s in services)
+
+
+def hd(s):
+    """head dim of a service tuple (name, layers, kv heads, q heads[, head dim = 128])"""
+    return s[4] if len(s) > 4 else 128
+
+
+def model_specs(P, services):
+    return [P.ModelSpec(s[0], s[1], s[2], hd(s), 2, s[3]) for s in services]
 
 
 def _subs(P, services):
-    specs = [P.ModelSpec(n, L, H, 128, 2, Hq) for n, L, H, Hq in services]
+    specs = model_specs(P, services)
     merged = P.plan_merged_shape(specs)
     return [int(merged // P.native_block_bytes(s)) for s in specs], merged
 
@@ -151,6 +163,14 @@ def make_workload(P, args):
                         f"{pool} merged blocks (~150 GB) filled to ~95 %, split-KV decode")
     nreq = args.requests or 256
     ctx = args.ctx or 2048
+    if args.workload == "config2d":  # config 2 with services of different head dims
+        ctxs = [[ctx] * nreq for _ in SERVICES_MIXED_D]
+        return Workload("config2d", SERVICES_MIXED_D, ctxs, args.phys_layers,
+                        _blocks(P, SERVICES_MIXED_D, ctxs, grow),
+                        f"config2-mixed-head-dims: 4 services (llama-3.2-1b d64 GQA4, llama-3-8b d128 GQA4, "
+                        f"llama-2-13b d128 MHA, gemma-7b d256 MHA) x {nreq} decode requests, ctx {ctx}+, one "
+                        f"unified pool; {args.phys_layers} physical layers per native block, 40 layer-index "
+                        f"launches per step")
     ctxs = [[ctx] * nreq for _ in SERVICES]
     blocks = _blocks(P, SERVICES, ctxs, grow)
     if args.phys_layers == 0:  # SURVEY §8d run (B): every layer stored, requests cut to fit one B200
@@ -189,7 +209,7 @@ def setup(P, torch, args, device, tp_shard=0):
     wl = make_workload(P, args)
     if tp_shard:
         add_tp_shard(P, wl, args, tp_shard)
-    models = [P.ModelSpec(n, L, H, 128, 2, Hq) for n, L, H, Hq in wl.services]
+    models = model_specs(P, wl.services)
     ctx_max = max(max(c) for c in wl.ctxs if c) + args.warmup * 2 + args.steps * 2 + 8
     nreq_total = sum(len(c) for c in wl.ctxs)
     cache = P.UnifiedKvCache(models, 16, 1, wl.pool_blocks, device=device, dtype=P.FP16,
@@ -216,12 +236,10 @@ def setup(P, torch, args, device, tp_shard=0):
     batch = cache.batch(groups)
     g = torch.Generator(device=device).manual_seed(1)
     sizes = [len(ids) for _, ids in groups]
-    q = [torch.randn((n, Hq, 128), generator=g, device=device).half() for n, (_, _, _, Hq) in zip(sizes, wl.services)]
+    q = [torch.randn((n, s[3], hd(s)), generator=g, device=device).half() for n, s in zip(sizes, wl.services)]
     out = [torch.empty_like(x) for x in q]
-    k = [torch.randn((n, 1, H, 128), generator=g, device=device).half() * 0.5 for n, (_, _, H, _) in
-         zip(sizes, wl.services)]
-    v = [torch.randn((n, 1, H, 128), generator=g, device=device).half() * 0.5 for n, (_, _, H, _) in
-         zip(sizes, wl.services)]
+    k = [torch.randn((n, 1, s[2], hd(s)), generator=g, device=device).half() * 0.5 for n, s in zip(sizes, wl.services)]
+    v = [torch.randn((n, 1, s[2], hd(s)), generator=g, device=device).half() * 0.5 for n, s in zip(sizes, wl.services)]
     torch.cuda.synchronize(device)
     return wl, cache, batch, q, out, k, v, stream
 
@@ -689,12 +707,12 @@ def cpu_baseline(cache, batch, q, args, budget_s=None):
             ctx[i] = cache.request_tokens(rid)
         qh = q[m][:len(rows)].view(__import__("torch").int16).cpu().numpy().view(np.uint16)
         work.append((olay, tabs, ctx, qh))
-        nbytes += float(ctx.sum()) * lay.kv_heads * 128 * 2 * 2
+        nbytes += float(ctx.sum()) * lay.kv_heads * lay.head_dim * 2 * 2
     t0 = time.perf_counter()
     reps = 0
     while True:
         for olay, tabs, ctx, qh in work:
-            O.decode_attention(olay, img, 0, tabs, ctx, qh, 1.0 / np.sqrt(128.0), nthreads=cores)
+            O.decode_attention(olay, img, 0, tabs, ctx, qh, 1.0 / np.sqrt(olay.head_dim), nthreads=cores)
         reps += 1
         if time.perf_counter() - t0 > budget_s:
             break
@@ -1073,13 +1091,13 @@ def run_reference(args):
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle_py as O
 
-    services = SERVICES_C1 if args.workload == "config1" else SERVICES
-    ctx_default = {"config1": 512, "config2": 2048, "config3": 2048, "config4": 4096}[args.workload]
+    services = {"config1": SERVICES_C1, "config2d": SERVICES_MIXED_D}.get(args.workload, SERVICES)
+    ctx_default = {"config1": 512, "config4": 4096}.get(args.workload, 2048)
     args.ctx = args.ctx or ctx_default
     cores = os.cpu_count() or 1
     # synthetic host pool for a bounded sample: per service `per` requests at ctx
     per = args.cpu_requests
-    models = [(L, H, 128, 2) for _, L, H, _ in services]
+    models = [(s[1], s[2], hd(s), 2) for s in services]
     allocator = O.RefCache(models, pool=200000) if O.ref_available() else O.OracleCache(models, pool=200000)
     kind = "reference" if O.ref_available() else "port"
     rid = 1
@@ -1099,27 +1117,27 @@ def run_reference(args):
     Lp = args.phys_layers
     stride = 0
     lays = []
-    for m, (name, L, H, Hq) in enumerate(services):
-        layer_stride = H * 2 * 16 * 128 * 2
+    for m, s in enumerate(services):
+        L, H, Hq, d = s[1], s[2], s[3], hd(s)
+        layer_stride = H * 2 * 16 * d * 2
         native = min(Lp, L) * layer_stride
-        lays.append((L, H, Hq, layer_stride, native))
-    sub = [int(merged // (16 * L * 2 * H * 128 * 2)) for _, L, H, _ in services]
+        lays.append((L, H, Hq, layer_stride, native, d))
+    sub = [int(merged // (16 * s[1] * 2 * s[2] * hd(s) * 2)) for s in services]
     stride = max(s * l[4] for s, l in zip(sub, lays))
-    stride = (stride + 255) // 256 * 256
+    stride = (stride + 1023) // 1024 * 1024
     img = rng.integers(0, 0x3C00, size=len(used) * stride // 2, dtype=np.uint16).view(np.uint8)
-    for m, (L, H, Hq, layer_stride, native) in enumerate(lays):
-        olay = O.layout(stride, native, layer_stride, 2 * 16 * 128 * 2, 16 * 128 * 2, 16, 128, H, Hq,
-                        min(Lp, L), 0)
+    for m, (L, H, Hq, layer_stride, native, d) in enumerate(lays):
+        olay = O.layout(stride, native, layer_stride, 2 * 16 * d * 2, 16 * d * 2, 16, d, H, Hq, min(Lp, L), 0)
         tabs = np.array([[(remap[b], s) for b, s in allocator.block_table(i)] for i in ids[m]], np.int32)
         ctx = np.full(len(ids[m]), args.ctx, np.int64)
-        qh = rng.integers(0, 0x3C00, size=(len(ids[m]), Hq, 128), dtype=np.uint16)
+        qh = rng.integers(0, 0x3C00, size=(len(ids[m]), Hq, d), dtype=np.uint16)
         work.append((olay, tabs, ctx, qh))
-        nbytes += float(ctx.sum()) * H * 128 * 2 * 2
+        nbytes += float(ctx.sum()) * H * d * 2 * 2
     # allocator: one decode step of grows for the sampled requests, timed separately
     def one_step():
         t = time.perf_counter()
         for olay, tabs, ctx, qh in work:
-            O.decode_attention(olay, img, 0, tabs, ctx, qh, 1.0 / np.sqrt(128.0), nthreads=cores)
+            O.decode_attention(olay, img, 0, tabs, ctx, qh, 1.0 / np.sqrt(olay.head_dim), nthreads=cores)
         return time.perf_counter() - t
 
     for _ in range(min(args.warmup, 1)):
@@ -1130,7 +1148,7 @@ def run_reference(args):
     # allocator: the decode-step op stream of the workload's request count (every request
     # +1 token per step, 64 steps), replayed through the reference allocator single-threaded
     # (kv_cache.hpp:45); the array is built before the timer starts
-    n_alloc_req = (args.requests or {"config1": 32, "config2": 256, "config3": 64, "config4": 32}[args.workload])
+    n_alloc_req = args.requests or {"config1": 32, "config3": 64, "config4": 32}.get(args.workload, 256)
     nsteps = 64
     acache = (O.RefCache if kind == "reference" else O.OracleCache)(models, pool=400000)
     aops = [(0, 1 + r * len(services) + m, m, args.ctx) for r in range(n_alloc_req) for m in range(len(services))]
@@ -1194,13 +1212,14 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="config2",
-                    choices=["config1", "config2", "config3", "config4", "config5", "prefill"])
+                    choices=["config1", "config2", "config2d", "config3", "config4", "config5", "prefill"])
     ap.add_argument("--chunk", type=int, default=2048, help="prefill workload: chunk length")
     ap.add_argument("--rate", type=float, default=20.0, help="config3 arrival rate (requests/s)")
     ap.add_argument("--pool-gb", dest="pool_gb", type=float, default=100.0, help="config3 pool size")
     ap.add_argument("--requests", type=int, default=0, help="decode requests per service (0 = workload default)")
     ap.add_argument("--ctx", type=int, default=0, help="context length (0 = workload default)")
-    ap.add_argument("--phys-layers", dest="phys_layers", type=int, default=4)
+    ap.add_argument("--phys-layers", dest="phys_layers", type=int, default=None,
+                    help="physical layers per native block (0 = all; default 4, config2d 2)")
     ap.add_argument("--cpu-seconds", dest="cpu_seconds", type=float, default=12.0,
                     help="CPU-baseline sample duration (bounded sample of the workload)")
     ap.add_argument("--cpu-requests", dest="cpu_requests", type=int, default=8)
@@ -1215,6 +1234,8 @@ def main():
     ap.add_argument("--no-graph", dest="no_graph", action="store_true",
                     help="eager launches instead of a CUDA graph per step")
     args = ap.parse_args()
+    if args.phys_layers is None:  # config2d: the d=64 service packs 25 sub-slots, so slice finer to fit
+        args.phys_layers = 2 if args.workload == "config2d" else 4
     env_world = os.environ.get("WORLD_SIZE")
     if env_world is not None and int(env_world) != args.gpus:
         print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={env_world}: launch one rank per GPU "
