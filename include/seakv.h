@@ -196,13 +196,17 @@ typedef struct {
 skv_status skv_append_kv(skv_pool* p, skv_batch* b, const skv_append_args* args, void* stream);
 
 /* Causal chunked-prefill attention: each request's last q_len tokens (positions
- * [tokens-q_len, tokens)) attend to keys [0, pos] already in the pool. */
+ * [tokens-q_len, tokens)) attend to keys [0, pos] already in the pool.  Per-request chunk
+ * lengths: q_lens[nreq] (host array, batch order; NULL = q_len for every request), and then
+ * each group's q / out are packed by request: [sum of its q_lens][Hq/tp][d].  Head dims 64,
+ * 128 and 256 (one tcgen05 launch per head dim present in the batch). */
 typedef struct {
   const void* const* q; /* [host array of n_groups dev ptrs] each [B_g][q_len][Hq/tp][d] */
   void* const* out;     /* same shape */
-  float softmax_scale;
+  float softmax_scale;  /* 0 -> 1/sqrt(head_dim) of each group */
   int32_t layer;
   int32_t q_len;
+  const int32_t* q_lens; /* optional per-request chunk lengths (host, [nreq]) */
 } skv_prefill_args;
 skv_status skv_prefill_attention(skv_pool* p, skv_batch* b, const skv_prefill_args* args,
                                  void* stream);

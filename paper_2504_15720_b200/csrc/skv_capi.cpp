@@ -115,8 +115,11 @@ struct skv_pool {
 
   void* storage = nullptr;
   size_t storage_bytes = 0;
-  alignas(64) CUtensorMap kv_tmap;
-  bool has_tmap = false;
+  alignas(64) CUtensorMap kv_tmap;     // head_dim 128
+  alignas(64) CUtensorMap kv_tmap64;   // head_dim 64 (K boxes)
+  alignas(64) CUtensorMap kv_tmap64v;  // head_dim 64 (V boxes, SW64)
+  alignas(64) CUtensorMap kv_tmap256;  // head_dim 256
+  int has_tmap = 0;                    // bit d/64 set: descriptor for head_dim d encoded
   uint64_t launches = 0;
   const skv::SplitView* split = nullptr;  // data path addresses a split-scheme pool (skv_split.cpp)
   std::string err;
@@ -152,6 +155,10 @@ struct skv_batch {
   long long last_sum_hkv = 0, last_ncut = 0;  // schedule of the last decode launch (skv_batch_plan_info)
   unsigned long long* d_trace = nullptr;  // SKV_TRACE=1: per-warp timing of the last decode
   size_t trace_n = 0;
+  int32_t* d_qlen = nullptr;  // prefill per-request chunk lengths [req_cap] and row offsets [req_cap]
+  int32_t* h_qlen = nullptr;  // pinned staging of the same
+  size_t qlen_cap = 0;
+  cudaEvent_t qlen_ev = nullptr;
 };
 
 namespace {
@@ -511,8 +518,11 @@ skv_status free_impl(skv_pool* p, uint64_t id) {  // kv_cache.hpp:126-134
   return SKV_OK;
 }
 
-// TMA descriptor for the pool: 2-D [rows of 256 B][128 x 16-bit], box {64, 16}, SW128.
-bool encode_pool_tmap(skv_pool* p) {
+// TMA descriptors of the pool for the chunked-prefill kernel: the pool viewed as a 2-D
+// tensor of 16-bit elements with one row per token row of a head dim d present in the pool
+// ([pool_bytes / 2d rows][d]), box {64, 16} with 128-B swizzle (d = 64: also a {32, 16}
+// SW64 box for the V halves).  Returns a mask of bits d/64.
+int encode_pool_tmaps(skv_pool* p) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -521,18 +531,28 @@ bool encode_pool_tmap(skv_pool* p) {
       return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
     return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }();
-  if (!encode) return false;
-  for (const ModelInfo& mi : p->models)
-    if (mi.d != 128 || mi.e != 2 || p->tpb != 16) return false;
-  const cuuint64_t rows = p->storage_bytes / 256;
-  if (rows == 0 || rows > 0x7fffffffull) return false;  // TMA coordinates are signed 32-bit
-  const cuuint64_t dims[2] = {128, rows};
-  const cuuint64_t strides[1] = {256};
-  const cuuint32_t box[2] = {64, 16};
-  const cuuint32_t estr[2] = {1, 1};
-  return encode(&p->kv_tmap, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, p->storage, dims, strides, box, estr,
-                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  if (!encode || p->tpb != 16) return 0;
+  int mask = 0;
+  auto enc = [&](CUtensorMap* m, int d, int box_x, CUtensorMapSwizzle sw) {
+    const cuuint64_t rows = p->storage_bytes / (2 * d);
+    if (rows == 0 || rows > 0x7fffffffull) return false;  // TMA coordinates are signed 32-bit
+    const cuuint64_t dims[2] = {(cuuint64_t)d, rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)(2 * d)};
+    const cuuint32_t box[2] = {(cuuint32_t)box_x, 16};
+    const cuuint32_t estr[2] = {1, 1};
+    return encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, p->storage, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  };
+  for (const ModelInfo& mi : p->models) {
+    if (mi.e != 2) continue;
+    if (mi.d == 128 && !(mask & 2) && enc(&p->kv_tmap, 128, 64, CU_TENSOR_MAP_SWIZZLE_128B)) mask |= 2;
+    if (mi.d == 64 && !(mask & 1) && enc(&p->kv_tmap64, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B) &&
+        enc(&p->kv_tmap64v, 64, 32, CU_TENSOR_MAP_SWIZZLE_64B))
+      mask |= 1;
+    if (mi.d == 256 && !(mask & 4) && enc(&p->kv_tmap256, 256, 64, CU_TENSOR_MAP_SWIZZLE_128B)) mask |= 4;
+  }
+  return mask;
 }
 
 skv_status ensure_storage(skv_pool* p) {
@@ -542,7 +562,7 @@ skv_status ensure_storage(skv_pool* p) {
   if (bytes == 0) return fail(p, SKV_ERR_ARG, "empty pool");
   SKV_CUDA(p, cudaMalloc(&p->storage, bytes));
   p->storage_bytes = bytes;
-  p->has_tmap = encode_pool_tmap(p);
+  p->has_tmap = encode_pool_tmaps(p);
   return SKV_OK;
 }
 
@@ -1008,6 +1028,9 @@ void skv_batch_destroy(skv_batch* b) {
     if (q) cudaFree(q);
   if (b->h_stage) cudaFreeHost(b->h_stage);
   if (b->stage_ev) cudaEventDestroy(b->stage_ev);
+  if (b->d_qlen) cudaFree(b->d_qlen);
+  if (b->h_qlen) cudaFreeHost(b->h_qlen);
+  if (b->qlen_ev) cudaEventDestroy(b->qlen_ev);
   delete b;
 }
 
@@ -1070,8 +1093,13 @@ static skv_status make_params(skv_pool* p, skv_batch* b, int layer, skv::DataPar
   dp->req_table = p->dev.req_table;
   dp->cap = p->cap;
   dp->pool = static_cast<char*>(p->storage);
-  dp->has_tmap = p->has_tmap ? 1 : 0;
-  if (p->has_tmap) dp->kv_tmap = p->kv_tmap;
+  dp->has_tmap = p->has_tmap;
+  if (p->has_tmap & 2) dp->kv_tmap = p->kv_tmap;
+  if (p->has_tmap & 1) {
+    dp->kv_tmap64 = p->kv_tmap64;
+    dp->kv_tmap64v = p->kv_tmap64v;
+  }
+  if (p->has_tmap & 4) dp->kv_tmap256 = p->kv_tmap256;
   dp->merged_stride = p->merged_stride;
   dp->tpb = p->tpb;
   dp->dtype = p->dtype;
@@ -1307,9 +1335,17 @@ skv_status skv_prefill_attention(skv_pool* p, skv_batch* b, const skv_prefill_ar
   skv_status st = check_batch(p, b);
   if (st) return st;
   if ((st = ensure_storage(p))) return st;
-  if (a->q_len < 1) return fail(p, SKV_ERR_ARG, "prefill: q_len must be >= 1");
+  if (!a->q_lens && a->q_len < 1) return fail(p, SKV_ERR_ARG, "prefill: q_len must be >= 1");
+  int max_q = a->q_len;
+  if (a->q_lens) {
+    max_q = 0;
+    for (int i = 0; i < b->nreq; ++i) {
+      if (a->q_lens[i] < 1) return fail(p, SKV_ERR_ARG, "prefill: every q_lens[i] must be >= 1");
+      max_q = std::max(max_q, a->q_lens[i]);
+    }
+  }
   for (int i = 0; i < b->nreq; ++i)
-    if (p->req[b->handles[i]].tokens < a->q_len)
+    if (p->req[b->handles[i]].tokens < (a->q_lens ? a->q_lens[i] : a->q_len))
       return fail(p, SKV_ERR_ARG, "prefill: request " + std::to_string(b->ids[i]) + " holds fewer than q_len tokens");
   DeviceGuard guard(p->device);
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : p->stream;
@@ -1318,13 +1354,41 @@ skv_status skv_prefill_attention(skv_pool* p, skv_batch* b, const skv_prefill_ar
   for (int g = 0; g < b->ngroups; ++g) {
     dp.g[g].q = a->q[g];
     dp.g[g].out = a->out[g];
-  }
-  for (int g = 0; g < b->ngroups; ++g) {
-    if (p->models[b->gmodel[g]].d != 128) return fail(p, SKV_ERR_ARG, "prefill: head_dim 128 only");
+    const int d = p->models[b->gmodel[g]].d;
+    if (!(p->has_tmap & (d / 64)))
+      return fail(p, SKV_ERR_ARG, "prefill: no TMA descriptor for head_dim " + std::to_string(d));
     if (a->softmax_scale > 0.f) dp.g[g].scale_log2 = a->softmax_scale * 1.4426950408889634f;
   }
   dp.scale_log2 = dp.g[0].scale_log2;
   dp.n_new = a->q_len;
+  dp.max_q_len = max_q;
+  if (a->q_lens && b->nreq) {  // per-request lengths + row offsets within each group's q/out
+    if ((size_t)b->nreq > b->qlen_cap) {
+      SKV_CUDA(p, cudaStreamSynchronize(s));
+      if (b->d_qlen) cudaFree(b->d_qlen);
+      if (b->h_qlen) cudaFreeHost(b->h_qlen);
+      b->qlen_cap = std::max<size_t>(b->req_cap, (size_t)b->nreq);
+      SKV_CUDA(p, cudaMalloc(&b->d_qlen, 2 * b->qlen_cap * sizeof(int32_t)));
+      SKV_CUDA(p, cudaHostAlloc(&b->h_qlen, 2 * b->qlen_cap * sizeof(int32_t), cudaHostAllocMapped));
+    }
+    if (b->qlen_ev) SKV_CUDA(p, cudaEventSynchronize(b->qlen_ev));  // staging buffer reuse
+    for (int g = 0; g < b->ngroups; ++g) {
+      int off = 0;
+      for (int i = 0; i < b->gsize[g]; ++i) {
+        const int r = b->gbegin[g] + i;
+        b->h_qlen[r] = a->q_lens[r];
+        b->h_qlen[b->qlen_cap + r] = off;
+        off += a->q_lens[r];
+      }
+    }
+    skv::launch_stage_copy(b->d_qlen, b->h_qlen, b->nreq * sizeof(int32_t), s);
+    skv::launch_stage_copy(b->d_qlen + b->qlen_cap, b->h_qlen + b->qlen_cap, b->nreq * sizeof(int32_t), s);
+    if (!b->qlen_ev) SKV_CUDA(p, cudaEventCreateWithFlags(&b->qlen_ev, cudaEventDisableTiming));
+    SKV_CUDA(p, cudaEventRecord(b->qlen_ev, s));
+    dp.q_lens = b->d_qlen;
+    dp.q_offs = b->d_qlen + b->qlen_cap;
+    p->launches += 2;
+  }
   static const int dbg = [] {
     const char* e = getenv("SKV_PREFILL_DBG");
     return e ? atoi(e) : 0;
@@ -1338,7 +1402,7 @@ skv_status skv_prefill_attention(skv_pool* p, skv_batch* b, const skv_prefill_ar
   if (trace_on) {  // prefill kernels built with -DSKV_PF_TRACE: 16 u64 per CTA (4 records)
     int tiles = 1, heads = 1;
     for (int g = 0; g < b->ngroups; ++g) {
-      tiles = std::max(tiles, (a->q_len * dp.g[g].G + 127) / 128);
+      tiles = std::max(tiles, (max_q * dp.g[g].G + 127) / 128);
       heads = std::max(heads, dp.g[g].Hkv);
     }
     const size_t n = (size_t)((tiles + 1) / 2) * heads * b->nreq * 4;
@@ -1352,7 +1416,9 @@ skv_status skv_prefill_attention(skv_pool* p, skv_batch* b, const skv_prefill_ar
   }
   if ((st = order_streams(p, s))) return st;
   skv::launch_prefill(dp, s);
-  p->launches++;
+  int dmask = 0;  // one launch per head dim present
+  for (int g = 0; g < b->ngroups; ++g) dmask |= p->models[b->gmodel[g]].d / 64;
+  p->launches += __builtin_popcount(dmask & 7);
   return after_data(p, s);
 }
 

@@ -108,7 +108,13 @@ struct DataParams {
   // (one row = one token's head_dim run), box {64, 16}, 128B swizzle: one box = one
   // 64-element half of a native block's K or V tile, landing in UMMA operand layout.
   alignas(64) CUtensorMap kv_tmap;
-  int has_tmap;
+  alignas(64) CUtensorMap kv_tmap64;   // head_dim 64: rows of 128 B, box {64, 16}, SW128 (K tiles)
+  alignas(64) CUtensorMap kv_tmap64v;  // head_dim 64: rows of 128 B, box {32, 16}, SW64 (V halves)
+  alignas(64) CUtensorMap kv_tmap256;  // head_dim 256: rows of 512 B, box {64, 16}, SW128
+  int has_tmap;                        // bit d/64: the pool has a descriptor for head_dim d
+  const int32_t* q_lens;               // prefill: per-request chunk length [nreq] (NULL: n_new)
+  const int32_t* q_offs;               // prefill: request's first row in its group's q/out [nreq]
+  int max_q_len;
   DataGroup g[kMaxGroups];
   int ngroups;
   int nreq;                  // batch size

@@ -120,7 +120,7 @@ class _AppendArgs(C.Structure):
 
 class _PrefillArgs(C.Structure):
     _fields_ = [("q", C.POINTER(C.c_void_p)), ("out", C.POINTER(C.c_void_p)), ("softmax_scale", C.c_float),
-                ("layer", C.c_int32), ("q_len", C.c_int32)]
+                ("layer", C.c_int32), ("q_len", C.c_int32), ("q_lens", C.POINTER(C.c_int32))]
 
 
 _lib = None
@@ -594,16 +594,34 @@ class Batch:
         a._keep = (ka, va)
         return a
 
-    def prefill(self, q: Sequence, out: Sequence, layer: int, q_len: int, softmax_scale: float = 0.0,
+    def prefill(self, q: Sequence, out: Sequence, layer: int, q_len, softmax_scale: float = 0.0,
                 stream=None):
+        """Causal chunked prefill of every request's last ``q_len`` tokens (already appended).
+        ``q_len``: one int for the whole batch (q/out of group g: [B_g, q_len, Hq, d]) or one
+        length per request in batch order (q/out of group g packed by request:
+        [sum of its lengths, Hq, d])."""
         dt, dev = self.cache.dtype, self.cache.device
-        _check_tensors(q, [(B, q_len, Hq, d) for B, Hq, _, d in self._shapes], dt, dev, "prefill q")
-        _check_tensors(out, [(B, q_len, Hq, d) for B, Hq, _, d in self._shapes], dt, dev, "prefill out")
         n = len(self.groups)
+        ragged = not isinstance(q_len, (int, np.integer))
+        if ragged:
+            lens = [int(x) for x in q_len]
+            if len(lens) != sum(B for B, _, _, _ in self._shapes):
+                raise ArgError(f"prefill: {len(lens)} q_lens for {sum(B for B, _, _, _ in self._shapes)} requests")
+            shp, k = [], 0
+            for B, Hq, _, d in self._shapes:
+                shp.append((sum(lens[k:k + B]), Hq, d))
+                k += B
+            ql = (C.c_int32 * max(1, len(lens)))(*lens)
+        else:
+            shp = [(B, int(q_len), Hq, d) for B, Hq, _, d in self._shapes]
+        _check_tensors(q, shp, dt, dev, "prefill q")
+        _check_tensors(out, shp, dt, dev, "prefill out")
         qa = (C.c_void_p * n)(*[_ptr(t) for t in q])
         oa = (C.c_void_p * n)(*[_ptr(t) for t in out])
         a = _PrefillArgs(C.cast(qa, C.POINTER(C.c_void_p)), C.cast(oa, C.POINTER(C.c_void_p)), softmax_scale,
-                         layer, q_len)
+                         layer, 0 if ragged else int(q_len))
+        if ragged:
+            a.q_lens = C.cast(ql, C.POINTER(C.c_int32))
         self.cache._chk(self.cache._lib.skv_prefill_attention(self.cache._h, self._h, C.byref(a),
                                                               _stream_ptr(stream)))
 

@@ -189,3 +189,73 @@ def test_randomised_mixed_head_dims(seed):
     layer = int(rng.integers(0, max(s[0] for s in shapes)))
     decode_check(shapes, ctxs, layer, dtype=P.BF16 if seed % 2 else P.FP16, seed=seed, fused=bool(seed % 3 == 0),
                  split=int(rng.choice([0, 0, 48])))
+
+
+# ---------------------------------------------------------------------------- prefill ---
+def prefill_check(shapes, ctxs, q_lens, layer, dtype=P.FP16, seed=11, qamp=1.0):
+    """q_lens: per-request chunk lengths (batch order) or one int for all."""
+    cache, groups, _ = build(shapes, ctxs, dtype)
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    nreq = [len(ids) for _, ids in groups]
+    lens = [q_lens] * sum(nreq) if isinstance(q_lens, int) else list(q_lens)
+    per, k = [], 0
+    for n in nreq:
+        per.append(lens[k:k + n])
+        k += n
+    qs, outs = [], []
+    for (m, ids), (L, H, Hq, d), pl in zip(groups, shapes, per):
+        shape = (len(ids), q_lens, Hq, d) if isinstance(q_lens, int) else (sum(pl), Hq, d)
+        qs.append(((torch.rand(shape, generator=g, device="cuda") * 2 - 1) * qamp).to(tdt(dtype)))
+        outs.append(torch.full(shape, float("nan"), device="cuda", dtype=tdt(dtype)))
+    b = cache.batch(groups)
+    b.prefill(qs, outs, layer, q_lens)
+    torch.cuda.synchronize()
+    img = image(cache)
+    worst = 0.0
+    for (m, ids), q, o, (L, H, Hq, d), pl in zip(groups, qs, outs, shapes, per):
+        if layer >= L:
+            continue
+        ctx = np.array([cache.request_tokens(i) for i in ids], np.int64)
+        ql = np.array(pl, np.int64)
+        qn = u16(q).reshape(-1, Hq, d)
+        ref = O.prefill_attention(olay(cache, m), img, layer, tables(cache, ids), ctx - ql, ql, qn, 1.0 / np.sqrt(d))
+        got = o.float().cpu().numpy().reshape(-1, Hq, d)
+        assert not np.isnan(got).any(), d
+        worst = max(worst, float(np.abs(got - ref).max()))
+    assert worst <= TOL[dtype], worst
+    return worst
+
+
+@pytest.mark.parametrize("d", [64, 256])
+@pytest.mark.parametrize("G", [1, 4])
+def test_prefill_head_dim(d, G):
+    prefill_check([(2, 2, 2 * G, d)], [[700, 300]], 256 if G == 1 else 64, layer=1)
+
+
+def test_prefill_mixed_head_dims_one_call():
+    """d = 64, 128, 256 services in one prefill call (one tcgen05 launch per head dim)."""
+    prefill_check([(2, 4, 16, 64), (2, 4, 4, 128), (2, 2, 4, 256), (3, 8, 8, 256)],
+                  [[513, 200], [1000], [77, 1500], [300]], 33, layer=1)
+
+
+@pytest.mark.parametrize("dtype", ["fp16", "bf16"])
+def test_prefill_per_request_q_len(dtype):
+    """Ragged chunks in one launch: each request's own chunk length (1 .. 700), q/out packed
+    by request within each group (the config-3 last-chunk case without a launch per length)."""
+    shapes = [(2, 8, 32, 128), (2, 4, 4, 128), (2, 2, 4, 64), (2, 2, 2, 256)]
+    ctxs = [[1000, 40, 600], [129, 700], [513, 16], [300, 301]]
+    q_lens = [512, 1, 300, 129, 700, 100, 16, 1, 257]
+    prefill_check(shapes, ctxs, q_lens, layer=0, dtype=P.FP16 if dtype == "fp16" else P.BF16)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_prefill_randomised_head_dims(seed):
+    rng = np.random.default_rng(500 + seed)
+    shapes, ctxs, lens = [], [], []
+    for _ in range(int(rng.integers(1, 4))):
+        H = int(rng.choice([1, 2, 4]))
+        shapes.append((2, H, H * int(rng.choice([1, 2, 4, 8])), int(rng.choice([64, 128, 256]))))
+        cl = [int(rng.integers(1, 1500)) for _ in range(int(rng.integers(1, 5)))]
+        ctxs.append(cl)
+        lens += [int(rng.integers(1, c + 1)) for c in cl]
+    prefill_check(shapes, ctxs, lens, layer=1, dtype=P.BF16 if seed == 2 else P.FP16, seed=seed)
