@@ -595,6 +595,21 @@ def run_gpu(args):
     cache.synchronize()  # surfaces any device-side invariant flag raised during the runs
     if rank == 0 and not args.no_parity:
         result["parity"] = headline_parity(torch, cache, batch, q, k, v, stream, NLAYERS)
+    if rank == 0 and not args.no_prefill:
+        # chunked prefill (tcgen05) measured in the same run, so the driver sees the tensor-pipe path
+        try:
+            with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+                tpk, tpk_kind = float(json.load(f)["bf16_tflops"]), "measured (burst, cuBLAS bf16)"
+        except Exception:  # noqa: BLE001
+            tpk, tpk_kind = 2250.0, "fallback (nominal dense bf16)"
+        pf = {"kernel": "skv prefill_kernel<T, 128> (cta_group::2 tcgen05.mma, TMA, TMEM)", "peak": tpk,
+              "peak_kind": tpk_kind, "unit": "TFLOP/s", "bound": "tensor",
+              "ncu": "profiles/r01_ncu_prefill_v10_final.txt (tensor pipe active % of cycles)"}
+        for key, (R_, ctx_, C_) in (("long_chunk", (4, 16384, 2048)), ("config3_chunk", (8, 2048, 512))):
+            s_ = prefill_sample(P, torch, local, R_, ctx_, C_)
+            s_["frac"] = round(s_["tflops"] / tpk, 4)
+            pf[key] = s_
+        result["prefill"] = pf
     if rank == 0 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(cache, batch, q, args)
     if rank == 0:
@@ -943,6 +958,69 @@ def run_config5(args):
         dist.destroy_process_group()
 
 
+def prefill_sample(P, torch, device, R, ctx, C, steps=10, warmup=3, services=None, check=True):
+    """Chunked prefill (tcgen05 CTA-pair kernel) on its own pool: the config-2 services, R
+    requests each, the last C tokens of a ctx-token context attending causally (layer 0),
+    timed with CUDA events on the launching stream (useful causal flops); plus an fp32-oracle
+    check of the last 64 query rows of each service's first request."""
+    services = services or SERVICES
+    models = model_specs(P, services)
+    cache = P.UnifiedKvCache(models, 16, 1, len(services) * R * (ctx // 16 + 2) + 64, device=device,
+                             phys_layers=2, allocate_storage=True)
+    groups, rid = [], 1
+    for m in range(len(services)):
+        ids = []
+        for _ in range(R):
+            assert cache.try_allocate(rid, m, ctx)
+            ids.append(rid)
+            rid += 1
+        groups.append((m, ids))
+    stream = torch.cuda.Stream(device=device)
+    cache.set_stream(stream)
+    cache.synth_fill(1, 1.0, stream)
+    b = cache.batch(groups)
+    gen = torch.Generator(device=device).manual_seed(3)
+    with torch.cuda.stream(stream):
+        qs = [torch.randn((R, C, s[3], hd(s)), generator=gen, device=device).half() for s in services]
+        outs = [torch.empty_like(x) for x in qs]
+    flops = sum(4.0 * hd(s) * s[3] * R * (C * (ctx - C) + C * (C + 1) / 2) for s in services)
+    for _ in range(warmup):
+        b.prefill(qs, outs, 0, C, stream=stream)
+    torch.cuda.synchronize(device)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(device) as clk:
+        e0.record(stream)
+        for _ in range(steps):
+            b.prefill(qs, outs, 0, C, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize(device)
+    ms = e0.elapsed_time(e1) / steps
+    res = {"tflops": round(flops / (ms * 1e-3) / 1e12, 1), "ms_per_launch": round(ms, 4),
+           "shape": f"{len(services)} services x {R} requests, last {C} of {ctx} tokens (causal)",
+           "clocks": clk.summary()}
+    if check:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle_py as O
+        worst, nq = 0.0, min(64, C)
+        for (m, ids), q, o in zip(groups, qs, outs):
+            bt = cache.block_table_np(ids[0])
+            img = cache.read_blocks(bt[:, 0])
+            tab = np.stack([np.arange(len(bt), dtype=np.int32), bt[:, 1]], axis=1)[None]
+            lay = cache.layout(m)
+            olay = O.layout(lay.merged_stride, lay.native_stride, lay.layer_stride, lay.head_stride, lay.kv_stride,
+                            16, lay.head_dim, lay.kv_heads, lay.q_heads, lay.phys_layers, lay.dtype)
+            qh = q[0, C - nq:].contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+            ref = O.prefill_attention(olay, img, 0, tab, np.array([ctx - nq], np.int64), np.array([nq], np.int64),
+                                      qh.reshape(nq, -1, lay.head_dim), 1.0 / np.sqrt(lay.head_dim))
+            got = o[0, C - nq:].float().cpu().numpy().reshape(ref.shape)
+            worst = max(worst, float(np.abs(got - ref).max()))
+        res["parity"] = {"max_abs": worst, "tol": 2e-3, "ok": bool(worst <= 2e-3),
+                         "rows": f"last {nq} query tokens of the first request of each service"}
+    b.close()
+    cache.close()
+    return res
+
+
 def run_prefill(args):
     """Chunked-prefill attention on tcgen05, one line in the bench format:
     the four config-2 services, R requests each, the last C tokens of a CTX-token context
@@ -1229,6 +1307,8 @@ def main():
     ap.add_argument("--share-gpu", dest="share_gpu", action="store_true",
                     help="dry run of the N-rank path on a box with fewer GPUs: every rank on GPU 0, gloo "
                          "(functional only; the numbers are meaningless)")
+    ap.add_argument("--no-prefill", dest="no_prefill", action="store_true",
+                    help="skip the chunked-prefill sample in the decode line")
     ap.add_argument("--no-parity", dest="no_parity", action="store_true",
                     help="skip the post-timing oracle check of a sample of the measured launch")
     ap.add_argument("--no-graph", dest="no_graph", action="store_true",

@@ -1,4 +1,5 @@
-"""Quick prefill timing: 4 config-2 services, R requests each, context CTX, chunk Q (last Q tokens)."""
+"""Quick prefill timing: 4 config-2 services (head dim D), R requests each, context CTX, chunk Q (last Q tokens).
+Usage: prefill_probe.py R CTX Q [reps] [D]"""
 import json
 import sys
 
@@ -10,8 +11,8 @@ import paper_2504_15720_b200 as P
 SERV = [("llama-3-8b", 32, 8, 32), ("mistral-7b", 32, 8, 32), ("llama-2-13b", 40, 40, 40), ("opt-6.7b", 32, 32, 32)]
 
 
-def main(R=8, CTX=2048, Q=512, reps=10):
-    models = [P.ModelSpec(n, L, H, 128, 2, Hq) for n, L, H, Hq in SERV]
+def main(R=8, CTX=2048, Q=512, reps=10, D=128):
+    models = [P.ModelSpec(n, L, H, D, 2, Hq) for n, L, H, Hq in SERV]
     cache = P.UnifiedKvCache(models, 16, 1, 4 * R * (CTX // 16 + 2) + 64, phys_layers=2, allocate_storage=True)
     groups = []
     rid = 1
@@ -27,10 +28,10 @@ def main(R=8, CTX=2048, Q=512, reps=10):
     cache.set_stream(s)
     cache.synth_fill(1, 1.0, s)
     b = cache.batch(groups)
-    qs = [torch.randn((R, Q, Hq, 128), device="cuda").half() for _, _, _, Hq in SERV]
+    qs = [torch.randn((R, Q, Hq, D), device="cuda").half() for _, _, _, Hq in SERV]
     outs = [torch.empty_like(x) for x in qs]
     p0 = CTX - Q
-    flops = sum(4 * 128 * Hq * R * (Q * p0 + Q * (Q + 1) / 2) for _, _, _, Hq in SERV)
+    flops = sum(4 * D * Hq * R * (Q * p0 + Q * (Q + 1) / 2) for _, _, _, Hq in SERV)
     for _ in range(3):
         b.prefill(qs, outs, 0, Q, stream=s)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -40,7 +41,7 @@ def main(R=8, CTX=2048, Q=512, reps=10):
     e1.record(s)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
-    print(json.dumps({"R": R, "ctx": CTX, "q_len": Q, "ms": ms, "tflops": flops / ms / 1e9,
+    print(json.dumps({"R": R, "ctx": CTX, "q_len": Q, "head_dim": D, "ms": ms, "tflops": flops / ms / 1e9,
                       "frac_of_1644": flops / ms / 1e9 / 1644.2}))
 
 
