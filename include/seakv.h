@@ -192,6 +192,8 @@ typedef struct {
   const void* const* v;
   int32_t layer;
   int32_t n_new; /* new tokens per request, written at positions [tokens-n_new, tokens) */
+  const int32_t* n_news; /* optional per-request counts (host, [nreq], batch order); then each
+                            group's k / v are packed by request: [sum of its n_news][Hkv/tp][d] */
 } skv_append_args;
 skv_status skv_append_kv(skv_pool* p, skv_batch* b, const skv_append_args* args, void* stream);
 

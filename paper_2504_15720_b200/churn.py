@@ -20,9 +20,10 @@ import math
 import time
 from typing import Dict, List, Optional, Sequence
 
+import numpy as np
 import torch
 
-from .kvcache import Batch, UnifiedKvCache
+from .kvcache import KVOP_DTYPE, Batch, UnifiedKvCache
 
 M64 = (1 << 64) - 1
 
@@ -119,10 +120,22 @@ class Req:
 
 
 class ChurnEngine:
+    """Host-driven serving loop over one unified pool.  Per iteration: admission (FCFS while the
+    pool is below the occupancy target), the decode step's +1-token grows and the prefill
+    chunks' grows as ONE batched allocator call each (skv_replay), preemption of decode
+    requests that hit CacheFull (free -> re-queue -> re-prefill from token 0,
+    simulation.hpp:144-157,333-340), then per layer one fused append+decode launch and one
+    ragged append + one ragged causal-prefill launch (every prefill chunk of the iteration,
+    whatever its length), then the frees of finished requests.  GPU timings are resolved
+    lazily (no per-iteration synchronize); the host still waits once per iteration for the
+    emptied-block counts of the previous iteration's frees before its next grows."""
+
     def __init__(self, cache: UnifiedKvCache, shapes: Sequence[tuple], profiles: Sequence[ServiceProfile],
                  chunk: int = 512, occupancy: float = 0.70, max_decode: int = 512, max_prefill: int = 8,
-                 layers: Optional[int] = None, stream=None, seed: int = 7):
+                 layers: Optional[int] = None, stream=None, seed: int = 7, io: bool = False):
         self.cache, self.shapes, self.profiles = cache, list(shapes), list(profiles)
+        self.io = io  # e2e: every decode step copies its per-layer q/k/v in from pinned host memory and
+        #              every layer's output back (prefill activations stay device-resident)
         self.chunk, self.occupancy = chunk, occupancy
         self.max_decode, self.max_prefill = max_decode, max_prefill
         self.nlayers = layers or max(L for L, _, _ in shapes)
@@ -134,33 +147,59 @@ class ChurnEngine:
         self.dtype = torch.float16
         g = torch.Generator(device="cuda").manual_seed(seed)
         M = len(shapes)
-        # synthetic activations, sliced per iteration (contents are irrelevant to the KV path)
+        # synthetic activations, sliced per iteration (contents are irrelevant to the KV path);
+        # prefill buffers are packed by request: [sum of the iteration's chunk lengths, heads, d]
         self.q_dec = [torch.randn((max_decode, Hq, 128), generator=g, device="cuda").half() for _, _, Hq in shapes]
         self.o_dec = [torch.empty_like(x) for x in self.q_dec]
         self.kv_dec = [torch.randn((max_decode, 1, H, 128), generator=g, device="cuda").half() for _, H, _ in shapes]
-        self.q_pre = [torch.randn((max_prefill, chunk, Hq, 128), generator=g, device="cuda").half()
+        self.q_pre = [torch.randn((max_prefill * chunk, Hq, 128), generator=g, device="cuda").half()
                       for _, _, Hq in shapes]
         self.o_pre = [torch.empty_like(x) for x in self.q_pre]
-        self.kv_pre = [torch.randn((max_prefill, chunk, H, 128), generator=g, device="cuda").half()
+        self.kv_pre = [torch.randn((max_prefill * chunk, H, 128), generator=g, device="cuda").half()
                        for _, H, _ in shapes]
+        if io:  # per-layer decode activations: pinned host <-> device staging
+            L = self.nlayers
+            self.h_q = [torch.randn((L, max_decode, Hq, 128), generator=g, device="cuda").half().cpu().pin_memory()
+                        for _, _, Hq in shapes]
+            self.h_kv = [torch.randn((L, max_decode, 1, H, 128), generator=g, device="cuda").half().cpu().pin_memory()
+                         for _, H, _ in shapes]
+            self.h_o = [torch.empty((L, max_decode, Hq, 128), dtype=torch.float16).pin_memory() for _, _, Hq in shapes]
+            self.d_q = [torch.empty(x.shape, dtype=x.dtype, device="cuda") for x in self.h_q]
+            self.d_kv = [torch.empty(x.shape, dtype=x.dtype, device="cuda") for x in self.h_kv]
+            self.d_o = [torch.empty(x.shape, dtype=x.dtype, device="cuda") for x in self.h_o]
         self._dec_batch: Optional[Batch] = None
-        self._pre_batches: Dict[int, Batch] = {}
-        self.stats = dict(iterations=0, grow_ops=0, free_ops=0, preemptions=0, alloc_s=0.0, append_ms=0.0,
-                          decode_ms=0.0, prefill_ms=0.0, decode_bytes=0.0, append_bytes=0.0, data_path_ms=0.0,
-                          prefill_flops=0.0,
-                          occupancy_sum=0.0, finished=0, admitted=0, cache_full=0)
+        self._pre_batch: Optional[Batch] = None
+        self._marks: List[tuple] = []  # (kind, events) resolved by summary()
+        self.stats = dict(iterations=0, grow_ops=0, free_ops=0, preemptions=0, reprefilled=0, alloc_s=0.0,
+                          append_ms=0.0, decode_ms=0.0, prefill_ms=0.0, decode_bytes=0.0, append_bytes=0.0,
+                          data_path_ms=0.0, prefill_flops=0.0, occupancy_sum=0.0, finished=0, admitted=0,
+                          cache_full=0, prefill_launches=0, h2d_bytes=0.0, d2h_bytes=0.0)
         self.M = M
+        self.preempted_ids: set = set()
 
-    # -- allocator calls, recorded -----------------------------------------------------------
+    # -- allocator calls, recorded (one C-ABI call per batch) ---------------------------------
+    def _replay(self, kind: int, reqs: Sequence[Req], tokens: Sequence[int]) -> np.ndarray:
+        n = len(reqs)
+        if n == 0:
+            return np.zeros(0, dtype=bool)
+        arr = np.zeros(n, dtype=KVOP_DTYPE)
+        arr["kind"] = kind
+        arr["model"] = [r.model for r in reqs]
+        arr["id"] = [r.rid for r in reqs]
+        arr["tokens"] = tokens
+        self.ops.extend((kind, r.rid, r.model, int(t)) for r, t in zip(reqs, tokens))
+        self.stats["grow_ops" if kind == 0 else "free_ops"] += n
+        return self.cache.replay_array(arr).astype(bool)
+
+    def _grow_many(self, reqs: Sequence[Req], tokens: Sequence[int]) -> np.ndarray:
+        return self._replay(0, reqs, tokens)
+
+    def _free_many(self, reqs: Sequence[Req]) -> None:
+        self._replay(1, reqs, [0] * len(reqs))
+
+    # single-op forms (warm start)
     def _grow(self, r: Req, tokens: int) -> bool:
-        self.ops.append((0, r.rid, r.model, tokens))
-        self.stats["grow_ops"] += 1
-        return self.cache.try_allocate(r.rid, r.model, tokens)
-
-    def _free(self, r: Req):
-        self.ops.append((1, r.rid, r.model, 0))
-        self.stats["free_ops"] += 1
-        self.cache.free_request(r.rid)
+        return bool(self._grow_many([r], [tokens])[0])
 
     def add_arrivals(self, arrivals: Sequence[Arrival]):
         for a in arrivals:
@@ -168,16 +207,11 @@ class ChurnEngine:
             self.waiting.append(Req(self.next_id, a.svc, p.model_idx, a.in_len, a.out_len))
             self.next_id += 1
 
-    def _batch(self, key, groups):
-        if key == "dec":
-            if self._dec_batch is None:
-                self._dec_batch = self.cache.batch(groups)
-            else:
-                self._dec_batch.reset(groups)
-            return self._dec_batch
-        b = self._pre_batches.get(key)
+    def _batch(self, attr: str, groups):
+        b = getattr(self, attr)
         if b is None:
-            b = self._pre_batches[key] = self.cache.batch(groups)
+            b = self.cache.batch(groups)
+            setattr(self, attr, b)
         else:
             b.reset(groups)
         return b
@@ -215,6 +249,8 @@ class ChurnEngine:
 
     def reset_stats(self) -> None:
         """Zero the counters (the recorded KvOp stream is kept)."""
+        self._resolve()
+        self._marks = []
         for k in self.stats:
             self.stats[k] = 0.0 if isinstance(self.stats[k], float) else 0
 
@@ -232,112 +268,147 @@ class ChurnEngine:
             self.running[r.rid] = r
             prefill.append(r)
             st["admitted"] += 1
-        # decode growth: the last generated token is fed back, so the cache holds prompt +
-        # generated tokens (+1 per step); CacheFull -> preempt (free + re-queue for re-prefill)
+        # decode growth (one batched call): the last generated token is fed back, so the cache
+        # holds prompt + generated tokens (+1 per step); CacheFull -> preempt: free + re-queue
+        # at the head of the waiting queue, re-prefilled from token 0 when re-admitted
         decode = [r for r in self.running.values() if r.phase == "decode"][: self.max_decode]
-        dec_ok = []
-        for r in decode:
-            if self._grow(r, r.in_len + r.generated):
-                dec_ok.append(r)
-            else:
-                st["cache_full"] += 1
-                st["preemptions"] += 1
-                self._free(r)
+        ok = self._grow_many(decode, [r.in_len + r.generated for r in decode])
+        dec_ok = [r for r, g in zip(decode, ok) if g]
+        victims = [r for r, g in zip(decode, ok) if not g]
+        if victims:
+            st["cache_full"] += len(victims)
+            st["preemptions"] += len(victims)
+            self._free_many(victims)
+            for r in reversed(victims):
                 del self.running[r.rid]
                 r.phase = "waiting"
+                self.preempted_ids.add(r.rid)
                 self.waiting.insert(0, r)
-        # prefill chunk growth
-        pre_ok: Dict[int, List[Req]] = {}
-        for r in prefill:
-            c = min(self.chunk, r.in_len - r.done)
-            if self._grow(r, r.done + c):
-                pre_ok.setdefault(c, []).append(r)
-            else:
-                st["cache_full"] += 1
+        # prefill chunk growth (one batched call)
+        chunks = [min(self.chunk, r.in_len - r.done) for r in prefill]
+        ok = self._grow_many(prefill, [r.done + c for r, c in zip(prefill, chunks)])
+        pre_ok = [(r, c) for r, c, g in zip(prefill, chunks, ok) if g]
+        st["cache_full"] += int(len(prefill) - len(pre_ok))
         cache.flush(self.stream)
         st["alloc_s"] += time.perf_counter() - t0
         # data path over every layer index
         ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
-        marks = []
-        span = [ev(), ev()]  # GPU time of the whole data path of this step
+        span = [ev(), ev()]  # GPU span of the whole data path of this step
         span[0].record(self.stream)
         if dec_ok:
             groups = [(m, [r.rid for r in dec_ok if r.model == m]) for m in range(self.M)]
             groups = [g for g in groups if g[1]]
-            b = self._batch("dec", groups)
+            b = self._batch("_dec_batch", groups)
             q = [self.q_dec[m][: len(ids)] for m, ids in groups]
             o = [self.o_dec[m][: len(ids)] for m, ids in groups]
             kv = [self.kv_dec[m][: len(ids)] for m, ids in groups]
             # one launch per layer: the new token's K/V is appended inside the decode kernel
-            # (fused append); the layer loop is bracketed by one pair of events, so decode_ms
-            # is the GPU span of the decode phase (host submission runs ahead of it)
+            # (fused append); bracketed by one pair of events = GPU span of the decode phase
             e = [ev(), ev(), ev()]
             e[0].record(self.stream)
+            if self.io:  # this step's q / new K,V of every layer from pinned host memory
+                with torch.cuda.stream(self.stream):
+                    for (m, ids) in groups:
+                        n = len(ids)
+                        self.d_q[m][:, :n].copy_(self.h_q[m][:, :n], non_blocking=True)
+                        self.d_kv[m][:, :n].copy_(self.h_kv[m][:, :n], non_blocking=True)
+                        st["h2d_bytes"] += 2.0 * (self.h_q[m][:, :n].numel() + self.h_kv[m][:, :n].numel())
             e[1].record(self.stream)
             for layer in range(self.nlayers):
+                if self.io:
+                    sel = [(m, len(ids), min(layer, self.shapes[m][0] - 1)) for m, ids in groups]
+                    q = [self.d_q[m][li, :n] for m, n, li in sel]
+                    o = [self.d_o[m][li, :n] for m, n, li in sel]
+                    kv = [self.d_kv[m][li, :n] for m, n, li in sel]
                 b.decode(q, o, layer, stream=self.stream, k=kv, v=kv)
             e[2].record(self.stream)
-            marks.append(("dec", e))
+            if self.io:  # every layer's attention output back to the host
+                with torch.cuda.stream(self.stream):
+                    for (m, ids) in groups:
+                        n = len(ids)
+                        self.h_o[m][:, :n].copy_(self.d_o[m][:, :n], non_blocking=True)
+                        st["d2h_bytes"] += 2.0 * self.h_o[m][:, :n].numel()
+            self._marks.append(("dec", e))
             for layer in range(self.nlayers):
-                kvb, _ = b.decode_bytes(layer)
-                st["decode_bytes"] += kvb
-        for c, rs in pre_ok.items():
-            groups = [(m, [r.rid for r in rs if r.model == m]) for m in range(self.M)]
-            groups = [g for g in groups if g[1]]
-            b = self._batch(c, groups)
-            q = [self.q_pre[m][: len(ids), :c] for m, ids in groups]
-            o = [self.o_pre[m][: len(ids), :c] for m, ids in groups]
-            kv = [self.kv_pre[m][: len(ids), :c] for m, ids in groups]
-            q = [x.contiguous() for x in q]
-            o = [torch.empty_like(x) for x in q]
-            kv = [x.contiguous() for x in kv]
+                st["decode_bytes"] += b.decode_bytes(layer)[0]
+        if pre_ok:
+            # every prefill chunk of the iteration in ONE ragged batch: per layer one append and
+            # one causal-prefill launch, whatever the chunk lengths
+            groups, lens = [], []
+            for m in range(self.M):
+                rs = [(r, c) for r, c in pre_ok if r.model == m]
+                if rs:
+                    groups.append((m, [r.rid for r, _ in rs]))
+                    lens += [c for _, c in rs]
+            tot = {m: sum(c for r, c in pre_ok if r.model == m) for m, _ in groups}
+            b = self._batch("_pre_batch", groups)
+            q = [self.q_pre[m][: tot[m]] for m, _ in groups]
+            o = [self.o_pre[m][: tot[m]] for m, _ in groups]
+            kv = [self.kv_pre[m][: tot[m]] for m, _ in groups]
+            e = [ev(), ev(), ev()]
+            e[0].record(self.stream)
             for layer in range(self.nlayers):
-                e = [ev(), ev(), ev()]
-                e[0].record(self.stream)
-                b.append(kv, kv, layer, c, self.stream)
-                e[1].record(self.stream)
-                b.prefill(q, o, layer, c, stream=self.stream)
-                e[2].record(self.stream)
-                marks.append(("pre", e))
-            for r in rs:
+                b.append(kv, kv, layer, lens, self.stream)
+            e[1].record(self.stream)
+            for layer in range(self.nlayers):
+                b.prefill(q, o, layer, lens, stream=self.stream)
+            e[2].record(self.stream)
+            self._marks.append(("pre", e))
+            st["prefill_launches"] += self.nlayers
+            for r, c in pre_ok:
                 L, H, Hq = self.shapes[r.model]
-                p0 = r.done
-                st["prefill_flops"] += 4.0 * 128 * Hq * L * (c * p0 + c * (c + 1) / 2)
+                st["prefill_flops"] += 4.0 * 128 * Hq * L * (c * r.done + c * (c + 1) / 2)
                 st["append_bytes"] += c * L * 2 * H * 128 * 2 * 2
         span[1].record(self.stream)
-        torch.cuda.synchronize()
-        st["data_path_ms"] += span[0].elapsed_time(span[1])
-        for kind, e in marks:
-            st["append_ms"] += e[0].elapsed_time(e[1])
-            st["decode_ms" if kind == "dec" else "prefill_ms"] += e[1].elapsed_time(e[2])
-        # bookkeeping: finished requests are freed
+        self._marks.append(("span", span))
+        # bookkeeping: finished requests are freed (one batched call)
         t1 = time.perf_counter()
+        done = []
         for r in dec_ok:
             r.generated += 1
             if r.generated >= r.out_len:
-                self._free(r)
-                del self.running[r.rid]
-                st["finished"] += 1
-        for c, rs in pre_ok.items():
-            for r in rs:
-                r.done += c
-                if r.done >= r.in_len:
-                    r.phase, r.generated = "decode", 1  # the prefill iteration emits token 1
-                    if r.generated >= r.out_len:
-                        self._free(r)
-                        del self.running[r.rid]
-                        st["finished"] += 1
+                done.append(r)
+        for r, c in pre_ok:
+            r.done += c
+            if r.done >= r.in_len:
+                r.phase, r.generated = "decode", 1  # the prefill iteration emits token 1
+                if r.rid in self.preempted_ids:
+                    st["reprefilled"] += 1
+                    self.preempted_ids.discard(r.rid)
+                if r.generated >= r.out_len:
+                    done.append(r)
+        self._free_many(done)
+        for r in done:
+            del self.running[r.rid]
+        st["finished"] += len(done)
         st["alloc_s"] += time.perf_counter() - t1
         st["iterations"] += 1
         st["occupancy_sum"] += cache.allocated_blocks() / max(1, pool)
         return st
 
+    def _resolve(self) -> None:
+        """GPU times of the recorded phases (one synchronize, after the timed region)."""
+        if not self._marks:
+            return
+        torch.cuda.synchronize()
+        st = self.stats
+        for kind, e in self._marks:
+            if kind == "span":
+                st["data_path_ms"] += e[0].elapsed_time(e[1])
+            elif kind == "dec":
+                st["decode_ms"] += e[1].elapsed_time(e[2])
+            else:
+                st["append_ms"] += e[0].elapsed_time(e[1])
+                st["prefill_ms"] += e[1].elapsed_time(e[2])
+        self._marks = []
+
     def summary(self) -> dict:
+        self._resolve()
         st = self.stats
         it = max(1, st["iterations"])
         return {
             "iterations": st["iterations"], "admitted": st["admitted"], "finished": st["finished"],
-            "preemptions": st["preemptions"], "cache_full": st["cache_full"],
+            "preemptions": st["preemptions"], "reprefilled": st["reprefilled"], "cache_full": st["cache_full"],
             "grow_ops": st["grow_ops"], "free_ops": st["free_ops"],
             "alloc_ops_per_s": round((st["grow_ops"] + st["free_ops"]) / max(st["alloc_s"], 1e-9), 1),
             "mean_occupancy": round(st["occupancy_sum"] / it, 4),
@@ -347,6 +418,8 @@ class ChurnEngine:
             "prefill_TFLOPs": round(st["prefill_flops"] / max(st["prefill_ms"], 1e-9) / 1e9, 1),
             "decode_ms": round(st["decode_ms"], 2), "prefill_ms": round(st["prefill_ms"], 2),
             "append_ms": round(st["append_ms"], 2), "data_path_ms": round(st["data_path_ms"], 2),
+            "prefill_launches": st["prefill_launches"],
+            "h2d_bytes": st["h2d_bytes"], "d2h_bytes": st["d2h_bytes"],
         }
 
 

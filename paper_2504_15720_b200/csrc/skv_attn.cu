@@ -983,18 +983,20 @@ __global__ void append_kernel(const __grid_constant__ DataParams p) {
   if (!g.active) return;
   const int lane = threadIdx.x & 31;
   const int wglob = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int total = p.n_new * g.Hkv;
+  const int n_new = p.q_lens ? p.q_lens[r] : p.n_new;  // ragged: this request's own count
+  const int total = n_new * g.Hkv;
   if (wglob >= total) return;
   const int i = wglob / g.Hkv, h = wglob % g.Hkv;
   const int handle = p.handles[r];
-  const int pos = p.req_tokens[handle] - p.n_new + i;
+  const int pos = p.req_tokens[handle] - n_new + i;
   if (pos < 0) return;
   const int2 e = table_row(p, handle, h)[pos / kTpb];
   const int row = 2 * g.D, cpr = g.D / 8;  // bytes of a token row, 16-B chunks per row
   char* run = p.pool + (long long)e.x * p.merged_stride + (long long)e.y * g.native_stride + g.layer_off +
               (long long)h * g.head_stride + (pos % kTpb) * row;
   const int rl = r - g.req_begin;
-  const size_t src_row = (((size_t)rl * p.n_new + i) * g.Hkv + h) * row;
+  const size_t first = p.q_offs ? (size_t)p.q_offs[r] : (size_t)rl * p.n_new;  // request's first packed token
+  const size_t src_row = ((first + i) * g.Hkv + h) * row;
   for (int ch = lane; ch < 2 * cpr; ch += 32) {  // K row then V row, 16 B per lane
     const int kv = ch >= cpr, c = ch - kv * cpr;
     const char* src = reinterpret_cast<const char*>(kv ? g.v : g.k) + src_row + c * 16;
@@ -1100,7 +1102,7 @@ void launch_decode(const DataParams& p, int max_g, int grid, cudaStream_t s) {
 void launch_append(const DataParams& p, cudaStream_t s) {
   int maxh = 1;
   for (int i = 0; i < p.ngroups; ++i) maxh = max(maxh, p.g[i].Hkv);
-  const int warps = p.n_new * maxh;
+  const int warps = (p.q_lens ? p.max_q_len : p.n_new) * maxh;
   dim3 grid((warps + 7) / 8, p.nreq);
   launch_pdl(append_kernel, grid, dim3(256), 0, s, p);
 }

@@ -155,10 +155,12 @@ struct skv_batch {
   long long last_sum_hkv = 0, last_ncut = 0;  // schedule of the last decode launch (skv_batch_plan_info)
   unsigned long long* d_trace = nullptr;  // SKV_TRACE=1: per-warp timing of the last decode
   size_t trace_n = 0;
-  int32_t* d_qlen = nullptr;  // prefill per-request chunk lengths [req_cap] and row offsets [req_cap]
+  int32_t* d_qlen = nullptr;  // ragged append/prefill: per-request lengths [req_cap] and row offsets [req_cap]
   int32_t* h_qlen = nullptr;  // pinned staging of the same
   size_t qlen_cap = 0;
   cudaEvent_t qlen_ev = nullptr;
+  std::vector<int32_t> qlen_last;  // lengths currently on the device (skip identical re-uploads)
+  uint64_t qlen_epoch = 0, launch_epoch = 1;  // launch_epoch bumps when the batch is re-pointed
 };
 
 namespace {
@@ -995,6 +997,7 @@ static skv_status batch_fill(skv_pool* p, skv_batch* b, const int32_t* group_mod
     SKV_CUDA(p, cudaEventRecord(b->stage_ev, p->stream));
   }
   b->plan_epoch = ~0ull;
+  b->launch_epoch++;
   return SKV_OK;
 }
 
@@ -1300,6 +1303,46 @@ skv_status skv_decode_attention(skv_pool* p, skv_batch* b, const skv_decode_args
   return after_data(p, s);
 }
 
+// Per-request token counts of a ragged append / prefill: lens[r] (batch order) and each
+// request's first row in its group's packed tensors go to the device ([lens | offsets]).
+// Consecutive calls with the same lengths (append then prefill of a layer, every layer of a
+// step) reuse the uploaded arrays; a new upload waits only for the previous one's copy.
+static skv_status stage_lengths(skv_pool* p, skv_batch* b, const int32_t* lens, cudaStream_t s,
+                                const int32_t** d_lens, const int32_t** d_offs) {
+  const size_t n = (size_t)b->nreq;
+  if (n > b->qlen_cap) {
+    SKV_CUDA(p, cudaStreamSynchronize(s));
+    if (b->d_qlen) cudaFree(b->d_qlen);
+    if (b->h_qlen) cudaFreeHost(b->h_qlen);
+    b->qlen_cap = std::max(b->req_cap, n);
+    SKV_CUDA(p, cudaMalloc(&b->d_qlen, 2 * b->qlen_cap * sizeof(int32_t)));
+    SKV_CUDA(p, cudaHostAlloc(&b->h_qlen, 2 * b->qlen_cap * sizeof(int32_t), cudaHostAllocMapped));
+    b->qlen_last.clear();
+  }
+  *d_lens = b->d_qlen;
+  *d_offs = b->d_qlen + b->qlen_cap;
+  if (b->qlen_last.size() == n && std::equal(lens, lens + n, b->qlen_last.begin()) && b->qlen_epoch == b->launch_epoch)
+    return SKV_OK;
+  if (b->qlen_ev) SKV_CUDA(p, cudaEventSynchronize(b->qlen_ev));  // staging buffer reuse
+  for (int g = 0; g < b->ngroups; ++g) {
+    int off = 0;
+    for (int i = 0; i < b->gsize[g]; ++i) {
+      const int r = b->gbegin[g] + i;
+      b->h_qlen[r] = lens[r];
+      b->h_qlen[b->qlen_cap + r] = off;
+      off += lens[r];
+    }
+  }
+  skv::launch_stage_copy(b->d_qlen, b->h_qlen, n * sizeof(int32_t), s);
+  skv::launch_stage_copy(b->d_qlen + b->qlen_cap, b->h_qlen + b->qlen_cap, n * sizeof(int32_t), s);
+  if (!b->qlen_ev) SKV_CUDA(p, cudaEventCreateWithFlags(&b->qlen_ev, cudaEventDisableTiming));
+  SKV_CUDA(p, cudaEventRecord(b->qlen_ev, s));
+  b->qlen_last.assign(lens, lens + n);
+  b->qlen_epoch = b->launch_epoch;
+  p->launches += 2;
+  return SKV_OK;
+}
+
 skv_status skv_batch_plan_info(skv_pool* p, skv_batch* b, int32_t* split_tokens, int64_t* n_cut,
                                int64_t* sum_hkv) {
   if (!b || b->pool != p) return fail(p, SKV_ERR_ARG, "batch belongs to another pool");
@@ -1313,7 +1356,18 @@ skv_status skv_append_kv(skv_pool* p, skv_batch* b, const skv_append_args* a, vo
   skv_status st = check_batch(p, b);
   if (st) return st;
   if (!p->split && (st = ensure_storage(p))) return st;
-  if (a->n_new < 1) return fail(p, SKV_ERR_ARG, "append: n_new must be >= 1");
+  int max_new = a->n_new;
+  if (a->n_news) {
+    max_new = 0;
+    for (int i = 0; i < b->nreq; ++i) {
+      if (a->n_news[i] < 1) return fail(p, SKV_ERR_ARG, "append: every n_news[i] must be >= 1");
+      if (p->req[b->handles[i]].tokens < a->n_news[i])
+        return fail(p, SKV_ERR_ARG, "append: request " + std::to_string(b->ids[i]) + " holds fewer than n_new tokens");
+      max_new = std::max(max_new, a->n_news[i]);
+    }
+  } else if (a->n_new < 1) {
+    return fail(p, SKV_ERR_ARG, "append: n_new must be >= 1");
+  }
   DeviceGuard guard(p->device);
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : p->stream;
   skv::DataParams dp;
@@ -1323,7 +1377,9 @@ skv_status skv_append_kv(skv_pool* p, skv_batch* b, const skv_append_args* a, vo
     dp.g[g].v = a->v[g];
   }
   dp.n_new = a->n_new;
+  dp.max_q_len = max_new;
   if ((st = order_streams(p, s))) return st;
+  if (a->n_news && b->nreq && (st = stage_lengths(p, b, a->n_news, s, &dp.q_lens, &dp.q_offs))) return st;
   if (b->nreq) {
     skv::launch_append(dp, s);
     p->launches++;
@@ -1363,31 +1419,8 @@ skv_status skv_prefill_attention(skv_pool* p, skv_batch* b, const skv_prefill_ar
   dp.n_new = a->q_len;
   dp.max_q_len = max_q;
   if (a->q_lens && b->nreq) {  // per-request lengths + row offsets within each group's q/out
-    if ((size_t)b->nreq > b->qlen_cap) {
-      SKV_CUDA(p, cudaStreamSynchronize(s));
-      if (b->d_qlen) cudaFree(b->d_qlen);
-      if (b->h_qlen) cudaFreeHost(b->h_qlen);
-      b->qlen_cap = std::max<size_t>(b->req_cap, (size_t)b->nreq);
-      SKV_CUDA(p, cudaMalloc(&b->d_qlen, 2 * b->qlen_cap * sizeof(int32_t)));
-      SKV_CUDA(p, cudaHostAlloc(&b->h_qlen, 2 * b->qlen_cap * sizeof(int32_t), cudaHostAllocMapped));
-    }
-    if (b->qlen_ev) SKV_CUDA(p, cudaEventSynchronize(b->qlen_ev));  // staging buffer reuse
-    for (int g = 0; g < b->ngroups; ++g) {
-      int off = 0;
-      for (int i = 0; i < b->gsize[g]; ++i) {
-        const int r = b->gbegin[g] + i;
-        b->h_qlen[r] = a->q_lens[r];
-        b->h_qlen[b->qlen_cap + r] = off;
-        off += a->q_lens[r];
-      }
-    }
-    skv::launch_stage_copy(b->d_qlen, b->h_qlen, b->nreq * sizeof(int32_t), s);
-    skv::launch_stage_copy(b->d_qlen + b->qlen_cap, b->h_qlen + b->qlen_cap, b->nreq * sizeof(int32_t), s);
-    if (!b->qlen_ev) SKV_CUDA(p, cudaEventCreateWithFlags(&b->qlen_ev, cudaEventDisableTiming));
-    SKV_CUDA(p, cudaEventRecord(b->qlen_ev, s));
-    dp.q_lens = b->d_qlen;
-    dp.q_offs = b->d_qlen + b->qlen_cap;
-    p->launches += 2;
+    if ((st = order_streams(p, s))) return st;
+    if ((st = stage_lengths(p, b, a->q_lens, s, &dp.q_lens, &dp.q_offs))) return st;
   }
   static const int dbg = [] {
     const char* e = getenv("SKV_PREFILL_DBG");

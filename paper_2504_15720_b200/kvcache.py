@@ -100,6 +100,11 @@ class KvOp(C.Structure):
                 ("tokens", C.c_int64)]
 
 
+# KvOp as a numpy record (same layout as the C struct skv_kv_op)
+KVOP_DTYPE = np.dtype([("kind", "<i4"), ("model", "<i4"), ("id", "<u8"), ("tokens", "<i8")])
+assert KVOP_DTYPE.itemsize == C.sizeof(KvOp)
+
+
 class Layout(C.Structure):
     _fields_ = [("merged_stride", C.c_int64), ("native_stride", C.c_int64), ("layer_stride", C.c_int64),
                 ("head_stride", C.c_int64), ("kv_stride", C.c_int64), ("tpb", C.c_int32),
@@ -115,7 +120,7 @@ class _DecodeArgs(C.Structure):
 
 class _AppendArgs(C.Structure):
     _fields_ = [("k", C.POINTER(C.c_void_p)), ("v", C.POINTER(C.c_void_p)), ("layer", C.c_int32),
-                ("n_new", C.c_int32)]
+                ("n_new", C.c_int32), ("n_news", C.POINTER(C.c_int32))]
 
 
 class _PrefillArgs(C.Structure):
@@ -417,6 +422,16 @@ class UnifiedKvCache:
         self._chk(self._lib.skv_replay(self._h, arr, len(ops), granted.ctypes.data))
         return granted[: len(ops)]
 
+    def replay_array(self, arr: np.ndarray) -> np.ndarray:
+        """Batched KvOp stream (numpy structured array of KVOP_DTYPE): one C-ABI call applies every
+        op in order with try_allocate / free_request semantics (skv_replay); returns granted
+        flags (1 granted / 0 CacheFull for grows, 0 for frees)."""
+        arr = np.ascontiguousarray(arr, dtype=KVOP_DTYPE)
+        granted = np.zeros(max(1, len(arr)), dtype=np.int32)
+        if len(arr):
+            self._chk(self._lib.skv_replay(self._h, arr.ctypes.data, len(arr), granted.ctypes.data))
+        return granted[: len(arr)]
+
     def flush(self, stream=None):
         self._chk(self._lib.skv_flush(self._h, _stream_ptr(stream)))
 
@@ -578,20 +593,44 @@ class Batch:
                                                                buf.size, C.byref(n)))
         return buf[: n.value]
 
-    def append(self, k: Sequence, v: Sequence, layer: int, n_new: int = 1, stream=None):
+    def append(self, k: Sequence, v: Sequence, layer: int, n_new=1, stream=None):
+        """Writes each request's last ``n_new`` tokens' K/V of ``layer``.  ``n_new``: one int
+        (k/v of group g: [B_g, n_new, Hkv, d]) or one count per request in batch order (k/v of
+        group g packed by request: [sum of its counts, Hkv, d])."""
         self.cache._chk(self.cache._lib.skv_append_kv(self.cache._h, self._h, C.byref(self._append_args(k, v, layer,
                                                                                                        n_new)),
                                                       _stream_ptr(stream)))
 
+    def _ragged_shapes(self, lens, what, heads):
+        lens = [int(x) for x in lens]
+        total = sum(B for B, _, _, _ in self._shapes)
+        if len(lens) != total:
+            raise ArgError(f"{what}: {len(lens)} lengths for {total} requests")
+        shp, k = [], 0
+        for B, Hq, Hkv, d in self._shapes:
+            shp.append((sum(lens[k:k + B]), Hq if heads == "q" else Hkv, d))
+            k += B
+        return lens, shp
+
     def _append_args(self, k, v, layer, n_new):
         dt, dev = self.cache.dtype, self.cache.device
-        _check_tensors(k, [(B, n_new, Hkv, d) for B, _, Hkv, d in self._shapes], dt, dev, "append k")
-        _check_tensors(v, [(B, n_new, Hkv, d) for B, _, Hkv, d in self._shapes], dt, dev, "append v")
+        ragged = not isinstance(n_new, (int, np.integer))
+        if ragged:
+            lens, shp = self._ragged_shapes(n_new, "append", "kv")
+        else:
+            shp = [(B, int(n_new), Hkv, d) for B, _, Hkv, d in self._shapes]
+        _check_tensors(k, shp, dt, dev, "append k")
+        _check_tensors(v, shp, dt, dev, "append v")
         n = len(self.groups)
         ka = (C.c_void_p * n)(*[_ptr(t) for t in k])
         va = (C.c_void_p * n)(*[_ptr(t) for t in v])
-        a = _AppendArgs(C.cast(ka, C.POINTER(C.c_void_p)), C.cast(va, C.POINTER(C.c_void_p)), layer, n_new)
+        a = _AppendArgs(C.cast(ka, C.POINTER(C.c_void_p)), C.cast(va, C.POINTER(C.c_void_p)), layer,
+                        0 if ragged else int(n_new))
         a._keep = (ka, va)
+        if ragged:
+            arr = (C.c_int32 * max(1, len(lens)))(*lens)
+            a.n_news = C.cast(arr, C.POINTER(C.c_int32))
+            a._keep = (ka, va, arr)
         return a
 
     def prefill(self, q: Sequence, out: Sequence, layer: int, q_len, softmax_scale: float = 0.0,
@@ -604,13 +643,7 @@ class Batch:
         n = len(self.groups)
         ragged = not isinstance(q_len, (int, np.integer))
         if ragged:
-            lens = [int(x) for x in q_len]
-            if len(lens) != sum(B for B, _, _, _ in self._shapes):
-                raise ArgError(f"prefill: {len(lens)} q_lens for {sum(B for B, _, _, _ in self._shapes)} requests")
-            shp, k = [], 0
-            for B, Hq, _, d in self._shapes:
-                shp.append((sum(lens[k:k + B]), Hq, d))
-                k += B
+            lens, shp = self._ragged_shapes(q_len, "prefill", "q")
             ql = (C.c_int32 * max(1, len(lens)))(*lens)
         else:
             shp = [(B, int(q_len), Hq, d) for B, Hq, _, d in self._shapes]

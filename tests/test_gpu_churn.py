@@ -105,3 +105,70 @@ def test_churn_warm_start_reaches_target_and_replays_bit_exact():
     for rid in eng.running:
         assert np.array_equal(cache.block_table_np(rid), oracle.block_table_np(rid))
     assert cache.stats() == oracle.stats()
+
+
+def test_churn_preemption_reprefill_replays_bit_exact():
+    """Pool sized so decode growth runs into CacheFull: victims are freed,
+    re-queued and re-prefilled from token 0 (simulation.hpp:144-157,333-340); every prefill
+    chunk of an iteration runs as one ragged launch per layer.  The whole recorded op stream
+    replays through the oracle bit-exact, and a decode over the final running set (including
+    re-prefilled requests) matches the fp32 oracle."""
+    shapes = [(2, 4, 16), (3, 8, 8)]
+    models = [P.ModelSpec(f"m{i}", L, H, 128, 2, Hq) for i, (L, H, Hq) in enumerate(shapes)]
+    pool = 40
+    cache = P.UnifiedKvCache(models, 16, 1, pool, allocate_storage=True)
+    s = torch.cuda.Stream()
+    torch.cuda.set_stream(s)
+    cache.set_stream(s)
+    cache.synth_fill(8, 1.0, s)
+    prof = [ServiceProfile("chat0", 0, 60, 30, 150, 20), ServiceProfile("summ0", 0, 300, 50, 40, 10),
+            ServiceProfile("chat1", 1, 50, 20, 150, 20), ServiceProfile("summ1", 1, 200, 40, 40, 10)]
+    trace = generate_trace(prof, rate=20.0, duration=30.0, skewness=2, seed=21)
+    eng = ChurnEngine(cache, shapes, prof, chunk=48, occupancy=0.95, max_decode=64, max_prefill=4, stream=s)
+    t, k = 0.0, 0
+    for _ in range(600):  # until preemptions, re-prefills and completions have all happened
+        t += 0.04
+        new = []
+        while k < len(trace) and trace[k].t <= t:
+            new.append(trace[k])
+            k += 1
+        eng.add_arrivals(new)
+        eng.step()
+        st = eng.stats
+        if st["preemptions"] > 0 and st["reprefilled"] > 0 and st["finished"] > 5:
+            break
+    summ = eng.summary()
+    assert summ["preemptions"] > 0 and summ["reprefilled"] > 0, summ
+    assert summ["finished"] > 5
+    oracle = O.OracleCache([(L, H, 128, 2) for L, H, _ in shapes], pool=pool)
+    for kind, rid, m, tok in eng.ops:
+        if kind == 0:
+            oracle.try_allocate(rid, m, tok)
+        else:
+            oracle.free_request(rid)
+    for rid in eng.running:
+        assert np.array_equal(cache.block_table_np(rid), oracle.block_table_np(rid))
+    assert cache.stats() == oracle.stats() and cache.free_blocks() == oracle.free_blocks()
+    # decode over every running request (current contexts) against the oracle
+    groups = [(m, [r.rid for r in eng.running.values() if r.model == m and cache.request_tokens(r.rid) > 0])
+              for m in range(2)]
+    groups = [g for g in groups if g[1]]
+    b = cache.batch(groups)
+    g = torch.Generator(device="cuda").manual_seed(2)
+    qs = [torch.rand((len(ids), shapes[m][2], 128), generator=g, device="cuda").half() for m, ids in groups]
+    outs = [torch.empty_like(q) for q in qs]
+    b.decode(qs, outs, 1)
+    torch.cuda.synchronize()
+    img = cache.read_blocks(np.arange(pool, dtype=np.int32))
+    for (m, ids), q, o in zip(groups, qs, outs):
+        lay = cache.layout(m)
+        olay = O.layout(lay.merged_stride, lay.native_stride, lay.layer_stride, lay.head_stride, lay.kv_stride, 16,
+                        128, lay.kv_heads, lay.q_heads, lay.phys_layers, 0)
+        tabs = [cache.block_table_np(i) for i in ids]
+        tt = np.zeros((len(ids), max(len(x) for x in tabs), 2), np.int32)
+        for j, x in enumerate(tabs):
+            tt[j, :len(x)] = x
+        ctx = np.array([cache.request_tokens(i) for i in ids], np.int64)
+        ref = O.decode_attention(olay, img, 1, tt, ctx, q.view(torch.int16).cpu().numpy().view(np.uint16),
+                                 1 / np.sqrt(128.0))
+        assert np.abs(o.float().cpu().numpy() - ref).max() <= 2e-3

@@ -259,3 +259,35 @@ def test_prefill_randomised_head_dims(seed):
         ctxs.append(cl)
         lens += [int(rng.integers(1, c + 1)) for c in cl]
     prefill_check(shapes, ctxs, lens, layer=1, dtype=P.BF16 if seed == 2 else P.FP16, seed=seed)
+
+
+def test_append_ragged_counts_byte_exact():
+    """skv_append_args.n_news: each request appends its own number of tokens in one launch
+    (k / v packed by request), byte-exact against the oracle scatter."""
+    shapes = [(3, 4, 8, 64), (3, 2, 2, 256), (3, 4, 4, 128)]
+    ctxs = [[40, 7], [16, 33], [50]]
+    cache, groups, _ = build(shapes, ctxs)
+    b = cache.batch(groups)
+    g = torch.Generator(device="cuda").manual_seed(19)
+    counts = [17, 3, 16, 1, 50]  # batch order
+    before = image(cache)
+    ks, vs, k = [], [], 0
+    for (m, ids), (L, H, Hq, d) in zip(groups, shapes):
+        n = sum(counts[k:k + len(ids)])
+        k += len(ids)
+        ks.append((torch.rand((n, H, d), generator=g, device="cuda") - 0.5).half())
+        vs.append((torch.rand((n, H, d), generator=g, device="cuda") - 0.5).half())
+    b.append(ks, vs, 1, counts)
+    torch.cuda.synchronize()
+    after = image(cache)
+    k = 0
+    for (m, ids), kk, vv in zip(groups, ks, vs):
+        off = 0
+        for i in ids:
+            n = counts[k]
+            k += 1
+            pos = np.array([cache.request_tokens(i) - n], np.int64)
+            O.append(olay(cache, m), before, 1, tables(cache, [i]), pos, u16(kk[off:off + n][None]),
+                     u16(vv[off:off + n][None]))
+            off += n
+    assert np.array_equal(before, after)
