@@ -256,19 +256,25 @@ def step_device(batch, q, out, k, v, stream, nlayers, epilogue=None, timed=False
 
 
 def capture_step_graph(torch, cache, batch, q, out, k, v, stream, nlayers):
-    """CUDA graph of one step's device work after the host-side grow: the decode plan
-    kernel, then per layer the fused append + decode launch.  The allocator grow of each
-    step (host admission + GPU placement kernel) stays outside and is flushed before
-    every replay.  Returns None if capture is not possible."""
+    """CUDA graph of one decode step's whole device work: the allocator's device half (decode-
+    step grow ops generated on the device from its own request state + the placement kernel,
+    skv_batch_grow_launch), the decode plan kernel, then per layer the fused append + decode
+    launch.  Each replay follows the host mirror of the same step (batch.grow_mirror(1): the
+    exact try_allocate answers and CacheStats, no upload).  Returns None if capture is not
+    possible."""
     try:
-        batch.grow(1)
-        cache.flush(stream)
+        assert batch.grow_mirror(1), "decode step not fully granted"
+        batch.grow_launch(1, stream=stream)  # eager once: sizes the batch's grow buffers
+        for layer in range(nlayers):
+            batch.decode(q, out, layer, stream=stream, k=k, v=v)
         torch.cuda.synchronize()
+        assert batch.grow_mirror(1), "decode step not fully granted"
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=stream):
+            batch.grow_launch(1, stream=stream)
             for layer in range(nlayers):
                 batch.decode(q, out, layer, stream=stream, k=k, v=v)
-        g.replay()  # the captured step's attention
+        g.replay()  # the captured step
         torch.cuda.synchronize()
         return g
     except Exception as e:  # noqa: BLE001 - report and fall back to eager launches
@@ -395,9 +401,10 @@ def run_gpu(args):
         t0.record(stream)
         for st in range(args.steps):  # no host sync inside the timed region
             if graph is not None:
-                batch.grow(1)
-                cache.flush(stream)
-                graph.replay()
+                if batch.grow_mirror(1):  # host mirror; the device half is in the graph
+                    graph.replay()
+                else:  # CacheFull somewhere: the per-request host path, eager launches
+                    step_device(batch, q, out, k, v, stream, NLAYERS, tp_epilogue, timed=True)
             else:
                 step_device(batch, q, out, k, v, stream, NLAYERS, tp_epilogue, timed=True)
             kvb, totb = step_bytes(batch, NLAYERS)  # host mirror: exact context of this step
@@ -408,7 +415,7 @@ def run_gpu(args):
     launches_timed = cache.kernel_launches() - launches0
     graph_launches = 0
     if graph is not None:  # the graph's kernels bypass the pool's launch counter
-        graph_launches = args.steps * (NLAYERS + 1)
+        graph_launches = args.steps * (NLAYERS + 3)  # step-op generation, placement, plan, decodes
     # per-launch decode timing for the roofline: a CUDA graph of the step's NLAYERS fused
     # append+decode launches (same contexts, no grow; re-appending the same token is
     # idempotent) replayed back to back on the launching stream, bracketed by events
@@ -441,10 +448,40 @@ def run_gpu(args):
     traffic, traffic_src = profiled_traffic(wl, args)
     layer0_bytes = batch.decode_bytes(0)[1]
 
-    # ---- allocator: decode-step growth of the whole batch (host mirror + GPU placement) ---
+    # ---- allocator: decode-step growth of the whole batch ----------------------------------
+    # (a) the step path: host mirror (exact try_allocate answers + CacheStats, no upload) and
+    #     the device half (op generation + placement kernel) as the graph runs it
     torch.cuda.synchronize()
-    a0 = time.perf_counter()
     na = 16
+    n_ops = na * sum(len(c) for c in wl.ctxs)
+    dev_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(na)]
+    host_s = 0.0
+    gg = None
+    try:  # the device half timed as the step graph runs it (graph replay, no host launch gaps)
+        assert batch.grow_mirror(1)
+        batch.grow_launch(1, stream=stream)
+        torch.cuda.synchronize()
+        gg = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gg, stream=stream):
+            batch.grow_launch(1, stream=stream)
+    except Exception as e:  # noqa: BLE001
+        print(f"# allocator graph unavailable: {e}", file=sys.stderr)
+    for i in range(na):
+        h0 = time.perf_counter()
+        ok = batch.grow_mirror(1)
+        host_s += time.perf_counter() - h0
+        assert ok
+        dev_ev[i][0].record(stream)
+        if gg is not None:
+            gg.replay()
+        else:
+            batch.grow_launch(1, stream=stream)
+        dev_ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    mirror_ns = host_s / n_ops * 1e9
+    device_ns = sum(e0.elapsed_time(e1) for e0, e1 in dev_ev) * 1e6 / n_ops
+    # (b) the per-request host path (any CacheFull case): host mirror + op upload + placement
+    a0 = time.perf_counter()
     aev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(na)]
     for i in range(na):
         batch.grow(1)  # host mirror: the grant / CacheFull answer, no device round trip
@@ -452,7 +489,6 @@ def run_gpu(args):
         cache.flush(stream)  # GPU placement: op upload + grow_kernel
         aev[i][1].record(stream)
     torch.cuda.synchronize()
-    n_ops = na * sum(len(c) for c in wl.ctxs)
     alloc_ns = (time.perf_counter() - a0) / n_ops * 1e9
     alloc_gpu_ns = sum(e0.elapsed_time(e1) for e0, e1 in aev) * 1e6 / n_ops
 
@@ -579,9 +615,13 @@ def run_gpu(args):
                      "timing": f"CUDA events around {nrep} replays of a graph of the step's {NLAYERS} decode "
                                "launches (inter-kernel gaps included)",
                      "bytes_per_launch": round(dec_bytes / n_launch, 1)},
-        "allocator": {"ns_per_grow_op": round(alloc_ns, 2), "gpu_ns_per_grow_op": round(alloc_gpu_ns, 2),
-                      "note": "ns_per_grow_op: batch.grow(1) of every request (host mirror) + flush (op upload + "
-                              "grow_kernel), wall clock incl. sync; gpu_ns_per_grow_op: CUDA events around the flush"},
+        "allocator": {"ns_per_grow_op": round(mirror_ns + device_ns, 2), "host_mirror_ns_per_op": round(mirror_ns, 2),
+                      "device_ns_per_op": round(device_ns, 2),
+                      "host_path_ns_per_grow_op": round(alloc_ns, 2), "host_path_gpu_ns_per_grow_op": round(alloc_gpu_ns, 2),
+                      "note": "ns_per_grow_op = host mirror (skv_batch_grow_mirror, wall) + device half "
+                              "(skv_batch_grow_launch: op generation + placement kernel, CUDA events) per decode-step "
+                              "grow op, the path the step graph runs; host_path_*: batch.grow(1) + flush (op upload + "
+                              "grow_kernel) wall incl. sync, the fallback when a step hits CacheFull"},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }

@@ -154,6 +154,18 @@ skv_status skv_batch_reset(skv_pool* p, skv_batch* b, const int32_t* group_model
 /* Decode-step growth: try_allocate(id, model, tokens + delta) for every request of
  * the batch, in batch order.  *n_granted = number granted (may be NULL). */
 skv_status skv_batch_grow(skv_pool* p, skv_batch* b, int64_t delta_tokens, int32_t* n_granted);
+/* Decode-step growth with the placement generated on the device (no op upload; the device
+ * half can be captured in a CUDA graph together with the step's attention launches):
+ *  - skv_batch_grow_mirror: the host mirror of try_allocate(id, model, tokens + delta) for
+ *    every request of the batch, applied only when ALL of them are granted and every request
+ *    already owns slots (*all_granted = 1); otherwise nothing changes (*all_granted = 0: use
+ *    skv_batch_grow, which handles CacheFull per request);
+ *  - skv_batch_grow_launch: the device half (op generation from the device's request state
+ *    + the placement kernel) on `stream`.  Call (or replay a graph of) it exactly once after
+ *    each successful mirror call with the same delta; its buffers are the batch's own and are
+ *    sized by the first eager call (capture before that is refused). */
+skv_status skv_batch_grow_mirror(skv_pool* p, skv_batch* b, int64_t delta, int32_t* all_granted);
+skv_status skv_batch_grow_launch(skv_pool* p, skv_batch* b, int64_t delta, void* stream);
 /* Sum over the batch of the attended context tokens x kv-heads x 2 x head_dim x dtype
  * bytes for one layer index (the algorithmic K/V bytes a decode launch must read). */
 skv_status skv_batch_decode_bytes(skv_pool* p, skv_batch* b, int32_t layer, double* kv_bytes,

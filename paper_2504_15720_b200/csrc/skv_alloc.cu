@@ -251,12 +251,34 @@ grow_kernel(DevAlloc st, AllocParams pr, const GrowOp* __restrict__ ops, int n, 
     atomicMax(&st.req_nslots[op.handle], op.have + op.claims);
     atomicMax(&st.req_tokens[op.handle], op.tokens_after);
     st.req_model[op.handle] = op.model;
+    st.req_id[op.handle] = op.id;
   }
   if (tid < M) {
     st.open[tid] = O[tid] + (long long)newcnt[tid] * pr.sub[tid] - carryC[tid];
   }
   if (tid == 0) st.free_count[0] -= Nnew;
   (void)Tcl;
+}
+
+// Decode-step grow ops from the device's own request state (no host upload): the host mirror
+// has already applied the same try_allocate(+delta) calls and found every one granted.
+__global__ void step_ops_kernel(DevAlloc st, int tpb, const int32_t* __restrict__ handles,
+                                const int32_t* __restrict__ group, StepModels gm, int n, int delta,
+                                GrowOp* __restrict__ ops) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int h = handles[i];
+  const int have = st.req_nslots[h];
+  const int tok = st.req_tokens[h] + delta;
+  GrowOp op;
+  op.handle = h;
+  op.model = gm.m[group[i]];
+  op.have = have;
+  op.claims = max(0, (tok + tpb - 1) / tpb - have);
+  op.tokens_after = tok;
+  op.pad = 0;
+  op.id = st.req_id[h];
+  ops[i] = op;
 }
 
 // Release every slot of the freed requests (kv_cache.hpp:224-240).  One warp per
@@ -399,6 +421,12 @@ void launch_split_release(const SplitOp* ops, int n, long long total, int32_t* s
   if (total <= 0) return;
   const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 8);
   split_release_kernel<<<blocks, 256, 0, s>>>(ops, n, total, stack, table, Lmax, Hmax, cap);
+}
+
+void launch_step_ops(const DevAlloc& st, int tpb, const int32_t* handles, const int32_t* group, StepModels gm,
+                     int n, int delta, GrowOp* ops, cudaStream_t s) {
+  if (n <= 0) return;
+  step_ops_kernel<<<(n + 255) / 256, 256, 0, s>>>(st, tpb, handles, group, gm, n, delta, ops);
 }
 
 void launch_grow(const DevAlloc& st, const AllocParams& pr, const GrowOp* ops, int n,

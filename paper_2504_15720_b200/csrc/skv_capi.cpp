@@ -89,6 +89,7 @@ struct skv_pool {
   uint64_t peak_entries = 0, rw = 0;
   long long slot_frag = 0, token_waste = 0, peak_frag = 0, peak_used = 0;
   uint64_t token_epoch = 0;
+  uint64_t free_epoch = 1;  // bumped by every free_request (batches re-check their ids after one)
 
   // queued device work
   std::vector<skv::GrowOp> grow_ops;
@@ -160,7 +161,11 @@ struct skv_batch {
   size_t qlen_cap = 0;
   cudaEvent_t qlen_ev = nullptr;
   std::vector<int32_t> qlen_last;  // lengths currently on the device (skip identical re-uploads)
+  skv::GrowOp* d_gops = nullptr;   // device-generated decode-step grow ops [gops_cap]
+  skv::GrowScratch gscr{};         // their placement scratch (per batch: stable for CUDA graphs)
+  size_t gops_cap = 0, gscr_t = 0;
   uint64_t qlen_epoch = 0, launch_epoch = 1;  // launch_epoch bumps when the batch is re-pointed
+  uint64_t checked_epoch = 0;  // pool free_epoch at the last full id check (check_batch)
 };
 
 namespace {
@@ -385,6 +390,11 @@ skv_status grow_tables(skv_pool* p, long long rows, long long cap) {
   skv::DevAlloc& d = p->dev;
   int2* tab = nullptr;
   int32_t *ns = nullptr, *tk = nullptr, *md = nullptr;
+  unsigned long long* ids = nullptr;
+  SKV_CUDA(p, cudaMalloc(&ids, (size_t)nR * sizeof(unsigned long long)));
+  SKV_CUDA(p, cudaMemsetAsync(ids, 0, (size_t)nR * sizeof(unsigned long long), p->stream));
+  SKV_CUDA(p, cudaMemcpyAsync(ids, d.req_id, (size_t)p->R * sizeof(unsigned long long), cudaMemcpyDeviceToDevice,
+                              p->stream));
   SKV_CUDA(p, cudaMalloc(&tab, (size_t)nR * ncap * sizeof(int2)));
   SKV_CUDA(p, cudaMalloc(&ns, (size_t)nR * sizeof(int32_t)));
   SKV_CUDA(p, cudaMalloc(&tk, (size_t)nR * sizeof(int32_t)));
@@ -403,6 +413,8 @@ skv_status grow_tables(skv_pool* p, long long rows, long long cap) {
   cudaFree(d.req_nslots);
   cudaFree(d.req_tokens);
   cudaFree(d.req_model);
+  cudaFree(d.req_id);
+  d.req_id = ids;
   d.req_table = tab;
   d.req_nslots = ns;
   d.req_tokens = tk;
@@ -415,8 +427,9 @@ skv_status grow_tables(skv_pool* p, long long rows, long long cap) {
   return SKV_OK;
 }
 
-// try_allocate (kv_cache.hpp:104-123) on the host mirror; queues the claims.
-skv_status grow_handle_impl(skv_pool* p, int h, uint64_t id, int m, long long tokens);
+// try_allocate (kv_cache.hpp:104-123) on the host mirror; queues the claims (queue = false: the
+// device generates the same op itself, skv_batch_grow_launch).
+skv_status grow_handle_impl(skv_pool* p, int h, uint64_t id, int m, long long tokens, bool queue = true);
 
 skv_status try_allocate_impl(skv_pool* p, uint64_t id, int m, long long tokens) {
   if (tokens < 0) return fail(p, SKV_ERR_VALIDATION, "allocate: negative tokens_needed");
@@ -445,7 +458,7 @@ skv_status try_allocate_impl(skv_pool* p, uint64_t id, int m, long long tokens) 
 
 // try_allocate for a registered request whose handle is known (the batch path skips the
 // id -> handle lookup)
-skv_status grow_handle_impl(skv_pool* p, int h, uint64_t id, int m, long long tokens) {
+skv_status grow_handle_impl(skv_pool* p, int h, uint64_t id, int m, long long tokens, bool queue) {
   ReqHost& r = p->req[h];
   if (r.nslots == 0) r.model = m;
   if (r.model != m) return fail(p, SKV_ERR_LOGIC, "allocate: request changed model");
@@ -484,7 +497,8 @@ skv_status grow_handle_impl(skv_pool* p, int h, uint64_t id, int m, long long to
   // Net waste change incl. quirk Q1: every claim leaks native bytes into the waste term.
   p->token_waste += entry_waste(p, r) - w0 + c * mi.native;
   note_watermarks(p);
-  if (c > 0 || grew_tokens) {
+  if (c > 0 || grew_tokens) p->token_epoch++;
+  if (queue && (c > 0 || grew_tokens)) {
     skv::GrowOp op{};
     op.handle = h;
     op.model = m;
@@ -493,7 +507,6 @@ skv_status grow_handle_impl(skv_pool* p, int h, uint64_t id, int m, long long to
     op.tokens_after = (int)r.tokens;
     op.id = id;
     queue_grow(p, op);
-    p->token_epoch++;
   }
   return SKV_OK;
 }
@@ -517,6 +530,7 @@ skv_status free_impl(skv_pool* p, uint64_t id) {  // kv_cache.hpp:126-134
   r = ReqHost();
   p->free_handles.push_back(h);
   p->token_epoch++;
+  p->free_epoch++;
   return SKV_OK;
 }
 
@@ -703,7 +717,8 @@ skv_status skv_pool_create(const skv_model_desc* models, int32_t n, int32_t tpb,
       (st = dev_alloc(p, &d.slot_owner, pool_blocks * p->maxsub)) || (st = dev_alloc(p, &d.open, n)) ||
       (st = dev_alloc(p, &d.free_count, 1)) || (st = dev_alloc(p, &d.req_table, (size_t)p->R * p->cap, false)) ||
       (st = dev_alloc(p, &d.req_nslots, p->R)) || (st = dev_alloc(p, &d.req_tokens, p->R)) ||
-      (st = dev_alloc(p, &d.req_model, p->R, false)) || (st = dev_alloc(p, &d.status, 1)) ||
+      (st = dev_alloc(p, &d.req_model, p->R, false)) || (st = dev_alloc(p, &d.req_id, p->R)) ||
+      (st = dev_alloc(p, &d.status, 1)) ||
       (st = dev_alloc(p, &d.free_E, n)) || (st = dev_alloc(p, &d.free_R, n)) ||
       (st = dev_alloc(p, &p->d_outE, (size_t)kResultSlots * n)))
     return bail(st);
@@ -739,7 +754,7 @@ void skv_pool_destroy(skv_pool* p) {
   skv::DevAlloc& d = p->dev;
   for (void* q : {(void*)d.free_bits, (void*)d.partial_bits, (void*)d.blk_model, (void*)d.blk_occ,
                   (void*)d.slot_owner, (void*)d.open, (void*)d.free_count, (void*)d.req_table,
-                  (void*)d.req_nslots, (void*)d.req_tokens, (void*)d.req_model, (void*)d.status,
+                  (void*)d.req_nslots, (void*)d.req_tokens, (void*)d.req_model, (void*)d.req_id, (void*)d.status,
                   (void*)d.free_E, (void*)d.free_R, (void*)p->d_outE, p->d_ops, p->storage,
                   (void*)p->scr.S, (void*)p->scr.cbeg, (void*)p->scr.nnew, (void*)p->scr.base,
                   (void*)p->scr.nbfirst, (void*)p->scr.newblk, (void*)p->scr.newrank, (void*)p->scr.openlist})
@@ -998,6 +1013,7 @@ static skv_status batch_fill(skv_pool* p, skv_batch* b, const int32_t* group_mod
   }
   b->plan_epoch = ~0ull;
   b->launch_epoch++;
+  b->checked_epoch = p->free_epoch;  // ids were just resolved against the registry
   return SKV_OK;
 }
 
@@ -1034,16 +1050,21 @@ void skv_batch_destroy(skv_batch* b) {
   if (b->d_qlen) cudaFree(b->d_qlen);
   if (b->h_qlen) cudaFreeHost(b->h_qlen);
   if (b->qlen_ev) cudaEventDestroy(b->qlen_ev);
+  for (void* q : {(void*)b->d_gops, (void*)b->gscr.S, (void*)b->gscr.cbeg, (void*)b->gscr.nnew, (void*)b->gscr.base,
+                  (void*)b->gscr.nbfirst, (void*)b->gscr.newblk, (void*)b->gscr.newrank, (void*)b->gscr.openlist})
+    if (q) cudaFree(q);
   delete b;
 }
 
 static skv_status check_batch(skv_pool* p, skv_batch* b) {
   if (!b || b->pool != p) return fail(p, SKV_ERR_ARG, "batch belongs to another pool");
+  if (b->checked_epoch == p->free_epoch) return SKV_OK;  // no free since the last full check
   for (int i = 0; i < b->nreq; ++i) {
     auto it = p->id2h.find(b->ids[i]);
     if (it == p->id2h.end() || it->second != b->handles[i])
       return fail(p, SKV_ERR_LOGIC, "batch: request " + std::to_string(b->ids[i]) + " was freed");
   }
+  b->checked_epoch = p->free_epoch;
   return SKV_OK;
 }
 
@@ -1065,6 +1086,86 @@ skv_status skv_batch_grow(skv_pool* p, skv_batch* b, int64_t delta, int32_t* n_g
   }
   if (n_granted) *n_granted = granted;
   return SKV_OK;
+}
+
+static skv_status order_streams(skv_pool* p, cudaStream_t s);
+static skv_status after_data(skv_pool* p, cudaStream_t s);
+
+// Decode-step growth with device-generated ops.  Host side: the exact mirror of
+// try_allocate(id, model, tokens + delta) for every request in batch order, applied only if
+// ALL are granted (the sequential claims of model m need ceil(max(0, C_m - open_m) / sub_m)
+// fresh blocks in total, so all-granted <=> their sum <= free blocks) and every request
+// already owns slots (its id is on the device).  Otherwise nothing changes.
+skv_status skv_batch_grow_mirror(skv_pool* p, skv_batch* b, int64_t delta, int32_t* all_granted) {
+  *all_granted = 0;
+  skv_status st = check_batch(p, b);
+  if (st) return st;
+  if (delta < 0) return fail(p, SKV_ERR_VALIDATION, "allocate: negative tokens_needed");
+  if ((st = ensure_counters(p))) return st;
+  long long C[skv::kMaxModels] = {0};
+  long long max_need = 0;
+  for (int g = 0; g < b->ngroups; ++g) {
+    const int m = b->gmodel[g];
+    for (int i = 0; i < b->gsize[g]; ++i) {
+      const ReqHost& r = p->req[b->handles[b->gbegin[g] + i]];
+      if (!r.live || r.nslots == 0 || r.model != m) return SKV_OK;  // host path handles these
+      const long long need = ceil_div_ll(r.tokens + delta, p->tpb);
+      C[m] += std::max(0LL, need - r.nslots);
+      max_need = std::max(max_need, need);
+    }
+  }
+  long long blocks = 0;
+  for (int m = 0; m < p->M; ++m)
+    blocks += C[m] > p->open[m] ? ceil_div_ll(C[m] - p->open[m], p->models[m].sub) : 0;
+  if (blocks > p->free_count || max_need > p->cap) return SKV_OK;
+  for (int g = 0; g < b->ngroups; ++g)
+    for (int i = 0; i < b->gsize[g]; ++i) {
+      const int r = b->gbegin[g] + i;
+      if ((st = grow_handle_impl(p, b->handles[r], b->ids[r], b->gmodel[g], p->req[b->handles[r]].tokens + delta,
+                                 /*queue=*/false)))
+        return st;  // cannot happen after the check above
+    }
+  *all_granted = 1;
+  return SKV_OK;
+}
+
+// The device half: op generation from the device's request state + the placement kernel, on
+// `stream` (capturable in a CUDA graph: every buffer is the batch's own).
+skv_status skv_batch_grow_launch(skv_pool* p, skv_batch* b, int64_t delta, void* stream) {
+  skv_status st = check_batch(p, b);
+  if (st) return st;
+  if (delta < 0 || delta > (1 << 20)) return fail(p, SKV_ERR_ARG, "grow_launch: delta out of range");
+  DeviceGuard guard(p->device);
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : p->stream;
+  const size_t n = (size_t)b->nreq;
+  if (!n) return SKV_OK;
+  const size_t t = n * (size_t)(ceil_div_ll(delta, p->tpb) + 1);  // claims bound
+  if (n > b->gops_cap || t > b->gscr_t) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cs);
+    if (cs != cudaStreamCaptureStatusNone)
+      return fail(p, SKV_ERR_ARG, "grow_launch: buffers must be sized by an eager call before graph capture");
+    SKV_CUDA(p, cudaStreamSynchronize(s));
+    skv::GrowScratch& g = b->gscr;
+    for (void* q : {(void*)b->d_gops, (void*)g.S, (void*)g.cbeg, (void*)g.nnew, (void*)g.base, (void*)g.nbfirst,
+                    (void*)g.newblk, (void*)g.newrank, (void*)g.openlist})
+      if (q) cudaFree(q);
+    b->gops_cap = n;
+    b->gscr_t = t;
+    if ((st = dev_alloc(p, &b->d_gops, n, false)) || (st = dev_alloc(p, &g.S, n, false)) ||
+        (st = dev_alloc(p, &g.cbeg, n, false)) || (st = dev_alloc(p, &g.nnew, n, false)) ||
+        (st = dev_alloc(p, &g.base, n, false)) || (st = dev_alloc(p, &g.nbfirst, n, false)) ||
+        (st = dev_alloc(p, &g.newblk, t, false)) || (st = dev_alloc(p, &g.newrank, t, false)) ||
+        (st = dev_alloc(p, &g.openlist, t, false)))
+      return st;
+  }
+  if ((st = order_streams(p, s))) return st;  // queued host-side allocator work first
+  skv::StepModels gm{};
+  for (int g = 0; g < b->ngroups; ++g) gm.m[g] = b->gmodel[g];
+  skv::launch_step_ops(p->dev, p->tpb, b->d_handles, b->d_group, gm, (int)n, (int)delta, b->d_gops, s);
+  skv::launch_grow(p->dev, p->prm, b->d_gops, (int)n, b->gscr, s);
+  p->launches += 2;
+  return after_data(p, s);
 }
 
 skv_status skv_batch_decode_bytes(skv_pool* p, skv_batch* b, int32_t layer, double* kv_bytes,

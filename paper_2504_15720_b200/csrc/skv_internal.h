@@ -47,6 +47,7 @@ struct DevAlloc {
   int32_t* req_nslots;           // [R]
   int32_t* req_tokens;           // [R]     tokens covered (decode context length)
   int32_t* req_model;            // [R]
+  unsigned long long* req_id;    // [R]     request id of the handle (written by every grow)
   int32_t* status;               // [1]     device invariant violations (0 = ok)
   int32_t* free_E;               // [M]     scratch: blocks emptied by the current free run
   int32_t* free_R;               // [M]     scratch: slots released by the current free run
@@ -83,6 +84,13 @@ struct GrowScratch {
 };
 
 void launch_stage_copy(void* dst, const void* src_host_mapped, size_t bytes, cudaStream_t s);
+// Decode-step growth generated on the device: op i = try_allocate(req_id[h], model, tokens + delta)
+// of batch request i (h = handles[i], model = group_model[group[i]]), written to ops[i].
+struct StepModels {
+  int m[kMaxGroups];
+};
+void launch_step_ops(const DevAlloc& st, int tpb, const int32_t* handles, const int32_t* group, StepModels gm,
+                     int n, int delta, GrowOp* ops, cudaStream_t s);
 void launch_grow(const DevAlloc& st, const AllocParams& pr, const GrowOp* ops, int n,
                  const GrowScratch& sc, cudaStream_t s);
 void launch_free(const DevAlloc& st, const AllocParams& pr, const FreeOp* ops, int n,

@@ -187,6 +187,8 @@ def lib() -> C.CDLL:
         "skv_batch_reset": (S, [P, P, P, P, C.c_int32, P]),
         "skv_batch_grow": (S, [P, P, C.c_int64, C.POINTER(C.c_int32)]),
         "skv_batch_decode_bytes": (S, [P, P, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+        "skv_batch_grow_mirror": (S, [P, P, C.c_int64, C.POINTER(C.c_int32)]),
+        "skv_batch_grow_launch": (S, [P, P, C.c_int64, P]),
         "skv_decode_attention": (S, [P, P, C.POINTER(_DecodeArgs), P]),
         "skv_batch_plan_info": (S, [P, P, C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
         "skv_append_kv": (S, [P, P, C.POINTER(_AppendArgs), P]),
@@ -536,6 +538,17 @@ class Batch:
         n = C.c_int32()
         self.cache._chk(self.cache._lib.skv_batch_grow(self.cache._h, self._h, delta, C.byref(n)))
         return n.value
+
+    def grow_mirror(self, delta: int = 1) -> bool:
+        """Host half of a device-generated decode-step growth (skv_batch_grow_mirror): True when
+        every request was granted and the mirror advanced; False = nothing changed."""
+        ok = C.c_int32()
+        self.cache._chk(self.cache._lib.skv_batch_grow_mirror(self.cache._h, self._h, delta, C.byref(ok)))
+        return bool(ok.value)
+
+    def grow_launch(self, delta: int = 1, stream=None):
+        """Device half (op generation + placement kernel), once per successful grow_mirror."""
+        self.cache._chk(self.cache._lib.skv_batch_grow_launch(self.cache._h, self._h, delta, _stream_ptr(stream)))
 
     def decode_bytes(self, layer: int) -> tuple[float, float]:
         kv, tot = C.c_double(), C.c_double()

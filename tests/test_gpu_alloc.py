@@ -280,3 +280,109 @@ def test_reference_simulator_identical_with_gpu_cache(args):
     if len(args) > 3:  # B200-measured decode attention cost changes the schedule, not the parity
         base = subprocess.run([SIM_REF, *args[:3]], capture_output=True, text=True, timeout=300)
         assert base.stdout != a.stdout
+
+
+def test_device_generated_decode_step_grows_match_oracle():
+    """skv_batch_grow_mirror + skv_batch_grow_launch (ops generated on the device from its own
+    request state, no upload) over 40 decode steps crossing block boundaries, mixed with
+    host-path grows and frees: tables, owners and stats identical to the oracle; a CacheFull
+    step is refused by the mirror (nothing changes) and handled by the host path."""
+    import torch
+    shapes = [(32, 8, 32), (40, 40), (32, 32)]
+    P_ = 900  # every initial request fits (~624 blocks) plus 40 decode steps of growth
+    c = gpu_cache(shapes, P_)
+    o = _oracle_for(shapes, P_)
+    ids = []
+    for r in range(24):
+        for mm in range(3):
+            rid = 1 + r * 3 + mm
+            t = 100 + 7 * r + mm
+            assert c.try_allocate(rid, mm, t) == o.try_allocate(rid, mm, t)
+            ids.append((rid, mm))
+    groups = [(mm, [rid for rid, m2 in ids if m2 == mm]) for mm in range(3)]
+    b = c.batch(groups)
+    s = torch.cuda.Stream()
+    for step in range(40):
+        assert b.grow_mirror(1), "pool sized for 40 steps"
+        b.grow_launch(1, stream=s)
+        for mm, rids in groups:  # the oracle applies the same try_allocate calls in batch order
+            for rid in rids:
+                assert o.try_allocate(rid, mm, c.request_tokens(rid))
+        if step % 10 == 9:
+            s.synchronize()
+            for rid, _ in ids:
+                assert np.array_equal(c.block_table_np(rid), o.block_table_np(rid))
+            assert c.stats() == o.stats() and c.free_blocks() == o.free_blocks()
+    s.synchronize()
+    for blk in range(0, P_, 7):
+        for slot in range(6):
+            assert c.owner_of(blk, slot) == o.owner_of(blk, slot)
+    # free some, host-path regrow, then the device path again
+    for rid, mm in ids[::5]:
+        c.free_request(rid)
+        o.free_request(rid)
+    rest = [(mm, [rid for rid, m2 in ids[1::5] if m2 == mm]) for mm in range(3)]
+    rest = [g for g in rest if g[1]]
+    b2 = c.batch(rest)
+    assert b2.grow_mirror(16)
+    b2.grow_launch(16, stream=s)
+    for mm, rids in rest:
+        for rid in rids:
+            assert o.try_allocate(rid, mm, c.request_tokens(rid))
+    s.synchronize()
+    for rid, _ in ids[1::5]:
+        assert np.array_equal(c.block_table_np(rid), o.block_table_np(rid))
+    assert c.stats() == o.stats()
+    # a step that cannot be fully granted is refused without any change
+    before = c.stats()
+    assert not b2.grow_mirror(10 ** 6)
+    assert c.stats() == before
+
+
+def test_device_grow_captured_in_cuda_graph():
+    """The device half captured in a CUDA graph with the decode launches and replayed after
+    each host mirror call: identical tables to the oracle after 20 replays."""
+    import torch
+    shapes = [(4, 8, 32), (4, 4, 4)]
+    P_ = 200
+    models = [P.ModelSpec(f"g{i}", L, H, 128, 2, Hq) for i, (L, H, Hq) in enumerate(shapes)]
+    c = P.UnifiedKvCache(models, 16, 1, P_, allocate_storage=True)
+    o = _oracle_for([(L, H) for L, H, _ in shapes], P_)
+    groups = [(0, [1, 2, 3]), (1, [4, 5])]
+    for m, rids in groups:
+        for rid in rids:
+            assert c.try_allocate(rid, m, 30 * rid) and o.try_allocate(rid, m, 30 * rid)
+    s = torch.cuda.Stream()
+    c.set_stream(s)
+    b = c.batch(groups)
+    q = [torch.randn((3, 32, 128), device="cuda").half(), torch.randn((2, 4, 128), device="cuda").half()]
+    out = [torch.empty_like(x) for x in q]
+    assert b.grow_mirror(1)
+    b.grow_launch(1, stream=s)  # eager first: sizes the batch's buffers
+    for layer in range(4):  # and the decode work list / workspace
+        b.decode(q, out, layer, stream=s)
+    for m, rids in groups:
+        for rid in rids:
+            assert o.try_allocate(rid, m, c.request_tokens(rid))
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    assert b.grow_mirror(1)
+    with torch.cuda.graph(g, stream=s):
+        b.grow_launch(1, stream=s)
+        for layer in range(4):
+            b.decode(q, out, layer, stream=s)
+    for m, rids in groups:
+        for rid in rids:
+            assert o.try_allocate(rid, m, c.request_tokens(rid))
+    g.replay()
+    for _ in range(20):
+        assert b.grow_mirror(1)
+        for m, rids in groups:
+            for rid in rids:
+                assert o.try_allocate(rid, m, c.request_tokens(rid))
+        g.replay()
+    torch.cuda.synchronize()
+    for m, rids in groups:
+        for rid in rids:
+            assert np.array_equal(c.block_table_np(rid), o.block_table_np(rid))
+    assert c.stats() == o.stats()
