@@ -352,3 +352,74 @@ def append(lay: KvLayout, pool: np.ndarray, layer, tables, pos, k, v):
 
 def synth_value(seed: int, i: int, amp: float = 1.0) -> float:
     return _attn_lib().skvo_synth_value(seed, i, amp)
+
+
+# ------------------------------------------------------- reference control plane (shims) --
+REF_CTL_SO = os.path.join(HERE, "_ref", "libref_ctl.so")
+
+
+def ref_ctl_available() -> bool:
+    return os.path.exists(REF_CTL_SO)
+
+
+def ref_generate_trace(profiles, rate, duration, skewness, seed, step_time=None, step_factor=1.0):
+    """The reference seasim::generate_trace (workload.hpp:181-212) through oracle/ref_ctl.cpp.
+    profiles: [(in_mean, in_sd, out_mean, out_sd)]; returns [(t, svc, in_len, out_len)]."""
+    lib = _load(REF_CTL_SO)
+    f = lib.ref_generate_trace
+    f.restype = C.c_long
+    d = C.POINTER(C.c_double)
+    f.argtypes = [C.c_int, d, d, d, d, C.c_double, C.c_double, C.c_int, C.c_uint64, C.c_int, C.c_double, C.c_double,
+                  C.c_long, d, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]
+    n = len(profiles)
+    cols = [np.ascontiguousarray([p[k] for p in profiles], np.float64) for k in range(4)]
+    cap = int(rate * duration * max(1.0, step_factor) * 3 + 1000)
+    t = np.zeros(cap, np.float64)
+    svc, il, ol = (np.zeros(cap, np.int32) for _ in range(3))
+    ptr = lambda a, ty: a.ctypes.data_as(C.POINTER(ty))  # noqa: E731
+    m = f(n, *[ptr(x, C.c_double) for x in cols], rate, duration, skewness, seed, 0 if step_time is None else 1,
+          step_time or 0.0, step_factor, cap, ptr(t, C.c_double), ptr(svc, C.c_int), ptr(il, C.c_int), ptr(ol, C.c_int))
+    if m < 0:
+        raise ValueError("ConfigError")
+    assert m <= cap
+    return [(float(t[i]), int(svc[i]), int(il[i]), int(ol[i])) for i in range(m)]
+
+
+def ref_dedicated_plan(services, gpus_per_node, num_nodes, mem_gib, share_cap, replica_cap, kv_reserve_gib, batch_cap,
+                       extra_models=(), min_tp_override=None, extra_entries=None):
+    """The reference seasim::dedicated_plan (placement.hpp:284-319) over default_cost_model()
+    plus extra models [(id, layers, heads, weight_gib, min_tp, {tp: (act_base_gib, act_per_gib)})]
+    (tp in 1, 2, 4, 8 consecutively from 1), min_tp overrides {id: tp} and extra activation
+    entries {id: {tp: (base, per)}}.  Returns (groups [(tp, node, gpu0, [services])], unplaced,
+    feasible) or None when required_tp throws."""
+    lib = _load(REF_CTL_SO)
+    f = lib.ref_dedicated_plan
+    f.restype = C.c_int
+    cs = lambda xs: (C.c_char_p * max(1, len(xs)))(*[x.encode() for x in xs])  # noqa: E731
+    ia = lambda xs: (C.c_int * max(1, len(xs)))(*xs)  # noqa: E731
+    da = lambda xs: (C.c_double * max(1, len(xs)))(*xs)  # noqa: E731
+    ex = list(extra_models)
+    act = []
+    for _, _, _, _, _, tab in ex:
+        for k in range(4):
+            act += list(tab.get(1 << k, (0.0, 0.0)))
+    ovr = dict(min_tp_override or {})
+    ent = [(mid, tp, v) for mid, d in (extra_entries or {}).items() for tp, v in d.items()]
+    G = 64
+    n_groups, n_unp, feas = C.c_int(), C.c_int(), C.c_int()
+    g_tp, g_node, g_gpu0, g_nsvc = (np.zeros(G, np.int32) for _ in range(4))
+    g_svcs = np.zeros(G * 32, np.int32)
+    unplaced = np.zeros(max(1, len(services)), np.int32)
+    ip = lambda a: a.ctypes.data_as(C.POINTER(C.c_int))  # noqa: E731
+    rc = f(len(services), cs(services), gpus_per_node, num_nodes, C.c_double(mem_gib), share_cap, replica_cap,
+           C.c_double(kv_reserve_gib), batch_cap, len(ex), cs([e[0] for e in ex]), ia([e[1] for e in ex]),
+           ia([e[2] for e in ex]), da([e[3] for e in ex]), ia([e[4] for e in ex]),
+           ia([max(k for k in range(4) if (1 << k) in e[5]) + 1 for e in ex]), da(act), len(ovr), cs(list(ovr)),
+           ia(list(ovr.values())), len(ent), cs([e[0] for e in ent]), ia([e[1] for e in ent]),
+           da([x for e in ent for x in e[2]]), C.byref(n_groups), ip(g_tp), ip(g_node), ip(g_gpu0), ip(g_nsvc),
+           ip(g_svcs), C.byref(n_unp), ip(unplaced), C.byref(feas))
+    if rc < 0:
+        return None
+    groups = [(int(g_tp[g]), int(g_node[g]), int(g_gpu0[g]), [int(x) for x in g_svcs[g * 32:g * 32 + g_nsvc[g]]])
+              for g in range(n_groups.value)]
+    return groups, [int(x) for x in unplaced[:n_unp.value]], bool(feas.value)

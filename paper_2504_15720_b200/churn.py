@@ -64,8 +64,17 @@ class ServiceProfile:
 
     def sample(self, rng: Rng, mean: float, sd: float) -> int:  # LengthDist::sample, workload.hpp:33-38
         if sd == 0.0:
-            return max(1, int(round(mean)))
-        return max(1, int(round(rng.gaussian(mean, sd))))
+            return max(1, llround(mean))
+        return max(1, llround(rng.gaussian(mean, sd)))
+
+
+def llround(x: float) -> int:
+    """std::llround: nearest integer, halfway cases away from zero (Python's round() rounds
+    them to even)."""
+    a = abs(x)
+    r = math.floor(a)  # a - r is exact in binary floating point (x + 0.5 is not)
+    r = int(r) + (1 if a - r >= 0.5 else 0)
+    return r if x >= 0 else -r
 
 
 def paper_services(n_models: int) -> List[ServiceProfile]:
