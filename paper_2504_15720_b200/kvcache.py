@@ -24,7 +24,8 @@ from typing import Iterable, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libseakv.so")
+# SKV_LIB_PATH: an alternative build of the same library (A/B measurements, scripts/build_variant.sh)
+LIB_PATH = os.environ.get("SKV_LIB_PATH") or os.path.join(_HERE, "libseakv.so")
 
 SKV_OK, SKV_CACHE_FULL = 0, 1
 SKV_ERR_CONFIG, SKV_ERR_VALIDATION, SKV_ERR_LOGIC, SKV_ERR_CUDA, SKV_ERR_ARG = -1, -2, -3, -4, -5
