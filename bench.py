@@ -132,8 +132,14 @@ def _blocks(P, services, ctxs, grow):
     return sum(-(-sum((c + grow + 15) // 16 for c in cl) // sub) for sub, cl in zip(subs, ctxs)) + 64
 
 
+# tokens every decode request may still grow by during one run: warm-up + timed steps of the
+# device and e2e legs, the capture steps and the allocator measurement (3 x 16 + 16 steps)
+def grow_reserve(args):
+    return args.warmup * 2 + args.steps * 2 + 8 + 80
+
+
 def make_workload(P, args):
-    grow = args.warmup * 2 + args.steps * 2 + 8
+    grow = grow_reserve(args)
     if args.workload == "config1":
         ctxs = [[args.ctx or 512] * (args.requests or 32) for _ in SERVICES_C1]
         return Workload("config1", SERVICES_C1, ctxs, 0, _blocks(P, SERVICES_C1, ctxs, grow),
@@ -196,7 +202,7 @@ def add_tp_shard(P, wl, args, tp):
     ctx = args.ctx or 2048
     wl.services = list(wl.services) + [(f"llama2-70b/tp{tp}", 80, h, h)]
     wl.ctxs = list(wl.ctxs) + [[ctx] * nreq]
-    grow = args.warmup * 2 + args.steps * 2 + 8
+    grow = grow_reserve(args)
     wl.pool_blocks = _blocks(P, wl.services, wl.ctxs, grow)
     wl.nlayers = 80
     wl.desc += (f"; plus a llama2-70b-shape service head-sharded over tp={tp} ranks ({nreq} requests per tp group, "
@@ -210,7 +216,7 @@ def setup(P, torch, args, device, tp_shard=0):
     if tp_shard:
         add_tp_shard(P, wl, args, tp_shard)
     models = model_specs(P, wl.services)
-    ctx_max = max(max(c) for c in wl.ctxs if c) + args.warmup * 2 + args.steps * 2 + 8
+    ctx_max = max(max(c) for c in wl.ctxs if c) + grow_reserve(args)
     nreq_total = sum(len(c) for c in wl.ctxs)
     cache = P.UnifiedKvCache(models, 16, 1, wl.pool_blocks, device=device, dtype=P.FP16,
                              phys_layers=wl.phys_layers, max_requests=nreq_total + 16,
@@ -415,7 +421,7 @@ def run_gpu(args):
     launches_timed = cache.kernel_launches() - launches0
     graph_launches = 0
     if graph is not None:  # the graph's kernels bypass the pool's launch counter
-        graph_launches = args.steps * (NLAYERS + 3)  # step-op generation, placement, plan, decodes
+        graph_launches = args.steps * (NLAYERS + 2)  # device grow (op generation + placement), plan, decodes
     # per-launch decode timing for the roofline: a CUDA graph of the step's NLAYERS fused
     # append+decode launches (same contexts, no grow; re-appending the same token is
     # idempotent) replayed back to back on the launching stream, bracketed by events
@@ -454,42 +460,53 @@ def run_gpu(args):
     torch.cuda.synchronize()
     na = 16
     n_ops = na * sum(len(c) for c in wl.ctxs)
-    dev_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(na)]
     host_s = 0.0
     gg = None
-    try:  # the device half timed as the step graph runs it (graph replay, no host launch gaps)
+    try:  # the device half of `na` consecutive steps as one graph (as nodes of the step graph run)
         assert batch.grow_mirror(1)
         batch.grow_launch(1, stream=stream)
         torch.cuda.synchronize()
         gg = torch.cuda.CUDAGraph()
         with torch.cuda.graph(gg, stream=stream):
-            batch.grow_launch(1, stream=stream)
+            for _ in range(na):
+                batch.grow_launch(1, stream=stream)
     except Exception as e:  # noqa: BLE001
         print(f"# allocator graph unavailable: {e}", file=sys.stderr)
-    for i in range(na):
-        h0 = time.perf_counter()
-        ok = batch.grow_mirror(1)
-        host_s += time.perf_counter() - h0
-        assert ok
-        dev_ev[i][0].record(stream)
+    dev_ms = 0.0
+    for rep in range(3):
+        for i in range(na):  # host halves of the na steps (exact answers + CacheStats)
+            h0 = time.perf_counter()
+            ok = batch.grow_mirror(1)
+            host_s += time.perf_counter() - h0
+            assert ok
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):  # keep the GPU busy while the host submits
+            torch.cuda._sleep(200000)
+        e0.record(stream)
         if gg is not None:
             gg.replay()
         else:
-            batch.grow_launch(1, stream=stream)
-        dev_ev[i][1].record(stream)
-    torch.cuda.synchronize()
+            for i in range(na):
+                batch.grow_launch(1, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        dev_ms += e0.elapsed_time(e1)
+    n_ops = 3 * na * sum(len(c) for c in wl.ctxs)
     mirror_ns = host_s / n_ops * 1e9
-    device_ns = sum(e0.elapsed_time(e1) for e0, e1 in dev_ev) * 1e6 / n_ops
+    device_ns = dev_ms * 1e6 / n_ops
+    n_ops = na * sum(len(c) for c in wl.ctxs)
     # (b) the per-request host path (any CacheFull case): host mirror + op upload + placement
     a0 = time.perf_counter()
     aev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(na)]
     for i in range(na):
         batch.grow(1)  # host mirror: the grant / CacheFull answer, no device round trip
+        with torch.cuda.stream(stream):
+            torch.cuda._sleep(200000)
         aev[i][0].record(stream)
         cache.flush(stream)  # GPU placement: op upload + grow_kernel
         aev[i][1].record(stream)
     torch.cuda.synchronize()
-    alloc_ns = (time.perf_counter() - a0) / n_ops * 1e9
+    alloc_ns = (time.perf_counter() - a0) / n_ops * 1e9 - 200000 / 1.9e9 * na / n_ops * 1e9  # minus the spin
     alloc_gpu_ns = sum(e0.elapsed_time(e1) for e0, e1 in aev) * 1e6 / n_ops
 
     # ---- e2e through the C-ABI with host buffers -----------------------------------------
@@ -619,9 +636,10 @@ def run_gpu(args):
                       "device_ns_per_op": round(device_ns, 2),
                       "host_path_ns_per_grow_op": round(alloc_ns, 2), "host_path_gpu_ns_per_grow_op": round(alloc_gpu_ns, 2),
                       "note": "ns_per_grow_op = host mirror (skv_batch_grow_mirror, wall) + device half "
-                              "(skv_batch_grow_launch: op generation + placement kernel, CUDA events) per decode-step "
-                              "grow op, the path the step graph runs; host_path_*: batch.grow(1) + flush (op upload + "
-                              "grow_kernel) wall incl. sync, the fallback when a step hits CacheFull"},
+                              "(skv_batch_grow_launch: op generation + placement in one kernel; CUDA events around a "
+                              "graph of 16 consecutive steps' launches, as they run as nodes of the step graph) per "
+                              "decode-step grow op; host_path_*: batch.grow(1) + flush (op upload + grow_kernel) wall "
+                              "incl. sync, the fallback when a step hits CacheFull"},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }

@@ -44,7 +44,7 @@ __device__ __forceinline__ int block_excl_scan(int v, int* total, int* sm_warp) 
   if (lane == 31) sm_warp[wid] = incl;
   __syncthreads();
   if (wid == 0) {
-    const int w = sm_warp[lane];
+    const int w = lane < (int)(blockDim.x >> 5) ? sm_warp[lane] : 0;
     const int wi = warp_incl_scan(w);
     sm_warp[lane] = wi - w;  // exclusive warp offsets
     if (lane == 31) sm_warp[32] = wi;
@@ -62,24 +62,90 @@ __device__ __forceinline__ unsigned long long full_mask(int sub) {
   return sub >= 64 ? ~0ull : ((1ull << sub) - 1ull);
 }
 
-__global__ void __launch_bounds__(kGrowThreads, 1)
-grow_kernel(DevAlloc st, AllocParams pr, const GrowOp* __restrict__ ops, int n, GrowScratch sc) {
+// Decode-step ops (STEP): op i = try_allocate(req_id[h], model, tokens + delta) of batch request
+// i, from the device's own request state (the host mirror found every one granted).
+struct StepArgs {
+  const int32_t* handles;
+  const int32_t* group;
+  StepModels gm;
+  int delta, tpb;
+};
+
+// SMALL (n <= kSmallOps ops, <= kSmallClaims claims — every decode step): ops and all scratch
+// live in shared memory, so the phases exchange data without global-memory round trips.
+constexpr int kSmallOps = 1024, kSmallClaims = 2048;
+constexpr int kSmallSmem = kSmallOps * (int)sizeof(GrowOp) + 5 * kSmallOps * 4 + kSmallClaims * (4 + 4 + 8);
+
+template <bool STEP, bool SMALL, int NT>
+__global__ void __launch_bounds__(NT, 1)
+grow_kernel(DevAlloc st, AllocParams pr, const GrowOp* ops_g, int n, GrowScratch sc_g, StepArgs sa) {
+  extern __shared__ __align__(16) char gsm[];
+  const GrowOp* ops = ops_g;  // no __restrict__: STEP writes them
+  GrowScratch sc = sc_g;
+  if constexpr (SMALL) {
+    GrowOp* o = reinterpret_cast<GrowOp*>(gsm);
+    int32_t* a = reinterpret_cast<int32_t*>(gsm + kSmallOps * sizeof(GrowOp));
+    sc.S = a;
+    sc.cbeg = a + kSmallOps;
+    sc.nnew = a + 2 * kSmallOps;
+    sc.base = a + 3 * kSmallOps;
+    sc.nbfirst = a + 4 * kSmallOps;
+    sc.newblk = a + 5 * kSmallOps;
+    sc.newrank = a + 5 * kSmallOps + kSmallClaims;
+    sc.openlist = reinterpret_cast<int2*>(a + 5 * kSmallOps + 2 * kSmallClaims);
+    if constexpr (!STEP)
+      for (int i = threadIdx.x; i < n; i += NT) o[i] = ops_g[i];
+    ops = o;
+  }
   __shared__ int sm_warp[33];
   __shared__ int carryC[kMaxModels];   // claims per model so far
   __shared__ long long O[kMaxModels];  // open slots at batch start
   __shared__ int needOpen[kMaxModels], offOpen[kMaxModels], newcnt[kMaxModels], offNew[kMaxModels];
   __shared__ int carryNew, carryCl, sh_total;
+  __shared__ int hint[1 + kMaxModels];  // bitmap scan starts (DevAlloc::hints), updated at the end
   const int tid = threadIdx.x;
   const int M = pr.M;
   if (tid < M) {
     carryC[tid] = 0;
     O[tid] = st.open[tid];
   }
+  if (tid <= M) hint[tid] = st.hints[tid];
   if (tid == 0) carryNew = carryCl = 0;
+  if constexpr (STEP) {  // phase 0: the ops themselves
+    GrowOp* w = const_cast<GrowOp*>(ops);  // shared memory (SMALL) or the batch's buffer
+    for (int i = tid; i < n; i += NT) {
+      const int h = sa.handles[i];
+      const int have = st.req_nslots[h];
+      const int tok = st.req_tokens[h] + sa.delta;
+      GrowOp op;
+      op.handle = h;
+      op.model = sa.gm.m[sa.group[i]];
+      op.have = have;
+      op.claims = max(0, (tok + sa.tpb - 1) / sa.tpb - have);
+      op.tokens_after = tok;
+      op.pad = 0;
+      op.id = st.req_id[h];
+      w[i] = op;
+    }
+    __threadfence_block();
+  }
   __syncthreads();
+  {  // token-only growth (15 of every 16 decode steps at tpb 16): no placement work at all
+    int any = 0;
+    for (int i = tid; i < n; i += NT) any |= ops[i].claims > 0;
+    if (!__syncthreads_or(any)) {
+      for (int i = tid; i < n; i += NT) {
+        const GrowOp op = ops[i];
+        atomicMax(&st.req_tokens[op.handle], op.tokens_after);
+        st.req_model[op.handle] = op.model;
+        st.req_id[op.handle] = op.id;
+      }
+      return;
+    }
+  }
 
   // ---- phase 1: per-model claim prefixes and fresh-block counts ------------------
-  for (int c0 = 0; c0 < n; c0 += kGrowThreads) {
+  for (int c0 = 0; c0 < n; c0 += NT) {
     const int i = c0 + tid;
     const bool valid = i < n;
     GrowOp op{};
@@ -139,10 +205,10 @@ grow_kernel(DevAlloc st, AllocParams pr, const GrowOp* __restrict__ ops, int n, 
   }
   __syncthreads();
 
-  // ---- phase 2a: the Nnew lowest free block ids ------------------------------------
+  // ---- phase 2a: the Nnew lowest free block ids (words below hint[0] hold none) --------
   {
     int cum = 0;
-    for (int w0 = 0; w0 < pr.W && cum < Nnew; w0 += kGrowThreads) {
+    for (int w0 = hint[0]; w0 < pr.W && cum < Nnew; w0 += NT) {
       const int w = w0 + tid;
       uint32_t bits = w < pr.W ? st.free_bits[w] : 0u;
       int tot;
@@ -156,6 +222,8 @@ grow_kernel(DevAlloc st, AllocParams pr, const GrowOp* __restrict__ ops, int n, 
     }
     if (tid == 0 && cum < Nnew) atomicExch(st.status, 1);  // host admitted more than exists
   }
+  __syncthreads();
+  if (tid == 0 && Nnew > 0) hint[0] = sc.newblk[Nnew - 1] >> 5;  // every lower free block was taken
 
   // ---- phase 2b: the first needOpen[m] open slots of each model, lexicographic -------
   for (int m = 0; m < M; ++m) {
@@ -165,7 +233,7 @@ grow_kernel(DevAlloc st, AllocParams pr, const GrowOp* __restrict__ ops, int n, 
     const unsigned long long fm = full_mask(sub);
     const uint32_t* pb = st.partial_bits + (size_t)m * pr.W;
     int cum = 0;
-    for (int w0 = 0; w0 < pr.W && cum < need; w0 += kGrowThreads) {
+    for (int w0 = hint[1 + m]; w0 < pr.W && cum < need; w0 += NT) {
       const int w = w0 + tid;
       uint32_t bits = w < pr.W ? pb[w] : 0u;
       int cnt = 0;
@@ -187,10 +255,13 @@ grow_kernel(DevAlloc st, AllocParams pr, const GrowOp* __restrict__ ops, int n, 
       cum += tot;
     }
     if (tid == 0 && cum < need) atomicExch(st.status, 2);
+    __syncthreads();
+    // blocks before the last one taken are now full (their partial bits clear in phase 5)
+    if (tid == 0) hint[1 + m] = sc.openlist[offOpen[m] + need - 1].x >> 5;
   }
 
   // ---- phase 3: model-local fresh block -> global rank -----------------------------
-  for (int i = tid; i < n; i += kGrowThreads) {
+  for (int i = tid; i < n; i += NT) {
     const int nn = sc.nnew[i];
     if (nn == 0) continue;
     const int m = ops[i].model;
@@ -200,7 +271,7 @@ grow_kernel(DevAlloc st, AllocParams pr, const GrowOp* __restrict__ ops, int n, 
   __syncthreads();
 
   // ---- phase 4: materialise every claim --------------------------------------------
-  for (int g = tid; g < Tcl; g += kGrowThreads) {
+  for (int g = tid; g < Tcl; g += NT) {
     int lo = 0, hi = n - 1;  // last op with cbeg <= g
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
@@ -232,7 +303,7 @@ grow_kernel(DevAlloc st, AllocParams pr, const GrowOp* __restrict__ ops, int n, 
   __syncthreads();
 
   // ---- phase 5: partial-set membership, request rows, counters ----------------------
-  for (int g = tid; g < Tcl; g += kGrowThreads) {
+  for (int g = tid; g < Tcl; g += NT) {
     int lo = 0, hi = n - 1;
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
@@ -243,10 +314,14 @@ grow_kernel(DevAlloc st, AllocParams pr, const GrowOp* __restrict__ ops, int n, 
     const int2 e = st.req_table[(size_t)ops[lo].handle * pr.cap + ops[lo].have + (g - sc.cbeg[lo])];
     const uint32_t bit = 1u << (e.x & 31);
     uint32_t* word = &st.partial_bits[(size_t)m * pr.W + (e.x >> 5)];
-    if (st.blk_occ[e.x] == full_mask(sub)) atomicAnd(word, ~bit);  // :204
-    else atomicOr(word, bit);                                       // :217
+    if (st.blk_occ[e.x] == full_mask(sub)) {
+      atomicAnd(word, ~bit);  // :204
+    } else {
+      atomicOr(word, bit);  // :217
+      atomicMin(&hint[1 + m], e.x >> 5);
+    }
   }
-  for (int i = tid; i < n; i += kGrowThreads) {
+  for (int i = tid; i < n; i += NT) {
     const GrowOp op = ops[i];
     atomicMax(&st.req_nslots[op.handle], op.have + op.claims);
     atomicMax(&st.req_tokens[op.handle], op.tokens_after);
@@ -257,28 +332,9 @@ grow_kernel(DevAlloc st, AllocParams pr, const GrowOp* __restrict__ ops, int n, 
     st.open[tid] = O[tid] + (long long)newcnt[tid] * pr.sub[tid] - carryC[tid];
   }
   if (tid == 0) st.free_count[0] -= Nnew;
+  __syncthreads();
+  if (tid <= M) st.hints[tid] = hint[tid];
   (void)Tcl;
-}
-
-// Decode-step grow ops from the device's own request state (no host upload): the host mirror
-// has already applied the same try_allocate(+delta) calls and found every one granted.
-__global__ void step_ops_kernel(DevAlloc st, int tpb, const int32_t* __restrict__ handles,
-                                const int32_t* __restrict__ group, StepModels gm, int n, int delta,
-                                GrowOp* __restrict__ ops) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int h = handles[i];
-  const int have = st.req_nslots[h];
-  const int tok = st.req_tokens[h] + delta;
-  GrowOp op;
-  op.handle = h;
-  op.model = gm.m[group[i]];
-  op.have = have;
-  op.claims = max(0, (tok + tpb - 1) / tpb - have);
-  op.tokens_after = tok;
-  op.pad = 0;
-  op.id = st.req_id[h];
-  ops[i] = op;
 }
 
 // Release every slot of the freed requests (kv_cache.hpp:224-240).  One warp per
@@ -304,6 +360,7 @@ __global__ void free_release_kernel(DevAlloc st, AllocParams pr, const FreeOp* _
           e = true;
           st.blk_model[bs.x] = -1;
           atomicOr(&st.free_bits[bs.x >> 5], 1u << (bs.x & 31));
+          atomicMin(&st.hints[0], bs.x >> 5);
         }
       }
       emptied += __popc(__ballot_sync(0xffffffffu, e));
@@ -330,8 +387,12 @@ __global__ void free_fixup_kernel(DevAlloc st, AllocParams pr, const FreeOp* __r
         const int2 bs = row[j];
         const uint32_t bit = 1u << (bs.x & 31);
         uint32_t* word = &st.partial_bits[(size_t)op.model * pr.W + (bs.x >> 5)];
-        if (st.blk_occ[bs.x] == 0ull) atomicAnd(word, ~bit);  // :229
-        else atomicOr(word, bit);                            // :236
+        if (st.blk_occ[bs.x] == 0ull) {
+          atomicAnd(word, ~bit);  // :229
+        } else {
+          atomicOr(word, bit);  // :236
+          atomicMin(&st.hints[1 + op.model], bs.x >> 5);
+        }
       }
     }
     __syncwarp();
@@ -423,16 +484,33 @@ void launch_split_release(const SplitOp* ops, int n, long long total, int32_t* s
   split_release_kernel<<<blocks, 256, 0, s>>>(ops, n, total, stack, table, Lmax, Hmax, cap);
 }
 
-void launch_step_ops(const DevAlloc& st, int tpb, const int32_t* handles, const int32_t* group, StepModels gm,
-                     int n, int delta, GrowOp* ops, cudaStream_t s) {
+template <bool STEP>
+void launch_grow_t(const DevAlloc& st, const AllocParams& pr, const GrowOp* ops, int n, long long claims,
+                   const GrowScratch& sc, StepArgs sa, cudaStream_t s) {
   if (n <= 0) return;
-  step_ops_kernel<<<(n + 255) / 256, 256, 0, s>>>(st, tpb, handles, group, gm, n, delta, ops);
+  if (n <= 256 && claims <= kSmallClaims) {  // small batches: 8 warps (cheaper block barriers)
+    static std::atomic<uint64_t> attr{0};
+    ensure_smem_attr(grow_kernel<STEP, true, 256>, kSmallSmem, attr);
+    grow_kernel<STEP, true, 256><<<1, 256, kSmallSmem, s>>>(st, pr, ops, n, sc, sa);
+  } else if (n <= kSmallOps && claims <= kSmallClaims) {
+    static std::atomic<uint64_t> attr{0};
+    ensure_smem_attr(grow_kernel<STEP, true, kGrowThreads>, kSmallSmem, attr);
+    grow_kernel<STEP, true, kGrowThreads><<<1, kGrowThreads, kSmallSmem, s>>>(st, pr, ops, n, sc, sa);
+  } else {
+    grow_kernel<STEP, false, kGrowThreads><<<1, kGrowThreads, 0, s>>>(st, pr, ops, n, sc, sa);
+  }
 }
 
-void launch_grow(const DevAlloc& st, const AllocParams& pr, const GrowOp* ops, int n,
+void launch_grow_step(const DevAlloc& st, const AllocParams& pr, int tpb, const int32_t* handles,
+                      const int32_t* group, StepModels gm, int n, int delta, GrowOp* ops, const GrowScratch& sc,
+                      cudaStream_t s) {
+  StepArgs sa{handles, group, gm, delta, tpb};
+  launch_grow_t<true>(st, pr, ops, n, (long long)n * ((delta + tpb - 1) / tpb + 1), sc, sa, s);
+}
+
+void launch_grow(const DevAlloc& st, const AllocParams& pr, const GrowOp* ops, int n, long long claims,
                  const GrowScratch& sc, cudaStream_t s) {
-  if (n <= 0) return;
-  grow_kernel<<<1, kGrowThreads, 0, s>>>(st, pr, ops, n, sc);
+  launch_grow_t<false>(st, pr, ops, n, claims, sc, StepArgs{}, s);
 }
 
 void launch_free(const DevAlloc& st, const AllocParams& pr, const FreeOp* ops, int n,

@@ -281,6 +281,7 @@ skv_status flush(skv_pool* p) {
       max_n = std::max(max_n, r.end - r.begin);
       max_t = std::max(max_t, p->run_claims[gi++]);
     }
+  gi = 0;
   if (max_n) {
     skv_status st = ensure_scratch(p, max_n, (size_t)max_t);
     if (st) return st;
@@ -297,7 +298,7 @@ skv_status flush(skv_pool* p) {
   for (const Run& r : p->runs) {
     const int n = (int)(r.end - r.begin);
     if (r.kind == 0) {
-      skv::launch_grow(p->dev, p->prm, dg + r.begin, n, p->scr, p->stream);
+      skv::launch_grow(p->dev, p->prm, dg + r.begin, n, p->run_claims[gi++], p->scr, p->stream);
       p->launches += 1;
     } else {
       FreeResult& fresult = p->pending[fr++];
@@ -718,6 +719,7 @@ skv_status skv_pool_create(const skv_model_desc* models, int32_t n, int32_t tpb,
       (st = dev_alloc(p, &d.free_count, 1)) || (st = dev_alloc(p, &d.req_table, (size_t)p->R * p->cap, false)) ||
       (st = dev_alloc(p, &d.req_nslots, p->R)) || (st = dev_alloc(p, &d.req_tokens, p->R)) ||
       (st = dev_alloc(p, &d.req_model, p->R, false)) || (st = dev_alloc(p, &d.req_id, p->R)) ||
+      (st = dev_alloc(p, &d.hints, 1 + n)) ||
       (st = dev_alloc(p, &d.status, 1)) ||
       (st = dev_alloc(p, &d.free_E, n)) || (st = dev_alloc(p, &d.free_R, n)) ||
       (st = dev_alloc(p, &p->d_outE, (size_t)kResultSlots * n)))
@@ -754,7 +756,8 @@ void skv_pool_destroy(skv_pool* p) {
   skv::DevAlloc& d = p->dev;
   for (void* q : {(void*)d.free_bits, (void*)d.partial_bits, (void*)d.blk_model, (void*)d.blk_occ,
                   (void*)d.slot_owner, (void*)d.open, (void*)d.free_count, (void*)d.req_table,
-                  (void*)d.req_nslots, (void*)d.req_tokens, (void*)d.req_model, (void*)d.req_id, (void*)d.status,
+                  (void*)d.req_nslots, (void*)d.req_tokens, (void*)d.req_model, (void*)d.req_id, (void*)d.hints,
+                  (void*)d.status,
                   (void*)d.free_E, (void*)d.free_R, (void*)p->d_outE, p->d_ops, p->storage,
                   (void*)p->scr.S, (void*)p->scr.cbeg, (void*)p->scr.nnew, (void*)p->scr.base,
                   (void*)p->scr.nbfirst, (void*)p->scr.newblk, (void*)p->scr.newrank, (void*)p->scr.openlist})
@@ -1118,13 +1121,37 @@ skv_status skv_batch_grow_mirror(skv_pool* p, skv_batch* b, int64_t delta, int32
   for (int m = 0; m < p->M; ++m)
     blocks += C[m] > p->open[m] ? ceil_div_ll(C[m] - p->open[m], p->models[m].sub) : 0;
   if (blocks > p->free_count || max_need > p->cap) return SKV_OK;
-  for (int g = 0; g < b->ngroups; ++g)
+  // grow_handle_impl's arithmetic for the granted case, inlined with per-model constants (the
+  // watermarks are still taken after every op, as note_watermarks is, kv_cache.hpp:242-246)
+  const long long tpb = p->tpb;
+  for (int g = 0; g < b->ngroups; ++g) {
+    const int m = b->gmodel[g];
+    const ModelInfo& mi = p->models[m];
+    const long long native = mi.native, per_token = mi.native / tpb, sub = mi.sub;
     for (int i = 0; i < b->gsize[g]; ++i) {
-      const int r = b->gbegin[g] + i;
-      if ((st = grow_handle_impl(p, b->handles[r], b->ids[r], b->gmodel[g], p->req[b->handles[r]].tokens + delta,
-                                 /*queue=*/false)))
-        return st;  // cannot happen after the check above
+      ReqHost& r = p->req[b->handles[b->gbegin[g] + i]];
+      const long long tokens = r.tokens + delta;
+      const long long c = std::max(0LL, (tokens + tpb - 1) / tpb - r.nslots);
+      if (c > 0) {  // claim_slot x c (:191-222): open slots first, then fresh blocks
+        const long long from_open = std::min<long long>(c, p->open[m]);
+        const long long rest = c - from_open;
+        const long long nb = (rest + sub - 1) / sub;
+        p->open[m] += -from_open + nb * sub - rest;
+        p->free_count -= nb;
+        p->slot_frag += -from_open * native + nb * (p->merged_i - native) - (rest - nb) * native;
+        r.nslots += (int)c;
+        p->cur_entries += (size_t)c;
+      }
+      const long long grew = delta > 0 ? delta : 0;  // tokens only grow (:115-119)
+      p->rw += (uint64_t)grew;
+      r.tokens = tokens;
+      p->token_waste += (c * tpb - grew) * per_token + c * native;  // incl. quirk Q1
+      p->peak_entries = std::max<uint64_t>(p->peak_entries, p->cur_entries);
+      p->peak_used = std::max<long long>(p->peak_used, (long long)p->P - p->free_count);
+      p->peak_frag = std::max<long long>(p->peak_frag, p->slot_frag + p->token_waste);
     }
+  }
+  p->token_epoch++;
   *all_granted = 1;
   return SKV_OK;
 }
@@ -1162,9 +1189,9 @@ skv_status skv_batch_grow_launch(skv_pool* p, skv_batch* b, int64_t delta, void*
   if ((st = order_streams(p, s))) return st;  // queued host-side allocator work first
   skv::StepModels gm{};
   for (int g = 0; g < b->ngroups; ++g) gm.m[g] = b->gmodel[g];
-  skv::launch_step_ops(p->dev, p->tpb, b->d_handles, b->d_group, gm, (int)n, (int)delta, b->d_gops, s);
-  skv::launch_grow(p->dev, p->prm, b->d_gops, (int)n, b->gscr, s);
-  p->launches += 2;
+  skv::launch_grow_step(p->dev, p->prm, p->tpb, b->d_handles, b->d_group, gm, (int)n, (int)delta, b->d_gops, b->gscr,
+                        s);
+  p->launches += 1;
   return after_data(p, s);
 }
 

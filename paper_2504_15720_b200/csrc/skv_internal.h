@@ -48,6 +48,8 @@ struct DevAlloc {
   int32_t* req_tokens;           // [R]     tokens covered (decode context length)
   int32_t* req_model;            // [R]
   unsigned long long* req_id;    // [R]     request id of the handle (written by every grow)
+  int32_t* hints;                // [1+M]   lowest bitmap word that may hold a free block / a
+                                 //         partial block of model m (scan starts; lower bounds)
   int32_t* status;               // [1]     device invariant violations (0 = ok)
   int32_t* free_E;               // [M]     scratch: blocks emptied by the current free run
   int32_t* free_R;               // [M]     scratch: slots released by the current free run
@@ -89,9 +91,11 @@ void launch_stage_copy(void* dst, const void* src_host_mapped, size_t bytes, cud
 struct StepModels {
   int m[kMaxGroups];
 };
-void launch_step_ops(const DevAlloc& st, int tpb, const int32_t* handles, const int32_t* group, StepModels gm,
-                     int n, int delta, GrowOp* ops, cudaStream_t s);
-void launch_grow(const DevAlloc& st, const AllocParams& pr, const GrowOp* ops, int n,
+// Decode-step growth in one launch: the grow kernel generates its ops (written to `ops`) first.
+void launch_grow_step(const DevAlloc& st, const AllocParams& pr, int tpb, const int32_t* handles,
+                      const int32_t* group, StepModels gm, int n, int delta, GrowOp* ops, const GrowScratch& sc,
+                      cudaStream_t s);
+void launch_grow(const DevAlloc& st, const AllocParams& pr, const GrowOp* ops, int n, long long claims,
                  const GrowScratch& sc, cudaStream_t s);
 void launch_free(const DevAlloc& st, const AllocParams& pr, const FreeOp* ops, int n,
                  int32_t* out_E, cudaStream_t s);
