@@ -113,6 +113,7 @@ struct DataGroup {
   int req_begin, nreq;      // slice of the batch
   int D;                    // head_dim (64, 128, 256)
   float scale_log2;         // softmax scale * log2(e) (default 1/sqrt(D))
+  int pf_base, pf_npairs;   // prefill: first work item of the group, query-tile pairs per (request, head)
 };
 
 struct DataParams {

@@ -403,22 +403,25 @@ __device__ __forceinline__ int qoff_of(const DataParams& p, int r, int rl) {
   return p.q_offs ? p.q_offs[r] : rl * p.n_new;
 }
 
-// item order: (request, kv head) major, query-tile pair descending minor, so the pairs of
-// one (request, head) -- which read the same K/V -- run at the same time on different SMs
-// (L2 reuse) and each group starts with its longest pair
-__device__ __forceinline__ bool prefill_item(const DataParams& p, int i, int npairs, int hmax, int& r, int& h,
-                                             int& pair) {
-  pair = npairs - 1 - i % npairs;
-  const int rem = i / npairs;
-  h = rem % hmax;
-  r = rem / hmax;
-  const DataGroup& g = p.g[p.req_group[r]];
-  return g.active && h < g.Hkv && 2 * pair * kRows < qlen_of(p, r) * g.G;
+// Work items are numbered densely group by group (pf_base / pf_npairs set per launch): a
+// group's items are (request, kv head) major, query-tile pair descending minor, so the pairs of
+// one (request, head) -- which read the same K/V -- run at the same time on different SMs (L2
+// reuse) and each (request, head) starts with its longest pair.  Only pairs past a ragged
+// request's own chunk are skipped.
+__device__ __forceinline__ bool prefill_item(const DataParams& p, int i, int& r, int& h, int& pair) {
+  int gi = 0;
+  while (gi + 1 < p.ngroups && i >= p.g[gi + 1].pf_base) ++gi;
+  const DataGroup& g = p.g[gi];
+  const int rem = i - g.pf_base;
+  pair = g.pf_npairs - 1 - rem % g.pf_npairs;
+  const int rh = rem / g.pf_npairs;
+  h = rh % g.Hkv;
+  r = g.req_begin + rh / g.Hkv;
+  return 2 * pair * kRows < qlen_of(p, r) * g.G;
 }
 
 template <typename T, int D>
-__global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel(const __grid_constant__ DataParams p, int npairs,
-                                                                int hmax) {
+__global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel(const __grid_constant__ DataParams p, int n_items) {
   using F = PF<D>;
   extern __shared__ __align__(1024) char smem[];
   if (smem_u32(smem) & 1023) __trap();
@@ -446,7 +449,6 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel(const __grid_con
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + kRing);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t rank = cluster_rank();
-  const int n_items = npairs * hmax * p.nreq;
 
   if (warp == kMmaWarp) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
@@ -479,7 +481,7 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel(const __grid_con
   };
   auto geo = [&](int idx) {
     Geo e;
-    prefill_item(p, idx, npairs, hmax, e.r, e.h, e.pair);
+    prefill_item(p, idx, e.r, e.h, e.pair);
     e.g = &p.g[p.req_group[e.r]];
     e.G = e.g->G;
     e.handle = p.handles[e.r];
@@ -515,7 +517,7 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel(const __grid_con
           int idx = atomicAdd(p.counter, 1);
           while (idx < n_items) {
             int r_, h_, pr_;
-            if (prefill_item(p, idx, npairs, hmax, r_, h_, pr_)) break;
+            if (prefill_item(p, idx, r_, h_, pr_)) break;
             idx = atomicAdd(p.counter, 1);
           }
           pub = idx < n_items ? idx : -1;
@@ -532,6 +534,15 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel(const __grid_con
       }
       if (pub < 0) break;
       const Geo e = geo(pub);
+      {  // this CTA's Q rows of the item -> L2 (the softmax warps install them one item ahead)
+        const int t0 = e.t0A + (int)rank * e.tpt, ntok = min(e.tpt, e.q_len - t0);
+        const char* qb = reinterpret_cast<const char*>(e.g->q) +
+                         (((size_t)e.q_off + t0) * e.g->Hq + (size_t)e.h * e.G) * (D * 2);
+        for (int t = lane; t < ntok; t += 32)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(qb + (size_t)t * e.g->Hq * (D * 2)),
+                       "r"(e.G * D * 2)
+                       : "memory");
+      }
       const int2* row_tab = p.req_table + (size_t)e.handle * p.cap;
       const long long base_off = e.g->layer_off + (long long)e.h * e.g->head_stride;
       const int n_blk = (e.n_keys + kTpb - 1) / kTpb;
@@ -677,18 +688,14 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel(const __grid_con
     const uint32_t tO = tmem + F::OHALF * c + lane_off;
     const int nbar = 1 + (warp & 3);  // named barrier of the two warps sharing these rows
     constexpr int OCH = F::OHALF / 32;  // 32-column O chunks per half (1, 2, 4)
-    uint32_t jt = 0;
-    for (uint32_t k = 0;; ++k) {
-      const int idx = next_item(k);
-      if (idx < 0) break;
-      const Geo e = geo(idx);
-      const float c2 = e.g->scale_log2;
+    // Q of an item is installed as soon as the previous item's last S tile has been consumed
+    // (all of its QK^T retired), before that item's epilogue, so the next item's first QK^T
+    // runs while the epilogue drains O (the loader prefetched the rows into L2)
+    auto install_q = [&](const Geo& e) {
       const int t0 = e.t0A + (int)rank * e.tpt;
       const int my_tok = t0 + row / e.G;
       const bool row_ok = my_tok < e.q_len;
-      const int my_pos = e.start + my_tok;
-      const bool tail_rows = t0 + e.tpt > e.q_len;
-      {  // this thread's half of its Q row (all QK^T of the previous item retired)
+      {  // this thread's half of its Q row
         const uint4* src = reinterpret_cast<const uint4*>(
             reinterpret_cast<const char*>(e.g->q) +
             (((size_t)e.q_off + (row_ok ? my_tok : 0)) * e.g->Hq + e.h * e.G + row % e.G) * (D * 2) + c * D);
@@ -722,6 +729,18 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel(const __grid_con
           if (lane == 0) mbar_arrive_cluster_relaxed(q_full_l);
         }
       }
+    };
+    uint32_t jt = 0;
+    int idx = next_item(0);
+    if (idx >= 0) install_q(geo(idx));
+    for (uint32_t k = 0; idx >= 0; ++k) {
+      const Geo e = geo(idx);
+      const float c2 = e.g->scale_log2;
+      const int t0 = e.t0A + (int)rank * e.tpt;
+      const int my_tok = t0 + row / e.G;
+      const bool row_ok = my_tok < e.q_len;
+      const int my_pos = e.start + my_tok;
+      const bool tail_rows = t0 + e.tpt > e.q_len;
       float m = -INFINITY, l = 0.f;
       const uint32_t j0 = jt;
       for (int j = 0; j < e.n_kt; ++j) {
@@ -877,6 +896,8 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel(const __grid_con
       }
       const uint32_t gl = j0 + e.n_kt - 1;
       xl[c * 128 + row] = l;
+      const int nidx = next_item(k + 1);
+      if (nidx >= 0) install_q(geo(nidx));
       PF_T(2, mbar_wait(&pv_done[gl & 1], (gl >> 1) & 1));
       tc_fence_after();
       named_bar(nbar, 64);
@@ -906,6 +927,7 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel(const __grid_con
       }
       named_bar(nbar, 64);  // xl reused by the next item
       tc_fence_before();    // the next item's first P.V (after our p_full arrive) overwrites O
+      idx = nidx;
     }
   }
 #ifdef SKV_PF_TRACE
@@ -936,13 +958,15 @@ template <typename T, int D>
 void launch_prefill_d(const DataParams& p, cudaStream_t s) {
   static std::atomic<uint64_t> attr{0};
   ensure_smem_attr(prefill_kernel<T, D>, PF<D>::SMEM, attr);
-  int tiles = 1, heads = 1;
-  for (int i = 0; i < p.ngroups; ++i) {
-    tiles = max(tiles, (p.max_q_len * p.g[i].G + kRows - 1) / kRows);
-    heads = max(heads, p.g[i].Hkv);
+  DataParams q = p;  // dense work-item numbering, group by group (prefill_item)
+  long long items = 0;
+  for (int i = 0; i < q.ngroups; ++i) {
+    DataGroup& g = q.g[i];
+    g.pf_base = (int)items;
+    g.pf_npairs = ((p.max_q_len * g.G + kRows - 1) / kRows + 1) / 2;
+    if (g.active) items += (long long)g.nreq * g.Hkv * g.pf_npairs;
   }
-  const int npairs = (tiles + 1) / 2;
-  const long long items = (long long)npairs * heads * p.nreq;
+  if (items <= 0) return;
   const int clusters = (int)std::min<long long>(items, num_sms() / 2);
   cudaMemsetAsync(p.counter, 0, sizeof(int), s);
   cudaLaunchConfig_t cfg = {};
@@ -957,7 +981,7 @@ void launch_prefill_d(const DataParams& p, cudaStream_t s) {
   attrs[0].val.clusterDim.z = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, prefill_kernel<T, D>, p, npairs, heads);
+  cudaLaunchKernelEx(&cfg, prefill_kernel<T, D>, q, (int)items);
 }
 
 }  // namespace
