@@ -408,7 +408,8 @@ __device__ __forceinline__ int qoff_of(const DataParams& p, int r, int rl) {
 // one (request, head) -- which read the same K/V -- run at the same time on different SMs (L2
 // reuse) and each (request, head) starts with its longest pair.  Only pairs past a ragged
 // request's own chunk are skipped.
-__device__ __forceinline__ bool prefill_item(const DataParams& p, int i, int& r, int& h, int& pair) {
+__device__ __forceinline__ bool prefill_item(const DataParams& p, int i, int& r, int& h, int& pair,
+                                             int item_rows = 2 * kRows) {
   int gi = 0;
   while (gi + 1 < p.ngroups && i >= p.g[gi + 1].pf_base) ++gi;
   const DataGroup& g = p.g[gi];
@@ -417,7 +418,7 @@ __device__ __forceinline__ bool prefill_item(const DataParams& p, int i, int& r,
   const int rh = rem / g.pf_npairs;
   h = rh % g.Hkv;
   r = g.req_begin + rh / g.Hkv;
-  return 2 * pair * kRows < qlen_of(p, r) * g.G;
+  return pair * item_rows < qlen_of(p, r) * g.G;
 }
 
 template <typename T, int D>
@@ -954,6 +955,635 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel(const __grid_con
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// Ping-pong variant for head dim 128 (prefill_pp_kernel): every CTA of a pair holds TWO
+// 128-row query tiles, A and B, each with its own softmax warpgroup (warps 0-3: A, 4-7: B,
+// one thread per query row, all 128 key columns), so a TMEM lane quarter -- and an SM
+// sub-partition -- carries one A warp and one B warp whose tile phases are offset by half a
+// period: softmax(A, j) runs while the tensor core computes P.V(B, j-1) and S(B, j), and
+// vice versa.  No row-max exchange between warps; the running max is speculative (a 32-key
+// chunk is exponentiated against it and it is raised -- rescaling O, l and the chunks
+// already stored -- only when the chunk's max exceeds it by 2^kRescale).
+//   TMEM: O_A [0,128) | O_B [128,256) | S_A [256,384) | S_B [384,512); P_X over S_X [0,64).
+//   SMEM: Q_A | Q_B (K-major SW128, SS-form Q.K^T) | 5 K/V stages (same halves as above).
+// An item is four query tiles of a (request, kv head): A = tiles 0 (rank 0) and 1 (rank 1),
+// B = tiles 2 and 3; the K/V stream is shared by both.
+namespace pp {
+constexpr int kWarps = 10;  // 0-3 softmax A, 4-7 softmax B, 8 MMA, 9 scheduler + TMA
+constexpr int kThreads = kWarps * 32;
+constexpr int kD = 128;
+constexpr int kQTile = kRows * kD * 2;  // 32 KiB: 2 SW128 atom columns of 128 rows x 128 B
+constexpr int kKBytes = 2 * 64 * 128;   // this CTA's 64 keys x 128 dims
+constexpr int kVAtom = kKT * 128;       // all 128 keys x this CTA's 64 dims
+constexpr int kStage = kKBytes + kVAtom;
+constexpr int kStages = 5;
+constexpr int kKvOff = 2 * kQTile;
+constexpr int kBarOff = kKvOff + kStages * kStage;
+constexpr int kSmem = kBarOff + 512;
+constexpr int kOCol = 0, kSCol = 256;  // + 128 * X
+constexpr int kItemRows = 4 * kRows;
+static_assert(kSmem <= 227 * 1024, "shared memory");
+}  // namespace pp
+
+__device__ __forceinline__ void tmem_st16_nowait(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_ld16_issue(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                 "+r"(r[15])
+               :
+               : "memory");
+}
+template <typename T>
+__device__ __forceinline__ float2 unpack2(uint32_t u);
+template <>
+__device__ __forceinline__ float2 unpack2<__half>(uint32_t u) {
+  return __half22float2(*reinterpret_cast<__half2*>(&u));
+}
+template <>
+__device__ __forceinline__ float2 unpack2<__nv_bfloat16>(uint32_t u) {
+  return __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&u));
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+// Rare path of the ping-pong softmax (a 32-key chunk raised a row's reference max by more than
+// 2^kRescale): O (through the previous tile) and the P chunks already stored for this tile are
+// rescaled by alpha in TMEM.  Out of line to keep the hot loop small (instruction cache).
+template <typename T>
+__device__ __noinline__ void pp_rescale(uint32_t tO, uint32_t tS, int c, float alpha) {
+  for (int cc = 0; cc < 4; ++cc) {
+    float o[32];
+    tmem_ld32(tO + cc * 32, o);
+#pragma unroll
+    for (int kk = 0; kk < 32; ++kk) o[kk] *= alpha;
+    tmem_st32(tO + cc * 32, o);
+  }
+  tmem_wait_st();  // P chunks < c stored
+  for (int cc = 0; cc < c; ++cc) {
+    uint32_t q[16];
+    tmem_ld16_issue(tS + 16 * cc, q);
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      const float2 f = unpack2<T>(q[kk]);
+      q[kk] = pack2<T>(f.x * alpha, f.y * alpha);
+    }
+    tmem_st16u(tS + 16 * cc, q);
+  }
+}
+
+// 2^x for two values on the FMA/ALU pipes (FA4-style MUFU offload): x clamped to -125, split
+// x = j + f (round-to-nearest through the 1.5*2^23 magic add), 2^f by a degree-3 minimax
+// polynomial on [-0.5, 0.5] (max rel. error 1.3e-4, below fp16's half ulp), 2^j added into
+// the exponent field (LEA).  Packed FADD2/FFMA2: 10 instructions per pair.
+__device__ __forceinline__ float2 ex2_emu2(float2 x) {
+  x.x = fmaxf(x.x, -125.f);
+  x.y = fmaxf(x.y, -125.f);
+  const float2 t = __fadd2_rn(x, make_float2(12582912.f, 12582912.f));
+  const float2 jf = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
+  const float2 fr = __fadd2_rn(x, make_float2(-jf.x, -jf.y));
+  float2 q = __ffma2_rn(fr, make_float2(0.05504561f, 0.05504561f), make_float2(0.24229777f, 0.24229777f));
+  q = __ffma2_rn(q, fr, make_float2(0.69325471f, 0.69325471f));
+  q = __ffma2_rn(q, fr, make_float2(0.99994976f, 0.99994976f));
+  return make_float2(__uint_as_float(__float_as_uint(q.x) + (__float_as_uint(t.x) << 23)),
+                     __uint_as_float(__float_as_uint(q.y) + (__float_as_uint(t.y) << 23)));
+}
+#ifndef SKV_PP_EMU
+#define SKV_PP_EMU 4  // exponential pairs of every 16 (per 32-key chunk) computed by ex2_emu2
+#endif
+
+// warp-wide issue: the whole (converged) warp runs the MMA loop, one elected lane issues --
+// descriptors stay warp-uniform, no per-MMA lane-select loop
+__device__ __forceinline__ void mma_ss_pair_e(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_ts_pair_e(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+// eight K=16 steps of one tile in one asm block: one elect, only the descriptors' low words
+// move (immediate steps: Q atom column 16 KiB / K atom column 8 KiB per 4 steps, 32 B per step;
+// V 2 KiB and P 8 TMEM columns per step), high words are compile-time constants; `acc0` =
+// accumulate on the first step
+template <uint32_t AHI, uint32_t BHI>
+__device__ __forceinline__ void qk8_pair(uint32_t tmem_d, uint32_t alo, uint32_t blo, uint32_t idesc, uint32_t acc0) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\t"
+      ".reg .b32 al<8>, bl<8>, ah, bh;\n\t.reg .b64 a<8>, b<8>;\n\t"
+      "mov.b32 ah, %5;\n\tmov.b32 bh, %6;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "add.u32 al0, %1, 0;\n\tmov.b64 a0, {al0, ah};\n\t"
+      "add.u32 bl0, %2, 0;\n\tmov.b64 b0, {bl0, bh};\n\t"
+      "add.u32 al1, %1, 2;\n\tmov.b64 a1, {al1, ah};\n\t"
+      "add.u32 bl1, %2, 2;\n\tmov.b64 b1, {bl1, bh};\n\t"
+      "add.u32 al2, %1, 4;\n\tmov.b64 a2, {al2, ah};\n\t"
+      "add.u32 bl2, %2, 4;\n\tmov.b64 b2, {bl2, bh};\n\t"
+      "add.u32 al3, %1, 6;\n\tmov.b64 a3, {al3, ah};\n\t"
+      "add.u32 bl3, %2, 6;\n\tmov.b64 b3, {bl3, bh};\n\t"
+      "add.u32 al4, %1, 1024;\n\tmov.b64 a4, {al4, ah};\n\t"
+      "add.u32 bl4, %2, 512;\n\tmov.b64 b4, {bl4, bh};\n\t"
+      "add.u32 al5, %1, 1026;\n\tmov.b64 a5, {al5, ah};\n\t"
+      "add.u32 bl5, %2, 514;\n\tmov.b64 b5, {bl5, bh};\n\t"
+      "add.u32 al6, %1, 1028;\n\tmov.b64 a6, {al6, ah};\n\t"
+      "add.u32 bl6, %2, 516;\n\tmov.b64 b6, {bl6, bh};\n\t"
+      "add.u32 al7, %1, 1030;\n\tmov.b64 a7, {al7, ah};\n\t"
+      "add.u32 bl7, %2, 518;\n\tmov.b64 b7, {bl7, bh};\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a0, b0, %3, p;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a1, b1, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a2, b2, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a3, b3, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a4, b4, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a5, b5, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a6, b6, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a7, b7, %3, 1;\n\t"
+      "}"
+      ::"r"(tmem_d), "r"(alo), "r"(blo), "r"(idesc), "r"(acc0), "n"(AHI), "n"(BHI));
+}
+template <uint32_t BHI>
+__device__ __forceinline__ void pv8_pair(uint32_t tmem_d, uint32_t tmem_a, uint32_t blo, uint32_t idesc, uint32_t acc0) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\t"
+      ".reg .b32 a<8>, bl<8>, bh;\n\t.reg .b64 b<8>;\n\t"
+      "mov.b32 bh, %5;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "add.u32 a0, %1, 0;\n\t"
+      "add.u32 bl0, %2, 0;\n\tmov.b64 b0, {bl0, bh};\n\t"
+      "add.u32 a1, %1, 8;\n\t"
+      "add.u32 bl1, %2, 128;\n\tmov.b64 b1, {bl1, bh};\n\t"
+      "add.u32 a2, %1, 16;\n\t"
+      "add.u32 bl2, %2, 256;\n\tmov.b64 b2, {bl2, bh};\n\t"
+      "add.u32 a3, %1, 24;\n\t"
+      "add.u32 bl3, %2, 384;\n\tmov.b64 b3, {bl3, bh};\n\t"
+      "add.u32 a4, %1, 32;\n\t"
+      "add.u32 bl4, %2, 512;\n\tmov.b64 b4, {bl4, bh};\n\t"
+      "add.u32 a5, %1, 40;\n\t"
+      "add.u32 bl5, %2, 640;\n\tmov.b64 b5, {bl5, bh};\n\t"
+      "add.u32 a6, %1, 48;\n\t"
+      "add.u32 bl6, %2, 768;\n\tmov.b64 b6, {bl6, bh};\n\t"
+      "add.u32 a7, %1, 56;\n\t"
+      "add.u32 bl7, %2, 896;\n\tmov.b64 b7, {bl7, bh};\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a0], b0, %3, p;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a1], b1, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a2], b2, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a3], b3, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a4], b4, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a5], b5, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a6], b6, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a7], b7, %3, 1;\n\t"
+      "}"
+      ::"r"(tmem_d), "r"(tmem_a), "r"(blo), "r"(idesc), "r"(acc0), "n"(BHI));
+}
+__device__ __forceinline__ void commit_pair_e(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+          smem_u32(bar)),
+      "h"((unsigned short)3)
+      : "memory");
+}
+
+template <typename T>
+__global__ void __launch_bounds__(pp::kThreads, 1) prefill_pp_kernel(const __grid_constant__ DataParams p, int n_items) {
+  using namespace pp;
+  extern __shared__ __align__(1024) char smem[];
+  if (smem_u32(smem) & 1023) __trap();
+  char* qbase = smem;  // [X][128 rows x 128 d]
+  char* kvbase = smem + kKvOff;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBarOff);
+  constexpr int ST = kStages;
+  uint64_t* kv_full = bars;                 // [stages] leader: both CTAs' bytes
+  uint64_t* kv_empty = bars + ST;           // [stages] both CTAs (multicast commit)
+  uint64_t* q_full = bars + 2 * ST;         // [X] leader: 8 warp arrivals per item
+  uint64_t* p_full = bars + 2 * ST + 2;     // [X] leader: 8 warp arrivals per tile
+  uint64_t* s_full = bars + 2 * ST + 4;     // [X] both CTAs (multicast commit)
+  uint64_t* o_done = bars + 2 * ST + 6;     // [X] both CTAs: the item's last P.V retired
+  uint64_t* item_full = bars + 2 * ST + 8;  // [kRing] both CTAs
+  int* ring = reinterpret_cast<int*>(bars + 2 * ST + 8 + kRing);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + kRing);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t rank = cluster_rank();
+#ifdef SKV_PF_TRACE
+  long long pf_acc[5] = {0, 0, 0, 0, 0};
+  const long long pf_start = clock64();
+  long long pf_tiles = 0;
+#endif
+
+  if (warp == 8) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < ST; ++i) {
+      mbar_init_n(&kv_full[i], 1);
+      mbar_init_n(&kv_empty[i], 1);
+    }
+    for (int x = 0; x < 2; ++x) {
+      mbar_init_n(&q_full[x], 8);
+      mbar_init_n(&p_full[x], 8);
+      mbar_init_n(&s_full[x], 1);
+      mbar_init_n(&o_done[x], 1);
+    }
+    for (int i = 0; i < kRing; ++i) mbar_init_n(&item_full[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  struct Geo {
+    int r, h, quad, handle, ctx, start, tpt, t0Q, n_keys, n_kt, rl, G, q_len, q_off;
+    const DataGroup* g;
+  };
+  auto geo = [&](int idx) {
+    Geo e;
+    prefill_item(p, idx, e.r, e.h, e.quad, kItemRows);
+    e.g = &p.g[p.req_group[e.r]];
+    e.G = e.g->G;
+    e.handle = p.handles[e.r];
+    e.ctx = p.req_tokens[e.handle];
+    e.rl = e.r - e.g->req_begin;
+    e.q_len = qlen_of(p, e.r);
+    e.q_off = qoff_of(p, e.r, e.rl);
+    e.start = e.ctx - e.q_len;
+    e.tpt = kRows / e.G;
+    e.t0Q = 4 * e.quad * e.tpt;
+    e.n_keys = min(e.ctx, e.start + e.t0Q + 4 * e.tpt);
+    e.n_kt = (e.n_keys + kKT - 1) / kKT;
+    return e;
+  };
+  auto next_item = [&](uint32_t k) {
+    mbar_wait_cl(&item_full[k % kRing], (k / kRing) & 1);
+    return *reinterpret_cast<volatile int*>(&ring[k % kRing]);
+  };
+
+  if (warp == 9) {  // ----------------------------------------- scheduler (leader) + K/V streaming (both)
+    uint32_t jt = 0;
+    const uint32_t ring_peer = mapa_u32(smem_u32(ring), 1), item_peer = mapa_u32(smem_u32(item_full), 1);
+    const uint32_t kv_full_l = mapa_u32(smem_u32(kv_full), 0);
+    for (uint32_t k = 0;; ++k) {
+      int pub;
+      if (rank == 0) {
+        if (lane == 0) {
+          int idx = atomicAdd(p.counter, 1);
+          while (idx < n_items) {
+            int r_, h_, pr_;
+            if (prefill_item(p, idx, r_, h_, pr_, kItemRows)) break;
+            idx = atomicAdd(p.counter, 1);
+          }
+          pub = idx < n_items ? idx : -1;
+          const uint32_t slot = k % kRing;
+          ring[slot] = pub;
+          asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(ring_peer + 4 * slot), "r"(pub) : "memory");
+          asm volatile("mbarrier.arrive.release.cluster.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&item_full[slot]))
+                       : "memory");
+          mbar_arrive_cluster_rel(item_peer + 8 * slot);
+        }
+        pub = __shfl_sync(0xffffffffu, pub, 0);
+      } else {
+        pub = next_item(k);
+      }
+      if (pub < 0) break;
+      const Geo e = geo(pub);
+#pragma unroll
+      for (int x = 0; x < 2; ++x) {  // this CTA's Q rows of both tiles -> L2
+        const int t0 = e.t0Q + (2 * x + (int)rank) * e.tpt, ntok = min(e.tpt, e.q_len - t0);
+        const char* qb = reinterpret_cast<const char*>(e.g->q) +
+                         (((size_t)e.q_off + t0) * e.g->Hq + (size_t)e.h * e.G) * (kD * 2);
+        for (int t = lane; t < ntok; t += 32)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(qb + (size_t)t * e.g->Hq * (kD * 2)),
+                       "r"(e.G * kD * 2)
+                       : "memory");
+      }
+      const int2* row_tab = p.req_table + (size_t)e.handle * p.cap;
+      const long long base_off = e.g->layer_off + (long long)e.h * e.g->head_stride;
+      const int n_blk = (e.n_keys + kTpb - 1) / kTpb;
+      int2 ent_next = lane < n_blk ? row_tab[lane] : make_int2(-1, 0);
+      int row0 = 0;
+      bool valid = false;
+      for (int j = 0; j < e.n_kt; ++j, ++jt) {
+        if ((j & 3) == 0) {
+          valid = ent_next.x >= 0;
+          row0 = valid ? (int)(((long long)ent_next.x * p.merged_stride + (long long)ent_next.y * e.g->native_stride +
+                                base_off) / (2 * kD))
+                       : 0;
+          const int nx = (j + 4) * 8 + lane;
+          ent_next = nx < n_blk ? row_tab[nx] : make_int2(-1, 0);
+        }
+        const int st = jt % ST;
+        if (jt >= (uint32_t)ST) {
+          if (lane == 0) PF_T(0, mbar_wait(&kv_empty[st], ((jt / ST) - 1) & 1));
+          __syncwarp();
+        }
+        const int grp = (j & 3) * 8;
+        const bool mine = lane >= grp && lane < grp + 8 && valid;
+        const int nb = __popc(__ballot_sync(0xffffffffu, mine));
+        if (rank == 0 && lane == 0) mbar_expect_tx_v3(&kv_full[st], nb * (64 * kD));
+        __syncwarp();
+        if (mine) {
+          const int b = lane - grp;
+          const uint32_t sK = smem_u32(kvbase + st * kStage), sV = sK + kKBytes;
+          const uint32_t bar = kv_full_l + 8 * st;
+          if ((b >> 2) == (int)rank) {
+            tma_load_2d_pair(sK + (b & 3) * 2048, &p.kv_tmap, 0, row0, bar);
+            tma_load_2d_pair(sK + 8192 + (b & 3) * 2048, &p.kv_tmap, 64, row0, bar);
+          }
+          tma_load_2d_pair(sV + b * (kTpb * 128), &p.kv_tmap, (int)rank * 64, row0 + kTpb, bar);
+        }
+      }
+    }
+  } else if (warp == 8) {  // ------------------------------ MMA issue (leader; whole warp, elected lane)
+    if (rank == 0) {
+      const uint32_t idesc_qk = make_idesc_pair(p.dtype, 0, kKT);
+      const uint32_t idesc_pv = make_idesc_pair(p.dtype, 1, kD);
+      const uint64_t k_desc0 = make_desc(smem_u32(kvbase), 16, 1024);
+      const uint64_t v_desc0 = make_desc(smem_u32(kvbase) + kKBytes, kVAtom, 1024);
+      const uint64_t q_desc0 = make_desc(smem_u32(qbase), 16, 1024);
+      uint32_t jt = 0;
+      const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);  // warp-uniform (uniform datapath)
+      for (uint32_t k = 0;; ++k) {
+        const int idx = __shfl_sync(0xffffffffu, next_item(k), 0);
+        if (idx < 0) break;
+        const Geo e = geo(idx);
+        const uint32_t j0 = jt;
+        const int J = __shfl_sync(0xffffffffu, e.n_kt, 0);
+        auto wait_kv = [&](int j) {
+          const uint32_t gj = j0 + j;
+          PF_T(1, mbar_wait(&kv_full[gj % ST], (gj / ST) & 1));
+          tc_fence_after();
+        };
+        auto k_descs = [&](int j, uint64_t (&d)[8]) {
+          const uint64_t b = k_desc0 + (uint64_t)(((j0 + j) % ST) * (kStage >> 4));
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) d[kk] = b + (uint64_t)(((kk >> 2) * 8192 + (kk & 3) * 32) >> 4);
+        };
+        auto v_descs = [&](int j, uint64_t (&d)[8]) {
+          const uint64_t b = v_desc0 + (uint64_t)(((j0 + j) % ST) * (kStage >> 4));
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) d[kk] = b + (uint64_t)((kk * kTpb * 128) >> 4);
+        };
+        auto pin = [](const uint64_t* d, int n) {
+#pragma unroll
+          for (int i = 0; i < n; ++i) asm volatile("" ::"l"(d[i]));
+        };
+        // descriptor high words: SBO 1024 B, version 1, SWIZZLE_128B (K-major Q/K and MN-major V)
+        constexpr uint32_t kHi = (1024u >> 4) | (1u << 14) | (2u << 29);
+        auto qk = [&](int x, const uint64_t (&d)[8]) {
+          qk8_pair<kHi, kHi>(tm + kSCol + 128 * x, (uint32_t)q_desc0 + (uint32_t)((x * kQTile) >> 4), (uint32_t)d[0],
+                             idesc_qk, 0u);
+          commit_pair_e(&s_full[x]);
+        };
+        auto pv = [&](int x, int j, const uint64_t (&d)[8]) {
+          pv8_pair<kHi>(tm + kOCol + 128 * x, tm + kSCol + 128 * x, (uint32_t)d[0], idesc_pv, j > 0 ? 1u : 0u);
+          if (j == J - 1) commit_pair_e(&o_done[x]);
+        };
+        {
+          uint64_t kd[8];
+          k_descs(0, kd);
+          pin(kd, 8);
+          PF_T(0, mbar_wait(&q_full[0], k & 1));
+          tc_fence_after();
+          wait_kv(0);
+          qk(0, kd);
+          PF_T(0, mbar_wait(&q_full[1], k & 1));
+          tc_fence_after();
+          qk(1, kd);
+        }
+        for (int j = 0; j < J; ++j) {
+          const uint32_t gj = j0 + j;
+          uint64_t vd[8], kd[8];
+          v_descs(j, vd);
+          k_descs(j + 1, kd);
+          pin(vd, 8);
+          pin(kd, 8);
+          PF_T(2, mbar_wait(&p_full[0], gj & 1));
+          tc_fence_after();
+          PF_T(4, pv(0, j, vd));
+          if (j + 1 < J) {
+            wait_kv(j + 1);
+            PF_T(4, qk(0, kd));
+          }
+          PF_T(3, mbar_wait(&p_full[1], gj & 1));
+          tc_fence_after();
+          PF_T(4, pv(1, j, vd));
+          commit_pair_e(&kv_empty[gj % ST]);
+          if (j + 1 < J) PF_T(4, qk(1, kd));
+        }
+        jt += J;
+      }
+    }
+    __syncwarp();
+  } else {  // ---------------------------------------------------------------- softmax warps
+    const int x = warp >> 2;  // query tile (A = 0, B = 1)
+    const int row = (warp & 3) * 32 + lane;
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const uint32_t tS = tmem + kSCol + 128 * x + lane_off;
+    const uint32_t tO = tmem + kOCol + 128 * x + lane_off;
+    const uint32_t q_full_l = mapa_u32(smem_u32(&q_full[x]), 0), p_full_l = mapa_u32(smem_u32(&p_full[x]), 0);
+    char* qtile = qbase + x * kQTile;
+    auto install_q = [&](const Geo& e) {  // this thread's Q row into the tile's SW128 K-major layout
+      const int t0 = e.t0Q + (2 * x + (int)rank) * e.tpt;
+      const int my_tok = t0 + row / e.G;
+      const bool row_ok = my_tok < e.q_len;
+      const uint4* src = reinterpret_cast<const uint4*>(
+          reinterpret_cast<const char*>(e.g->q) +
+          (((size_t)e.q_off + (row_ok ? my_tok : 0)) * e.g->Hq + e.h * e.G + row % e.G) * (kD * 2));
+      uint4 v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = row_ok ? src[i] : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int a = i >> 3, ch = i & 7;
+        *reinterpret_cast<uint4*>(qtile + a * (kRows * 128) + (row >> 3) * 1024 + (row & 7) * 128 +
+                                  ((ch ^ (row & 7)) << 4)) = v[i];
+      }
+      fence_async_smem();  // generic-proxy writes read by the (leader's) tensor core
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster_rel(q_full_l);
+    };
+    uint32_t tc = 0;
+    int idx = next_item(0);
+    if (idx >= 0) install_q(geo(idx));
+    for (uint32_t k = 0; idx >= 0; ++k) {
+      const Geo e = geo(idx);
+      const float c2 = e.g->scale_log2;
+      const int t0 = e.t0Q + (2 * x + (int)rank) * e.tpt;
+      const int my_tok = t0 + row / e.G;
+      const bool row_ok = my_tok < e.q_len;
+      const int my_pos = e.start + my_tok;
+      const bool tail_rows = t0 + e.tpt > e.q_len;
+      float m = -INFINITY;  // reference max (log2 domain) of the row's P values
+      float2 lsum = make_float2(0.f, 0.f);
+      for (int j = 0; j < e.n_kt; ++j) {
+        const uint32_t gj = tc + j;
+        PF_T(0, mbar_wait(&s_full[x], gj & 1));  // CTA scope: an acquire.cluster wait invalidates L1 (CCTL.IVALL)
+        tc_fence_after();
+        const bool last_partial = j == e.n_kt - 1 && (j + 1) * kKT > e.n_keys;
+        if (x == 0 && last_partial) {  // V rows past the keys (stale or another owner's bytes) -> 0
+          char* sV = kvbase + (gj % ST) * kStage + kKBytes;
+          const int first = e.n_keys - j * kKT;
+          for (int i = tid; i < kKT * 8; i += 128)
+            if ((i >> 3) >= first) *reinterpret_cast<uint4*>(sV + (i >> 3) * 128 + (i & 7) * 16) = make_uint4(0, 0, 0, 0);
+        }
+        const bool masked = (j * kKT + kKT - 1 > e.start + t0) || tail_rows;
+        const int kb = j * kKT;
+#ifndef SKV_PP_STEP
+#define SKV_PP_STEP 64  // key columns per softmax step (one TMEM-load wait, one max vote)
+#endif
+        constexpr int SW = SKV_PP_STEP;
+        // one step: SW scores of this row -> masked, max-checked, exponentiated, P stored at
+        // packed column h*SW/2 (P(h) overwrites only S columns the steps <= h have consumed)
+        auto step = [&](uint32_t (&r)[SW], int h) {
+          if (masked) {
+#pragma unroll
+            for (int kk = 0; kk < SW; ++kk)
+              if (!(row_ok && kb + SW * h + kk <= my_pos)) r[kk] = __float_as_uint(-INFINITY);
+          }
+          float ma = __uint_as_float(r[0]), mb = __uint_as_float(r[1]);
+#pragma unroll
+          for (int kk = 2; kk < SW; kk += 4) {
+            ma = fmax3(ma, __uint_as_float(r[kk]), __uint_as_float(r[kk + 1]));
+            mb = fmax3(mb, __uint_as_float(r[kk + 2]), __uint_as_float(r[kk + 3]));
+          }
+          const float mt = fmaxf(ma, mb) * c2;
+          if (j == 0 && h == 0) m = mt;  // first step of an item: the reference is its max
+          const bool need = mt > m + kRescale;
+          if (__any_sync(0xffffffffu, need)) {  // raise the reference max: rescale O, l and stored P
+            const float mn = need ? mt : m;
+            const float alpha = need ? ex2(m - mn) : 1.f;
+            m = mn;
+            lsum.x *= alpha;
+            lsum.y *= alpha;
+            pp_rescale<T>(tO, tS, h * (SW / 32) * 2, alpha);
+          }
+          const float mu = m == -INFINITY ? 0.f : m;
+          const float2 c2v = make_float2(c2, c2), nmv = make_float2(-mu, -mu);
+          uint32_t pk[SW / 2];
+          float2 v[SW / 2];
+#pragma unroll
+          for (int i = 0; i < SW / 2; ++i) {
+            const float2 a = __ffma2_rn(make_float2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])), c2v, nmv);
+            if ((i & 15) >= 16 - SKV_PP_EMU) v[i] = ex2_emu2(a);
+            else v[i] = make_float2(ex2(a.x), ex2(a.y));
+          }
+#pragma unroll
+          for (int i = 0; i < SW / 2; ++i) pk[i] = pack2<T>(v[i].x, v[i].y);
+#pragma unroll
+          for (int w = SW / 4; w >= 1; w >>= 1)  // pairwise sums
+#pragma unroll
+            for (int i = 0; i < w; ++i) v[i] = __fadd2_rn(v[i], v[i + w]);
+          lsum = __fadd2_rn(lsum, v[0]);
+#pragma unroll
+          for (int q = 0; q < SW / 32; ++q) tmem_st16_nowait(tS + h * (SW / 2) + 16 * q, pk + 16 * q);
+        };
+#pragma unroll
+        for (int h = 0; h < 128 / SW; ++h) {
+          uint32_t r[SW];
+#pragma unroll
+          for (int q = 0; q < SW / 32; ++q) tmem_ld32_issue(tS + h * SW + 32 * q, *reinterpret_cast<uint32_t(*)[32]>(r + 32 * q));
+#pragma unroll
+          for (int q = 0; q < SW / 32; ++q) tmem_ld32_wait(*reinterpret_cast<uint32_t(*)[32]>(r + 32 * q));
+          step(r, h);
+        }
+        tmem_wait_st();
+        if (x == 0 && last_partial) fence_async_smem();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (x == 0 && last_partial) mbar_arrive_cluster(p_full_l);  // orders the V-row zeroing
+          else mbar_arrive_cluster_relaxed(p_full_l);
+        }
+      }
+      tc += e.n_kt;
+#ifdef SKV_PF_TRACE
+      pf_tiles += e.n_kt;
+#endif
+      const int nidx = next_item(k + 1);
+      if (nidx >= 0) install_q(geo(nidx));  // all Q.K^T of this item retired
+      PF_T(1, mbar_wait(&o_done[x], k & 1));
+      tc_fence_after();
+      const float lt = lsum.x + lsum.y;
+      const float inv = lt > 0.f ? 1.f / lt : 0.f;
+      char* dst = reinterpret_cast<char*>(e.g->out) +
+                  (((size_t)e.q_off + (row_ok ? my_tok : 0)) * e.g->Hq + e.h * e.G + row % e.G) * (kD * 2);
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        float o[32];
+        tmem_ld32(tO + cc * 32, o);
+        if (row_ok) {
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            uint4 v;
+            v.x = pack2<T>(o[8 * q4] * inv, o[8 * q4 + 1] * inv);
+            v.y = pack2<T>(o[8 * q4 + 2] * inv, o[8 * q4 + 3] * inv);
+            v.z = pack2<T>(o[8 * q4 + 4] * inv, o[8 * q4 + 5] * inv);
+            v.w = pack2<T>(o[8 * q4 + 6] * inv, o[8 * q4 + 7] * inv);
+            *reinterpret_cast<uint4*>(dst + cc * 64 + q4 * 16) = v;
+          }
+        }
+      }
+      tc_fence_before();  // the next item's first P.V (after our p_full arrive) overwrites O
+      idx = nidx;
+    }
+  }
+#ifdef SKV_PF_TRACE
+  if (p.trace) {  // [cta][16]: loader kv_empty 0; mma q_full 1, kv_full 2, p_full A 3, B 4; softmax A
+                  // (warp 0) s_full 5, o_done 6; B (warp 4) s_full 9, o_done 10; cycles 13, tiles 14
+    unsigned long long* t = p.trace + (size_t)blockIdx.x * 16;
+    if (warp == 9 && lane == 0) t[0] = pf_acc[0];
+    if (warp == 8 && lane == 0) {
+      for (int i = 0; i < 4; ++i) t[1 + i] = pf_acc[i];
+      t[15] = pf_acc[4];
+    }
+    if (warp < 8 && (tid & 127) == 0)
+      for (int i = 0; i < 2; ++i) t[5 + 4 * (warp >> 2) + i] = pf_acc[i];
+    if (tid == 0) {
+      t[13] = clock64() - pf_start;
+      t[14] = pf_tiles;
+    }
+  }
+#endif
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 8) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
 template <typename T, int D>
 void launch_prefill_d(const DataParams& p, cudaStream_t s) {
   static std::atomic<uint64_t> attr{0};
@@ -984,6 +1614,45 @@ void launch_prefill_d(const DataParams& p, cudaStream_t s) {
   cudaLaunchKernelEx(&cfg, prefill_kernel<T, D>, q, (int)items);
 }
 
+template <typename T>
+void launch_prefill_pp(const DataParams& p, cudaStream_t s) {
+  static std::atomic<uint64_t> attr{0};
+  ensure_smem_attr(prefill_pp_kernel<T>, pp::kSmem, attr);
+  DataParams q = p;
+  long long items = 0;
+  for (int i = 0; i < q.ngroups; ++i) {
+    DataGroup& g = q.g[i];
+    g.pf_base = (int)items;
+    g.pf_npairs = (p.max_q_len * g.G + pp::kItemRows - 1) / pp::kItemRows;  // items per (request, kv head)
+    if (g.active) items += (long long)g.nreq * g.Hkv * g.pf_npairs;
+  }
+  if (items <= 0) return;
+  const int clusters = (int)std::min<long long>(items, num_sms() / 2);
+  cudaMemsetAsync(p.counter, 0, sizeof(int), s);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * clusters, 1, 1);
+  cfg.blockDim = dim3(pp::kThreads, 1, 1);
+  cfg.dynamicSmemBytes = pp::kSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = 2;
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, prefill_pp_kernel<T>, q, (int)items);
+}
+
+// SKV_PREFILL_PP=0 selects the one-tile-per-CTA kernel for head dim 128 as well
+bool use_pp() {
+  static const bool on = [] {
+    const char* e = getenv("SKV_PREFILL_PP");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 }  // namespace
 
 // One launch per head dim present: the groups of other head dims are marked inactive in the
@@ -1003,11 +1672,11 @@ void launch_prefill(const DataParams& p, cudaStream_t s) {
       if (q.g[i].D == D) q.scale_log2 = q.g[i].scale_log2;
     if (p.dtype == 0) {
       if (D == 64) launch_prefill_d<__half, 64>(q, s);
-      else if (D == 128) launch_prefill_d<__half, 128>(q, s);
+      else if (D == 128) use_pp() ? launch_prefill_pp<__half>(q, s) : launch_prefill_d<__half, 128>(q, s);
       else launch_prefill_d<__half, 256>(q, s);
     } else {
       if (D == 64) launch_prefill_d<__nv_bfloat16, 64>(q, s);
-      else if (D == 128) launch_prefill_d<__nv_bfloat16, 128>(q, s);
+      else if (D == 128) use_pp() ? launch_prefill_pp<__nv_bfloat16>(q, s) : launch_prefill_d<__nv_bfloat16, 128>(q, s);
       else launch_prefill_d<__nv_bfloat16, 256>(q, s);
     }
   }

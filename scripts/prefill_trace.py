@@ -42,6 +42,9 @@ if os.environ.get("SEAKV_PREFILL_V", "10") == "10":  # CTA pairs: softmax halves
     names = ["load:kv_empty", "mma:q_full", "mma:kv_full", "mma:p_full", "mma:issue",
              "sm0:s_full", "sm0:pv_corr", "sm0:pv_last", "sm0:max_xchg", "sm1:s_full", "sm1:pv_corr", "sm1:pv_last",
              "sm1:max_xchg", "-", "-", "mma:descs"]
+if os.environ.get("SKV_PREFILL_PP", "1") != "0":  # ping-pong kernel (two query tiles per CTA)
+    names = ["load:kv_empty", "mma:q_full", "mma:kv_full", "mma:p_full_A", "mma:p_full_B",
+             "smA:s_full", "smA:o_done", "-", "-", "smB:s_full", "smB:o_done", "-", "-", "-", "-", "mma:issue"]
 res = {n: round(float((t[:, i] / tot).mean()), 4) for i, n in enumerate(names) if n != "-"}
 res["ctas"] = int(len(t))
 res["mean_cta_us_at_1.9GHz"] = round(float(tot.mean()) / 1.9e3, 1)
