@@ -969,7 +969,10 @@ __global__ void __launch_bounds__(kThreadsV3, 1) prefill_kernel(const __grid_con
 // An item is four query tiles of a (request, kv head): A = tiles 0 (rank 0) and 1 (rank 1),
 // B = tiles 2 and 3; the K/V stream is shared by both.
 namespace pp {
-constexpr int kWarps = 10;  // 0-3 softmax A, 4-7 softmax B, 8 MMA, 9 scheduler + TMA
+constexpr int kWarps = 12;  // 0-3 softmax A, 4-7 softmax B, 8 MMA, 9 scheduler + TMA, 10-11 idle
+// registers: launched at 168 per thread (12 warps), then setmaxnreg moves 80 per thread from
+// warpgroup 2 (MMA, loader) to the two softmax warpgroups
+constexpr int kRegSoftmax = 208, kRegOther = 88;  // 2*208 + 88 = 3*168
 constexpr int kThreads = kWarps * 32;
 constexpr int kD = 128;
 constexpr int kQTile = kRows * kD * 2;  // 32 KiB: 2 SW128 atom columns of 128 rows x 128 B
@@ -1066,7 +1069,7 @@ __device__ __forceinline__ float2 ex2_emu2(float2 x) {
                      __uint_as_float(__float_as_uint(q.y) + (__float_as_uint(t.y) << 23)));
 }
 #ifndef SKV_PP_EMU
-#define SKV_PP_EMU 4  // exponential pairs of every 16 (per 32-key chunk) computed by ex2_emu2
+#define SKV_PP_EMU 6  // exponential pairs of every 16 (per 32 keys) computed by ex2_emu2 (swept: 0-10, 6 best)
 #endif
 
 // warp-wide issue: the whole (converged) warp runs the MMA loop, one elected lane issues --
@@ -1249,7 +1252,10 @@ __global__ void __launch_bounds__(pp::kThreads, 1) prefill_pp_kernel(const __gri
     return *reinterpret_cast<volatile int*>(&ring[k % kRing]);
   };
 
-  if (warp == 9) {  // ----------------------------------------- scheduler (leader) + K/V streaming (both)
+  if (warp >= 8) {  // warpgroup 2: one setmaxnreg for all four warps (.aligned), then the roles
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegOther));
+  if (warp >= 10) {  // idle
+  } else if (warp == 9) {  // ------------------------------- scheduler (leader) + K/V streaming (both)
     uint32_t jt = 0;
     const uint32_t ring_peer = mapa_u32(smem_u32(ring), 1), item_peer = mapa_u32(smem_u32(item_full), 1);
     const uint32_t kv_full_l = mapa_u32(smem_u32(kv_full), 0);
@@ -1324,7 +1330,7 @@ __global__ void __launch_bounds__(pp::kThreads, 1) prefill_pp_kernel(const __gri
         }
       }
     }
-  } else if (warp == 8) {  // ------------------------------ MMA issue (leader; whole warp, elected lane)
+  } else {  // warp 8 --------------------------------------- MMA issue (leader; whole warp, elected lane)
     if (rank == 0) {
       const uint32_t idesc_qk = make_idesc_pair(p.dtype, 0, kKT);
       const uint32_t idesc_pv = make_idesc_pair(p.dtype, 1, kD);
@@ -1405,7 +1411,9 @@ __global__ void __launch_bounds__(pp::kThreads, 1) prefill_pp_kernel(const __gri
       }
     }
     __syncwarp();
+  }
   } else {  // ---------------------------------------------------------------- softmax warps
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegSoftmax));
     const int x = warp >> 2;  // query tile (A = 0, B = 1)
     const int row = (warp & 3) * 32 + lane;
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
@@ -1471,13 +1479,14 @@ __global__ void __launch_bounds__(pp::kThreads, 1) prefill_pp_kernel(const __gri
             for (int kk = 0; kk < SW; ++kk)
               if (!(row_ok && kb + SW * h + kk <= my_pos)) r[kk] = __float_as_uint(-INFINITY);
           }
-          float ma = __uint_as_float(r[0]), mb = __uint_as_float(r[1]);
+          float mx4[4] = {__uint_as_float(r[0]), __uint_as_float(r[1]), __uint_as_float(r[2]), __uint_as_float(r[3])};
 #pragma unroll
-          for (int kk = 2; kk < SW; kk += 4) {
-            ma = fmax3(ma, __uint_as_float(r[kk]), __uint_as_float(r[kk + 1]));
-            mb = fmax3(mb, __uint_as_float(r[kk + 2]), __uint_as_float(r[kk + 3]));
-          }
-          const float mt = fmaxf(ma, mb) * c2;
+          for (int kk = 4; kk < SW; kk += 8)  // four independent 3-input max chains
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              mx4[u] = kk + 2 * u + 1 < SW ? fmax3(mx4[u], __uint_as_float(r[kk + 2 * u]), __uint_as_float(r[kk + 2 * u + 1]))
+                                           : mx4[u];
+          const float mt = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * c2;
           if (j == 0 && h == 0) m = mt;  // first step of an item: the reference is its max
           const bool need = mt > m + kRescale;
           if (__any_sync(0xffffffffu, need)) {  // raise the reference max: rescale O, l and stored P
@@ -1508,6 +1517,25 @@ __global__ void __launch_bounds__(pp::kThreads, 1) prefill_pp_kernel(const __gri
 #pragma unroll
           for (int q = 0; q < SW / 32; ++q) tmem_st16_nowait(tS + h * (SW / 2) + 16 * q, pk + 16 * q);
         };
+#if SKV_PP_STEP == 64 && !defined(SKV_PP_NOPREFETCH)
+        {  // the second step's scores load while the first step computes
+          uint32_t ra[64], rb[64];
+          auto& ra0 = *reinterpret_cast<uint32_t(*)[32]>(ra);
+          auto& ra1 = *reinterpret_cast<uint32_t(*)[32]>(ra + 32);
+          auto& rb0 = *reinterpret_cast<uint32_t(*)[32]>(rb);
+          auto& rb1 = *reinterpret_cast<uint32_t(*)[32]>(rb + 32);
+          tmem_ld32_issue(tS, ra0);
+          tmem_ld32_issue(tS + 32, ra1);
+          tmem_ld32_wait(ra0);
+          tmem_ld32_wait(ra1);
+          tmem_ld32_issue(tS + 64, rb0);
+          tmem_ld32_issue(tS + 96, rb1);
+          step(ra, 0);
+          tmem_ld32_wait(rb0);
+          tmem_ld32_wait(rb1);
+          step(rb, 1);
+        }
+#else
 #pragma unroll
         for (int h = 0; h < 128 / SW; ++h) {
           uint32_t r[SW];
@@ -1517,6 +1545,7 @@ __global__ void __launch_bounds__(pp::kThreads, 1) prefill_pp_kernel(const __gri
           for (int q = 0; q < SW / 32; ++q) tmem_ld32_wait(*reinterpret_cast<uint32_t(*)[32]>(r + 32 * q));
           step(r, h);
         }
+#endif
         tmem_wait_st();
         if (x == 0 && last_partial) fence_async_smem();
         tc_fence_before();
