@@ -660,9 +660,8 @@ def run_gpu(args):
                 tpk, tpk_kind = float(json.load(f)["bf16_tflops"]), "measured (burst, cuBLAS bf16)"
         except Exception:  # noqa: BLE001
             tpk, tpk_kind = 2250.0, "fallback (nominal dense bf16)"
-        pf = {"kernel": "skv prefill_kernel<T, 128> (cta_group::2 tcgen05.mma, TMA, TMEM)", "peak": tpk,
-              "peak_kind": tpk_kind, "unit": "TFLOP/s", "bound": "tensor",
-              "ncu": "profiles/r01_ncu_prefill_v10_final.txt (tensor pipe active % of cycles)"}
+        pf = {"kernel": PREFILL_KERNEL, "peak": tpk, "peak_kind": tpk_kind, "unit": "TFLOP/s", "bound": "tensor",
+              "ncu": PREFILL_NCU}
         for key, (R_, ctx_, C_) in (("long_chunk", (4, 16384, 2048)), ("config3_chunk", (8, 2048, 512))):
             s_ = prefill_sample(P, torch, local, R_, ctx_, C_)
             s_["frac"] = round(s_["tflops"] / tpk, 4)
@@ -1030,6 +1029,14 @@ def run_config5(args):
         dist.destroy_process_group()
 
 
+# head dim 128 runs the ping-pong kernel (skv_prefill.cu prefill_pp_kernel; SKV_PREFILL_PP=0: the
+# one-tile-per-CTA prefill_kernel<T, 128>)
+PREFILL_KERNEL = ("skv prefill_pp_kernel<T> (cta_group::2 tcgen05.mma, two query tiles per CTA, TMA, TMEM)"
+                  if os.environ.get("SKV_PREFILL_PP", "1") != "0" else
+                  "skv prefill_kernel<T, 128> (cta_group::2 tcgen05.mma, TMA, TMEM)")
+PREFILL_NCU = "profiles/r02_ncu_prefill_pp.txt (tensor pipe active % of cycles)"
+
+
 def prefill_sample(P, torch, device, R, ctx, C, steps=10, warmup=3, services=None, check=True):
     """Chunked prefill (tcgen05 CTA-pair kernel) on its own pool: the config-2 services, R
     requests each, the last C tokens of a ctx-token context attending causally (layer 0),
@@ -1220,10 +1227,10 @@ def run_prefill(args):
                 "h2d_bytes_per_step": int(io_bytes), "d2h_bytes_per_step": int(io_bytes),
                 "ms_per_step": round(e2e_ms, 4),
                 "note": "per-service launches, H2D / D2H on their own streams overlapping the other services' prefill"},
-        "roofline": {"bound": "tensor", "kernel": "skv prefill_kernel_v10 (cta_group::2 tcgen05.mma)",
+        "roofline": {"bound": "tensor", "kernel": PREFILL_KERNEL,
                      "achieved": round(tflops, 1), "peak": peak, "peak_kind": peak_kind, "unit": "TFLOP/s",
                      "frac": round(tflops / peak, 4), "traffic": None,
-                     "ncu": "profiles/r01_ncu_prefill_v10_final.txt (tensor pipe active % of cycles)"},
+                     "ncu": PREFILL_NCU},
         "gpu_launches": int(launches), "clocks": clk.summary(),
     }
     if cpu:

@@ -113,3 +113,25 @@ def test_prefill_randomised_services(seed):
     layer = int(rng.integers(0, min(L for L, _, _ in shapes)))
     dtype = P.BF16 if seed % 3 == 0 else P.FP16
     run_prefill_check(shapes, ctxs, q_len=q_len, layer=layer, dtype=dtype, seed=seed)
+
+
+@pytest.mark.parametrize("q_len,G", [(129, 1), (385, 1), (513, 1), (200, 2), (97, 8)])
+def test_prefill_pingpong_partial_items(q_len, G):
+    """Ping-pong kernel items are four 128-row query tiles (A: rows 0-255, B: 256-511 of the
+    item); chunks ending inside A or B leave whole tiles of tail rows (masked, never stored)."""
+    run_prefill_check([(2, 2, 2 * G)], [[q_len + 700, q_len + 33]], q_len=q_len, layer=1)
+
+
+def test_prefill_one_tile_kernel_still_matches(tmp_path):
+    """SKV_PREFILL_PP=0 selects the one-query-tile-per-CTA kernel for head dim 128 (read once per
+    process): run a few of this module's checks in a fresh interpreter with it set."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, SKV_PREFILL_PP="0")
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", os.path.join(here, "test_gpu_prefill.py"),
+                        "-k", "gqa_folded or ragged or randomised_services or peaky or bf16"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
