@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(128, 1) bench(int iters, long long* out) {
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
         const uint64_t bd = make_desc(sb + st + (kk >> 2) * 8192 + (kk & 3) * 32, 16, 1024);
-        const uint32_t d = tmem + (N == 128 ? (kk & 1) * 128 : 0);
+        const uint32_t d = tmem + (N <= 128 ? (kk & 1) * N : 0);
         if (TS) {
           if (CG == 2)
             asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d), "r"(tmem + 384 + kk * 8), "l"(bd), "r"(idesc), "r"(1));
@@ -144,9 +144,13 @@ void run(long long* d) {
            VARY ? "walking" : "fixed  ", clk / iters, N / 2, flops / ms / 1e9, clk / ms / 1e6);
   }
 }
-int main() {
+int main(int argc, char**) {
   long long* d;
   cudaMalloc(&d, 148 * sizeof(long long));
+  if (argc > 1) {  // N = 64 shapes only
+    run<1, 64, 0, 1>(d); run<1, 64, 1, 1>(d); run<2, 64, 0, 1>(d); run<2, 64, 1, 1>(d); run<2, 128, 0, 1>(d);
+    return 0;
+  }
   run<1, 128, 0, 1>(d); run<1, 128, 1, 1>(d); run<1, 256, 0, 1>(d); run<1, 256, 1, 1>(d);
   run<2, 128, 0, 1>(d); run<2, 128, 1, 1>(d); run<2, 256, 0, 1>(d); run<2, 256, 1, 1>(d);
   run<2, 128, 1, 0>(d); run<1, 128, 1, 0>(d);
