@@ -10,8 +10,9 @@
 // prefill_kernel<T, D> (head dim D = 64, 128, 256): CTA pairs, one 256-row
 // tcgen05.mma.cta_group::2 per K=16 step (N = 128 keys for S = Q.K^T, N = D dims for
 // O += P.V), K/V halves per SM by TMA, S double-buffered in TMEM, persistent with a dynamic
-// work counter.  (Earlier single-CTA variants v2-v9 are in git history; DESIGN.md §5 has
-// their measurements.)
+// work counter.  prefill_pp_kernel<T> (head dim 128, the default for it): the same pairs with
+// two query tiles per CTA and one softmax warpgroup each (ping-pong, see below).  (Earlier
+// single-CTA variants v2-v9 are in git history; DESIGN.md §5.2 has the measurements.)
 //
 // UMMA operand layouts (cute canonical): K-major SW128 atoms of [8 rows x 64 elements]
 // (128 B rows, 16-byte chunk c of row r at chunk c ^ (r%8)) for Q and K — a [R x D] tile is
@@ -189,16 +190,6 @@ constexpr int kThreadsV3 = (kSoftmaxWarps + 2) * 32;
 
 __device__ __forceinline__ void mbar_init_n(uint64_t* b, uint32_t n) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(n));
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* tmap, int x, int y, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-          dst),
-      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(x), "r"(y), "r"(smem_u32(bar))
-      : "memory");
 }
 __device__ __forceinline__ void mbar_expect_tx_v3(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
@@ -1072,26 +1063,7 @@ __device__ __forceinline__ float2 ex2_emu2(float2 x) {
 #define SKV_PP_EMU 6  // exponential pairs of every 16 (per 32 keys) computed by ex2_emu2 (swept: 0-10, 6 best)
 #endif
 
-// warp-wide issue: the whole (converged) warp runs the MMA loop, one elected lane issues --
-// descriptors stay warp-uniform, no per-MMA lane-select loop
-__device__ __forceinline__ void mma_ss_pair_e(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                              uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
-}
-__device__ __forceinline__ void mma_ts_pair_e(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
-                                              uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(acc));
-}
+// warp-wide issue: the whole (converged) warp runs the MMA loop, one elected lane issues
 // eight K=16 steps of one tile in one asm block: one elect, only the descriptors' low words
 // move (immediate steps: Q atom column 16 KiB / K atom column 8 KiB per 4 steps, 32 B per step;
 // V 2 KiB and P 8 TMEM columns per step), high words are compile-time constants; `acc0` =
