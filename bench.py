@@ -669,10 +669,39 @@ def run_gpu(args):
         result["prefill"] = pf
     if rank == 0 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(cache, batch, q, args)
+    if rank == 0 and world == 1 and not args.no_faithful and args.workload == "config2" and args.phys_layers > 0:
+        # SURVEY §8d run (B) in the same driver run: the layer-sliced pool is released, then the
+        # capacity-faithful config 2 (every layer stored, 38 requests per service, ~152 GB) is timed
+        batch.close()
+        cache.close()
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        result["capacity_faithful"] = faithful_sample()
     if rank == 0:
         print(json.dumps(result), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def faithful_sample(steps=5, warmup=3, timeout=600):
+    """Config 2 with every layer stored (bench.py --phys-layers 0 --requests 38) in a child
+    process; returns the headline numbers of its line."""
+    import subprocess
+
+    cmd = [sys.executable, os.path.abspath(__file__), "--workload", "config2", "--phys-layers", "0", "--requests", "38",
+           "--steps", str(steps), "--warmup", str(warmup), "--no-prefill", "--no-cpu-baseline", "--no-faithful"]
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, env=dict(os.environ, WORLD_SIZE="1"))
+        line = [x for x in r.stdout.splitlines() if x.startswith("{")][-1]
+        d = json.loads(line)
+    except Exception as e:  # noqa: BLE001
+        return {"error": f"{type(e).__name__}: {e}"[:300]}
+    rf = d.get("roofline", {})
+    return {"value": d["value"], "unit": d["unit"], "ms_per_step": d["ms_per_step"], "steps": steps,
+            "e2e": d.get("e2e", {}).get("value"), "roofline_frac": rf.get("frac"), "achieved": rf.get("achieved"),
+            "peak": rf.get("peak"), "pool_gb": d["config"].get("pool_gb"), "requests": d["config"].get("requests"),
+            "parity_max_abs": d.get("parity", {}).get("max_abs"), "clocks": d.get("clocks"),
+            "workload": d["config"].get("workload"), "cmd": " ".join(cmd[1:])}
 
 
 def headline_parity(torch, cache, batch, q, k, v, stream, nlayers, per_end=2, tol=2e-3):
@@ -1387,6 +1416,8 @@ def main():
     ap.add_argument("--share-gpu", dest="share_gpu", action="store_true",
                     help="dry run of the N-rank path on a box with fewer GPUs: every rank on GPU 0, gloo "
                          "(functional only; the numbers are meaningless)")
+    ap.add_argument("--no-faithful", dest="no_faithful", action="store_true",
+                    help="skip the capacity-faithful config-2 sample (every layer stored) in the default line")
     ap.add_argument("--no-prefill", dest="no_prefill", action="store_true",
                     help="skip the chunked-prefill sample in the decode line")
     ap.add_argument("--no-parity", dest="no_parity", action="store_true",

@@ -21,7 +21,7 @@ def _run(*args):
 
 
 def test_bench_decode_small():
-    d = _run("--workload", "config2", "--requests", "8", "--ctx", "512")
+    d = _run("--workload", "config2", "--requests", "8", "--ctx", "512", "--no-faithful", "--no-prefill")
     for key in ("metric", "value", "unit", "e2e", "roofline", "gpu_launches", "clocks", "config"):
         assert key in d, key
     assert d["value"] > 0 and d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
@@ -40,3 +40,13 @@ def test_bench_gpus2_dry_run_without_torchrun():
     assert d["n_gpus"] == 2 and d["value"] > 0
     assert d["allreduce"]["group_size"] == 2 and d["allreduce"]["per_layer_ms_rank0"] > 0
     assert d["parity"]["ok"], d["parity"]
+
+
+def test_bench_capacity_faithful_sample():
+    """The default decode line also times config 2 with every layer stored (SURVEY §8d run (B),
+    ~152 GB pool) after releasing the layer-sliced pool, and reports it under capacity_faithful."""
+    d = _run("--workload", "config2", "--requests", "8", "--ctx", "512", "--no-prefill")
+    cf = d["capacity_faithful"]
+    assert "error" not in cf, cf
+    assert cf["value"] > 0 and cf["requests"] == 152 and cf["pool_gb"] > 100
+    assert cf["parity_max_abs"] is not None and cf["parity_max_abs"] <= 2e-3
