@@ -677,19 +677,22 @@ def run_gpu(args):
         torch.cuda.synchronize()
         torch.cuda.empty_cache()
         result["capacity_faithful"] = faithful_sample()
+        if not args.no_config4:  # BASELINE configs[3]: long contexts (lognormal, <= 32K), ~150 GB faithful pool
+            result["config4"] = faithful_sample(["--workload", "config4"])
     if rank == 0:
         print(json.dumps(result), flush=True)
     if dist:
         dist.destroy_process_group()
 
 
-def faithful_sample(steps=5, warmup=3, timeout=600):
-    """Config 2 with every layer stored (bench.py --phys-layers 0 --requests 38) in a child
-    process; returns the headline numbers of its line."""
+def faithful_sample(workload=("--workload", "config2", "--phys-layers", "0", "--requests", "38"), steps=5, warmup=3,
+                    timeout=600):
+    """A faithful-pool workload (default: config 2 with every layer stored) in a child process,
+    after the parent released its pool; returns the headline numbers of the child's line."""
     import subprocess
 
-    cmd = [sys.executable, os.path.abspath(__file__), "--workload", "config2", "--phys-layers", "0", "--requests", "38",
-           "--steps", str(steps), "--warmup", str(warmup), "--no-prefill", "--no-cpu-baseline", "--no-faithful"]
+    cmd = [sys.executable, os.path.abspath(__file__), *workload, "--steps", str(steps), "--warmup", str(warmup),
+           "--no-prefill", "--no-cpu-baseline", "--no-faithful"]
     try:
         r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, env=dict(os.environ, WORLD_SIZE="1"))
         line = [x for x in r.stdout.splitlines() if x.startswith("{")][-1]
@@ -1417,7 +1420,9 @@ def main():
                     help="dry run of the N-rank path on a box with fewer GPUs: every rank on GPU 0, gloo "
                          "(functional only; the numbers are meaningless)")
     ap.add_argument("--no-faithful", dest="no_faithful", action="store_true",
-                    help="skip the capacity-faithful config-2 sample (every layer stored) in the default line")
+                    help="skip the capacity-faithful config-2 and config-4 samples in the default line")
+    ap.add_argument("--no-config4", dest="no_config4", action="store_true",
+                    help="skip only the config-4 sample in the default line")
     ap.add_argument("--no-prefill", dest="no_prefill", action="store_true",
                     help="skip the chunked-prefill sample in the decode line")
     ap.add_argument("--no-parity", dest="no_parity", action="store_true",

@@ -44,8 +44,10 @@ def test_bench_gpus2_dry_run_without_torchrun():
 
 def test_bench_capacity_faithful_sample():
     """The default decode line also times config 2 with every layer stored (SURVEY §8d run (B),
-    ~152 GB pool) after releasing the layer-sliced pool, and reports it under capacity_faithful."""
+    ~152 GB pool) and config 4 (long contexts, ~150 GB pool) after releasing the layer-sliced pool,
+    and reports them under capacity_faithful and config4."""
     d = _run("--workload", "config2", "--requests", "8", "--ctx", "512", "--no-prefill")
+    assert "error" not in d["config4"] and d["config4"]["value"] > 0, d["config4"]
     cf = d["capacity_faithful"]
     assert "error" not in cf, cf
     assert cf["value"] > 0 and cf["requests"] == 152 and cf["pool_gb"] > 100
