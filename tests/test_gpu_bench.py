@@ -47,7 +47,9 @@ def test_bench_capacity_faithful_sample():
     ~152 GB pool) and config 4 (long contexts, ~150 GB pool) after releasing the layer-sliced pool,
     and reports them under capacity_faithful and config4."""
     d = _run("--workload", "config2", "--requests", "8", "--ctx", "512", "--no-prefill")
-    assert "error" not in d["config4"] and d["config4"]["value"] > 0, d["config4"]
+    for key in ("config4", "config1", "config3"):
+        assert "error" not in d[key] and d[key]["value"] > 0, d[key]
+    assert d["config3"]["churn"]["iterations"] > 0
     cf = d["capacity_faithful"]
     assert "error" not in cf, cf
     assert cf["value"] > 0 and cf["requests"] == 152 and cf["pool_gb"] > 100
