@@ -291,3 +291,14 @@ def test_append_ragged_counts_byte_exact():
                      u16(vv[off:off + n][None]))
             off += n
     assert np.array_equal(before, after)
+
+
+def test_prefill_long_context_bf16_gqa():
+    """A 64-token chunk at 16K / 9K context (ping-pong items walking ~130 K/V tiles), bf16."""
+    prefill_check([(1, 2, 8, 128)], [[16384, 9000]], 64, layer=0, dtype=P.BF16)
+
+
+def test_prefill_peaky_ragged_rescale_path():
+    """Large-magnitude q (the running max jumps inside tiles: O, l and already stored P chunks are
+    rescaled) with ragged chunk lengths crossing ping-pong item boundaries."""
+    prefill_check([(2, 2, 8, 128), (2, 4, 4, 128)], [[900, 300], [1500]], [300, 77, 640], layer=1, qamp=6.0)
