@@ -988,58 +988,22 @@ __device__ __forceinline__ void tmem_st16_nowait(uint32_t taddr, const uint32_t*
       : "memory");
 }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ void tmem_ld16_issue(uint32_t taddr, uint32_t (&r)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;"
-               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
-                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
-                 "+r"(r[15])
-               :
-               : "memory");
-}
-template <typename T>
-__device__ __forceinline__ float2 unpack2(uint32_t u);
-template <>
-__device__ __forceinline__ float2 unpack2<__half>(uint32_t u) {
-  return __half22float2(*reinterpret_cast<__half2*>(&u));
-}
-template <>
-__device__ __forceinline__ float2 unpack2<__nv_bfloat16>(uint32_t u) {
-  return __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&u));
-}
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
   float r;
   asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
   return r;
 }
 
-// Rare path of the ping-pong softmax (a 32-key chunk raised a row's reference max by more than
-// 2^kRescale): O (through the previous tile) and the P chunks already stored for this tile are
-// rescaled by alpha in TMEM.  Out of line to keep the hot loop small (instruction cache).
-template <typename T>
-__device__ __noinline__ void pp_rescale(uint32_t tO, uint32_t tS, int c, float alpha) {
+// Rare path of the ping-pong softmax (a tile raised a row's running max by more than
+// 2^kRescale): O (through the previous tile; that P.V has retired) is rescaled by alpha in
+// TMEM.  Out of line to keep the hot loop small (instruction cache).
+__device__ __noinline__ void pp_rescale_o(uint32_t tO, float alpha) {
   for (int cc = 0; cc < 4; ++cc) {
     float o[32];
     tmem_ld32(tO + cc * 32, o);
 #pragma unroll
     for (int kk = 0; kk < 32; ++kk) o[kk] *= alpha;
     tmem_st32(tO + cc * 32, o);
-  }
-  tmem_wait_st();  // P chunks < c stored
-  for (int cc = 0; cc < c; ++cc) {
-    uint32_t q[16];
-    tmem_ld16_issue(tS + 16 * cc, q);
-#pragma unroll
-    for (int kk = 0; kk < 16; ++kk) {
-      const float2 f = unpack2<T>(q[kk]);
-      q[kk] = pack2<T>(f.x * alpha, f.y * alpha);
-    }
-    tmem_st16u(tS + 16 * cc, q);
   }
 }
 
@@ -1138,6 +1102,53 @@ __device__ __forceinline__ void pv8_pair(uint32_t tmem_d, uint32_t tmem_a, uint3
       "}"
       ::"r"(tmem_d), "r"(tmem_a), "r"(blo), "r"(idesc), "r"(acc0), "n"(BHI));
 }
+// half a P.V tile (K-steps [4*HALF, 4*HALF+4), keys 64*HALF..): the softmax hands P over in two
+// 64-key halves, so the first half's MMAs overlap the second half's exponentials
+template <uint32_t BHI, int HALF>
+__device__ __forceinline__ void pv4_pair(uint32_t tmem_d, uint32_t tmem_a, uint32_t blo, uint32_t idesc, uint32_t acc0) {
+  if constexpr (HALF == 0)
+    asm volatile(
+        "{\n\t.reg .pred e, p;\n\t"
+      ".reg .b32 a<4>, bl<4>, bh;\n\t.reg .b64 b<4>;\n\t"
+      "mov.b32 bh, %5;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "add.u32 a0, %1, 0;\n\t"
+      "add.u32 bl0, %2, 0;\n\tmov.b64 b0, {bl0, bh};\n\t"
+      "add.u32 a1, %1, 8;\n\t"
+      "add.u32 bl1, %2, 128;\n\tmov.b64 b1, {bl1, bh};\n\t"
+      "add.u32 a2, %1, 16;\n\t"
+      "add.u32 bl2, %2, 256;\n\tmov.b64 b2, {bl2, bh};\n\t"
+      "add.u32 a3, %1, 24;\n\t"
+      "add.u32 bl3, %2, 384;\n\tmov.b64 b3, {bl3, bh};\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a0], b0, %3, p;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a1], b1, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a2], b2, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a3], b3, %3, 1;\n\t"
+      "}"
+        ::"r"(tmem_d), "r"(tmem_a), "r"(blo), "r"(idesc), "r"(acc0), "n"(BHI));
+  else
+    asm volatile(
+        "{\n\t.reg .pred e, p;\n\t"
+      ".reg .b32 a<4>, bl<4>, bh;\n\t.reg .b64 b<4>;\n\t"
+      "mov.b32 bh, %5;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "add.u32 a0, %1, 32;\n\t"
+      "add.u32 bl0, %2, 512;\n\tmov.b64 b0, {bl0, bh};\n\t"
+      "add.u32 a1, %1, 40;\n\t"
+      "add.u32 bl1, %2, 640;\n\tmov.b64 b1, {bl1, bh};\n\t"
+      "add.u32 a2, %1, 48;\n\t"
+      "add.u32 bl2, %2, 768;\n\tmov.b64 b2, {bl2, bh};\n\t"
+      "add.u32 a3, %1, 56;\n\t"
+      "add.u32 bl3, %2, 896;\n\tmov.b64 b3, {bl3, bh};\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a0], b0, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a1], b1, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a2], b2, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a3], b3, %3, 1;\n\t"
+      "}"
+        ::"r"(tmem_d), "r"(tmem_a), "r"(blo), "r"(idesc), "r"(acc0), "n"(BHI));
+}
 __device__ __forceinline__ void commit_pair_e(uint64_t* bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"
@@ -1163,8 +1174,9 @@ __global__ void __launch_bounds__(pp::kThreads, 1) prefill_pp_kernel(const __gri
   uint64_t* p_full = bars + 2 * ST + 2;     // [X] leader: 8 warp arrivals per tile
   uint64_t* s_full = bars + 2 * ST + 4;     // [X] both CTAs (multicast commit)
   uint64_t* o_done = bars + 2 * ST + 6;     // [X] both CTAs: the item's last P.V retired
-  uint64_t* item_full = bars + 2 * ST + 8;  // [kRing] both CTAs
-  int* ring = reinterpret_cast<int*>(bars + 2 * ST + 8 + kRing);
+  uint64_t* p_half = bars + 2 * ST + 8;     // [X] leader: 8 warp arrivals per tile (P keys 0-63 stored)
+  uint64_t* item_full = bars + 2 * ST + 10; // [kRing] both CTAs
+  int* ring = reinterpret_cast<int*>(bars + 2 * ST + 10 + kRing);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + kRing);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t rank = cluster_rank();
@@ -1186,6 +1198,7 @@ __global__ void __launch_bounds__(pp::kThreads, 1) prefill_pp_kernel(const __gri
     for (int x = 0; x < 2; ++x) {
       mbar_init_n(&q_full[x], 8);
       mbar_init_n(&p_full[x], 8);
+      mbar_init_n(&p_half[x], 8);
       mbar_init_n(&s_full[x], 1);
       mbar_init_n(&o_done[x], 1);
     }
@@ -1343,8 +1356,14 @@ __global__ void __launch_bounds__(pp::kThreads, 1) prefill_pp_kernel(const __gri
                              idesc_qk, 0u);
           commit_pair_e(&s_full[x]);
         };
-        auto pv = [&](int x, int j, const uint64_t (&d)[8]) {
-          pv8_pair<kHi>(tm + kOCol + 128 * x, tm + kSCol + 128 * x, (uint32_t)d[0], idesc_pv, j > 0 ? 1u : 0u);
+        auto pv = [&](int x, int j, const uint64_t (&d)[8]) {  // waits for the two P halves itself
+          const uint32_t gj = j0 + j;
+          PF_T(2 + x, mbar_wait(&p_half[x], gj & 1));
+          tc_fence_after();
+          pv4_pair<kHi, 0>(tm + kOCol + 128 * x, tm + kSCol + 128 * x, (uint32_t)d[0], idesc_pv, j > 0 ? 1u : 0u);
+          PF_T(2 + x, mbar_wait(&p_full[x], gj & 1));
+          tc_fence_after();
+          pv4_pair<kHi, 1>(tm + kOCol + 128 * x, tm + kSCol + 128 * x, (uint32_t)d[0], idesc_pv, 1u);
           if (j == J - 1) commit_pair_e(&o_done[x]);
         };
         {
@@ -1366,16 +1385,12 @@ __global__ void __launch_bounds__(pp::kThreads, 1) prefill_pp_kernel(const __gri
           k_descs(j + 1, kd);
           pin(vd, 8);
           pin(kd, 8);
-          PF_T(2, mbar_wait(&p_full[0], gj & 1));
-          tc_fence_after();
-          PF_T(4, pv(0, j, vd));
+          pv(0, j, vd);
           if (j + 1 < J) {
             wait_kv(j + 1);
             PF_T(4, qk(0, kd));
           }
-          PF_T(3, mbar_wait(&p_full[1], gj & 1));
-          tc_fence_after();
-          PF_T(4, pv(1, j, vd));
+          pv(1, j, vd);
           commit_pair_e(&kv_empty[gj % ST]);
           if (j + 1 < J) PF_T(4, qk(1, kd));
         }
@@ -1391,7 +1406,8 @@ __global__ void __launch_bounds__(pp::kThreads, 1) prefill_pp_kernel(const __gri
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     const uint32_t tS = tmem + kSCol + 128 * x + lane_off;
     const uint32_t tO = tmem + kOCol + 128 * x + lane_off;
-    const uint32_t q_full_l = mapa_u32(smem_u32(&q_full[x]), 0), p_full_l = mapa_u32(smem_u32(&p_full[x]), 0);
+    const uint32_t q_full_l = mapa_u32(smem_u32(&q_full[x]), 0), p_full_l = mapa_u32(smem_u32(&p_full[x]), 0),
+                   p_half_l = mapa_u32(smem_u32(&p_half[x]), 0);
     char* qtile = qbase + x * kQTile;
     auto install_q = [&](const Geo& e) {  // this thread's Q row into the tile's SW128 K-major layout
       const int t0 = e.t0Q + (2 * x + (int)rank) * e.tpt;
@@ -1439,92 +1455,81 @@ __global__ void __launch_bounds__(pp::kThreads, 1) prefill_pp_kernel(const __gri
         }
         const bool masked = (j * kKT + kKT - 1 > e.start + t0) || tail_rows;
         const int kb = j * kKT;
-#ifndef SKV_PP_STEP
-#define SKV_PP_STEP 64  // key columns per softmax step (one TMEM-load wait, one max vote)
-#endif
-        constexpr int SW = SKV_PP_STEP;
-        // one step: SW scores of this row -> masked, max-checked, exponentiated, P stored at
-        // packed column h*SW/2 (P(h) overwrites only S columns the steps <= h have consumed)
-        auto step = [&](uint32_t (&r)[SW], int h) {
+        {  // both 64-key halves loaded, one exact tile max and vote, then P handed over per half
+          uint32_t ra[64], rb[64];
+#pragma unroll
+          for (int q = 0; q < 2; ++q) tmem_ld32_issue(tS + 32 * q, *reinterpret_cast<uint32_t(*)[32]>(ra + 32 * q));
+#pragma unroll
+          for (int q = 0; q < 2; ++q) tmem_ld32_issue(tS + 64 + 32 * q, *reinterpret_cast<uint32_t(*)[32]>(rb + 32 * q));
+#pragma unroll
+          for (int q = 0; q < 2; ++q) tmem_ld32_wait(*reinterpret_cast<uint32_t(*)[32]>(ra + 32 * q));
+#pragma unroll
+          for (int q = 0; q < 2; ++q) tmem_ld32_wait(*reinterpret_cast<uint32_t(*)[32]>(rb + 32 * q));
           if (masked) {
 #pragma unroll
-            for (int kk = 0; kk < SW; ++kk)
-              if (!(row_ok && kb + SW * h + kk <= my_pos)) r[kk] = __float_as_uint(-INFINITY);
+            for (int kk = 0; kk < 64; ++kk) {
+              if (!(row_ok && kb + kk <= my_pos)) ra[kk] = __float_as_uint(-INFINITY);
+              if (!(row_ok && kb + 64 + kk <= my_pos)) rb[kk] = __float_as_uint(-INFINITY);
+            }
           }
-          float mx4[4] = {__uint_as_float(r[0]), __uint_as_float(r[1]), __uint_as_float(r[2]), __uint_as_float(r[3])};
+          float mx4[4] = {__uint_as_float(ra[0]), __uint_as_float(ra[1]), __uint_as_float(rb[0]), __uint_as_float(rb[1])};
 #pragma unroll
-          for (int kk = 4; kk < SW; kk += 8)  // four independent 3-input max chains
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-              mx4[u] = kk + 2 * u + 1 < SW ? fmax3(mx4[u], __uint_as_float(r[kk + 2 * u]), __uint_as_float(r[kk + 2 * u + 1]))
-                                           : mx4[u];
+          for (int kk = 2; kk < 64; kk += 4) {
+            mx4[0] = fmax3(mx4[0], __uint_as_float(ra[kk]), __uint_as_float(ra[kk + 1]));
+            mx4[1] = fmax3(mx4[1], __uint_as_float(ra[kk + 2]), __uint_as_float(ra[kk + 3]));
+            mx4[2] = fmax3(mx4[2], __uint_as_float(rb[kk]), __uint_as_float(rb[kk + 1]));
+            mx4[3] = fmax3(mx4[3], __uint_as_float(rb[kk + 2]), __uint_as_float(rb[kk + 3]));
+          }
           const float mt = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * c2;
-          if (j == 0 && h == 0) m = mt;  // first step of an item: the reference is its max
-          const bool need = mt > m + kRescale;
-          if (__any_sync(0xffffffffu, need)) {  // raise the reference max: rescale O, l and stored P
-            const float mn = need ? mt : m;
-            const float alpha = need ? ex2(m - mn) : 1.f;
-            m = mn;
-            lsum.x *= alpha;
-            lsum.y *= alpha;
-            pp_rescale<T>(tO, tS, h * (SW / 32) * 2, alpha);
+          if (j == 0) {
+            m = mt;
+          } else {
+            const bool need = mt > m + kRescale;
+            if (__any_sync(0xffffffffu, need)) {  // raise the max: rescale O and l (no P of this tile yet)
+              const float mn = need ? mt : m;
+              const float alpha = need ? ex2(m - mn) : 1.f;
+              m = mn;
+              lsum.x *= alpha;
+              lsum.y *= alpha;
+              pp_rescale_o(tO, alpha);
+            }
           }
           const float mu = m == -INFINITY ? 0.f : m;
           const float2 c2v = make_float2(c2, c2), nmv = make_float2(-mu, -mu);
-          uint32_t pk[SW / 2];
-          float2 v[SW / 2];
+          auto exps32 = [&](const uint32_t* r, uint32_t col) {  // 32 keys -> 16 packed P columns at col
+            uint32_t pk[16];
+            float2 v[16];
 #pragma unroll
-          for (int i = 0; i < SW / 2; ++i) {
-            const float2 a = __ffma2_rn(make_float2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])), c2v, nmv);
-            if ((i & 15) >= 16 - SKV_PP_EMU) v[i] = ex2_emu2(a);
-            else v[i] = make_float2(ex2(a.x), ex2(a.y));
+            for (int i = 0; i < 16; ++i) {
+              const float2 a = __ffma2_rn(make_float2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])), c2v, nmv);
+              if (i >= 16 - SKV_PP_EMU) v[i] = ex2_emu2(a);
+              else v[i] = make_float2(ex2(a.x), ex2(a.y));
+            }
+#pragma unroll
+            for (int i = 0; i < 16; ++i) pk[i] = pack2<T>(v[i].x, v[i].y);
+#pragma unroll
+            for (int w = 8; w >= 1; w >>= 1)
+#pragma unroll
+              for (int i = 0; i < w; ++i) v[i] = __fadd2_rn(v[i], v[i + w]);
+            lsum = __fadd2_rn(lsum, v[0]);
+            tmem_st16_nowait(tS + col, pk);
+          };
+          exps32(ra, 0);
+          exps32(ra + 32, 16);
+          tmem_wait_st();
+          if (x == 0 && last_partial) fence_async_smem();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if (x == 0 && last_partial) mbar_arrive_cluster(p_half_l);  // orders the V-row zeroing
+            else mbar_arrive_cluster_relaxed(p_half_l);
           }
-#pragma unroll
-          for (int i = 0; i < SW / 2; ++i) pk[i] = pack2<T>(v[i].x, v[i].y);
-#pragma unroll
-          for (int w = SW / 4; w >= 1; w >>= 1)  // pairwise sums
-#pragma unroll
-            for (int i = 0; i < w; ++i) v[i] = __fadd2_rn(v[i], v[i + w]);
-          lsum = __fadd2_rn(lsum, v[0]);
-#pragma unroll
-          for (int q = 0; q < SW / 32; ++q) tmem_st16_nowait(tS + h * (SW / 2) + 16 * q, pk + 16 * q);
-        };
-#if SKV_PP_STEP == 64 && !defined(SKV_PP_NOPREFETCH)
-        {  // the second step's scores load while the first step computes
-          uint32_t ra[64], rb[64];
-          auto& ra0 = *reinterpret_cast<uint32_t(*)[32]>(ra);
-          auto& ra1 = *reinterpret_cast<uint32_t(*)[32]>(ra + 32);
-          auto& rb0 = *reinterpret_cast<uint32_t(*)[32]>(rb);
-          auto& rb1 = *reinterpret_cast<uint32_t(*)[32]>(rb + 32);
-          tmem_ld32_issue(tS, ra0);
-          tmem_ld32_issue(tS + 32, ra1);
-          tmem_ld32_wait(ra0);
-          tmem_ld32_wait(ra1);
-          tmem_ld32_issue(tS + 64, rb0);
-          tmem_ld32_issue(tS + 96, rb1);
-          step(ra, 0);
-          tmem_ld32_wait(rb0);
-          tmem_ld32_wait(rb1);
-          step(rb, 1);
-        }
-#else
-#pragma unroll
-        for (int h = 0; h < 128 / SW; ++h) {
-          uint32_t r[SW];
-#pragma unroll
-          for (int q = 0; q < SW / 32; ++q) tmem_ld32_issue(tS + h * SW + 32 * q, *reinterpret_cast<uint32_t(*)[32]>(r + 32 * q));
-#pragma unroll
-          for (int q = 0; q < SW / 32; ++q) tmem_ld32_wait(*reinterpret_cast<uint32_t(*)[32]>(r + 32 * q));
-          step(r, h);
-        }
-#endif
-        tmem_wait_st();
-        if (x == 0 && last_partial) fence_async_smem();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          if (x == 0 && last_partial) mbar_arrive_cluster(p_full_l);  // orders the V-row zeroing
-          else mbar_arrive_cluster_relaxed(p_full_l);
+          exps32(rb, 32);
+          exps32(rb + 32, 48);
+          tmem_wait_st();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster_relaxed(p_full_l);
         }
       }
       tc += e.n_kt;
