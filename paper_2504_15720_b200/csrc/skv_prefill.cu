@@ -1102,14 +1102,13 @@ __device__ __forceinline__ void pv8_pair(uint32_t tmem_d, uint32_t tmem_a, uint3
       "}"
       ::"r"(tmem_d), "r"(tmem_a), "r"(blo), "r"(idesc), "r"(acc0), "n"(BHI));
 }
-// half a P.V tile (K-steps [4*HALF, 4*HALF+4), keys 64*HALF..): the softmax hands P over in two
-// 64-key halves, so the first half's MMAs overlap the second half's exponentials
-template <uint32_t BHI, int HALF>
-__device__ __forceinline__ void pv4_pair(uint32_t tmem_d, uint32_t tmem_a, uint32_t blo, uint32_t idesc, uint32_t acc0) {
-  if constexpr (HALF == 0)
+// a quarter of a P.V tile (K-steps [2Q, 2Q+2), keys 32Q..32Q+31)
+template <uint32_t BHI, int Q>
+__device__ __forceinline__ void pv2_pair(uint32_t tmem_d, uint32_t tmem_a, uint32_t blo, uint32_t idesc, uint32_t acc0) {
+  if constexpr (Q == 0)
     asm volatile(
         "{\n\t.reg .pred e, p;\n\t"
-      ".reg .b32 a<4>, bl<4>, bh;\n\t.reg .b64 b<4>;\n\t"
+      ".reg .b32 a<2>, bl<2>, bh;\n\t.reg .b64 b<2>;\n\t"
       "mov.b32 bh, %5;\n\t"
       "elect.sync _|e, 0xffffffff;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
@@ -1117,20 +1116,29 @@ __device__ __forceinline__ void pv4_pair(uint32_t tmem_d, uint32_t tmem_a, uint3
       "add.u32 bl0, %2, 0;\n\tmov.b64 b0, {bl0, bh};\n\t"
       "add.u32 a1, %1, 8;\n\t"
       "add.u32 bl1, %2, 128;\n\tmov.b64 b1, {bl1, bh};\n\t"
-      "add.u32 a2, %1, 16;\n\t"
-      "add.u32 bl2, %2, 256;\n\tmov.b64 b2, {bl2, bh};\n\t"
-      "add.u32 a3, %1, 24;\n\t"
-      "add.u32 bl3, %2, 384;\n\tmov.b64 b3, {bl3, bh};\n\t"
       "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a0], b0, %3, p;\n\t"
       "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a1], b1, %3, 1;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a2], b2, %3, 1;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a3], b3, %3, 1;\n\t"
       "}"
         ::"r"(tmem_d), "r"(tmem_a), "r"(blo), "r"(idesc), "r"(acc0), "n"(BHI));
-  else
+  else if constexpr (Q == 1)
     asm volatile(
         "{\n\t.reg .pred e, p;\n\t"
-      ".reg .b32 a<4>, bl<4>, bh;\n\t.reg .b64 b<4>;\n\t"
+      ".reg .b32 a<2>, bl<2>, bh;\n\t.reg .b64 b<2>;\n\t"
+      "mov.b32 bh, %5;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "add.u32 a0, %1, 16;\n\t"
+      "add.u32 bl0, %2, 256;\n\tmov.b64 b0, {bl0, bh};\n\t"
+      "add.u32 a1, %1, 24;\n\t"
+      "add.u32 bl1, %2, 384;\n\tmov.b64 b1, {bl1, bh};\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a0], b0, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a1], b1, %3, 1;\n\t"
+      "}"
+        ::"r"(tmem_d), "r"(tmem_a), "r"(blo), "r"(idesc), "r"(acc0), "n"(BHI));
+  else if constexpr (Q == 2)
+    asm volatile(
+        "{\n\t.reg .pred e, p;\n\t"
+      ".reg .b32 a<2>, bl<2>, bh;\n\t.reg .b64 b<2>;\n\t"
       "mov.b32 bh, %5;\n\t"
       "elect.sync _|e, 0xffffffff;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
@@ -1138,14 +1146,23 @@ __device__ __forceinline__ void pv4_pair(uint32_t tmem_d, uint32_t tmem_a, uint3
       "add.u32 bl0, %2, 512;\n\tmov.b64 b0, {bl0, bh};\n\t"
       "add.u32 a1, %1, 40;\n\t"
       "add.u32 bl1, %2, 640;\n\tmov.b64 b1, {bl1, bh};\n\t"
-      "add.u32 a2, %1, 48;\n\t"
-      "add.u32 bl2, %2, 768;\n\tmov.b64 b2, {bl2, bh};\n\t"
-      "add.u32 a3, %1, 56;\n\t"
-      "add.u32 bl3, %2, 896;\n\tmov.b64 b3, {bl3, bh};\n\t"
       "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a0], b0, %3, 1;\n\t"
       "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a1], b1, %3, 1;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a2], b2, %3, 1;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a3], b3, %3, 1;\n\t"
+      "}"
+        ::"r"(tmem_d), "r"(tmem_a), "r"(blo), "r"(idesc), "r"(acc0), "n"(BHI));
+  else if constexpr (Q == 3)
+    asm volatile(
+        "{\n\t.reg .pred e, p;\n\t"
+      ".reg .b32 a<2>, bl<2>, bh;\n\t.reg .b64 b<2>;\n\t"
+      "mov.b32 bh, %5;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "add.u32 a0, %1, 48;\n\t"
+      "add.u32 bl0, %2, 768;\n\tmov.b64 b0, {bl0, bh};\n\t"
+      "add.u32 a1, %1, 56;\n\t"
+      "add.u32 bl1, %2, 896;\n\tmov.b64 b1, {bl1, bh};\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a0], b0, %3, 1;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], [a1], b1, %3, 1;\n\t"
       "}"
         ::"r"(tmem_d), "r"(tmem_a), "r"(blo), "r"(idesc), "r"(acc0), "n"(BHI));
 }
@@ -1174,9 +1191,9 @@ __global__ void __launch_bounds__(pp::kThreads, 1) prefill_pp_kernel(const __gri
   uint64_t* p_full = bars + 2 * ST + 2;     // [X] leader: 8 warp arrivals per tile
   uint64_t* s_full = bars + 2 * ST + 4;     // [X] both CTAs (multicast commit)
   uint64_t* o_done = bars + 2 * ST + 6;     // [X] both CTAs: the item's last P.V retired
-  uint64_t* p_half = bars + 2 * ST + 8;     // [X] leader: 8 warp arrivals per tile (P keys 0-63 stored)
-  uint64_t* item_full = bars + 2 * ST + 10; // [kRing] both CTAs
-  int* ring = reinterpret_cast<int*>(bars + 2 * ST + 10 + kRing);
+  uint64_t* p_part = bars + 2 * ST + 8;     // [3][X] leader: 8 warp arrivals per tile (P keys < 32, 64, 96 stored)
+  uint64_t* item_full = bars + 2 * ST + 14; // [kRing] both CTAs
+  int* ring = reinterpret_cast<int*>(bars + 2 * ST + 14 + kRing);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ring + kRing);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t rank = cluster_rank();
@@ -1198,7 +1215,7 @@ __global__ void __launch_bounds__(pp::kThreads, 1) prefill_pp_kernel(const __gri
     for (int x = 0; x < 2; ++x) {
       mbar_init_n(&q_full[x], 8);
       mbar_init_n(&p_full[x], 8);
-      mbar_init_n(&p_half[x], 8);
+      for (int q = 0; q < 3; ++q) mbar_init_n(&p_part[2 * q + x], 8);
       mbar_init_n(&s_full[x], 1);
       mbar_init_n(&o_done[x], 1);
     }
@@ -1358,12 +1375,19 @@ __global__ void __launch_bounds__(pp::kThreads, 1) prefill_pp_kernel(const __gri
         };
         auto pv = [&](int x, int j, const uint64_t (&d)[8]) {  // waits for the two P halves itself
           const uint32_t gj = j0 + j;
-          PF_T(2 + x, mbar_wait(&p_half[x], gj & 1));
+          const uint32_t tO_ = tm + kOCol + 128 * x, tP_ = tm + kSCol + 128 * x, vlo = (uint32_t)d[0];
+          PF_T(2 + x, mbar_wait(&p_part[x], gj & 1));
           tc_fence_after();
-          pv4_pair<kHi, 0>(tm + kOCol + 128 * x, tm + kSCol + 128 * x, (uint32_t)d[0], idesc_pv, j > 0 ? 1u : 0u);
+          pv2_pair<kHi, 0>(tO_, tP_, vlo, idesc_pv, j > 0 ? 1u : 0u);
+          PF_T(2 + x, mbar_wait(&p_part[2 + x], gj & 1));
+          tc_fence_after();
+          pv2_pair<kHi, 1>(tO_, tP_, vlo, idesc_pv, 1u);
+          PF_T(2 + x, mbar_wait(&p_part[4 + x], gj & 1));
+          tc_fence_after();
+          pv2_pair<kHi, 2>(tO_, tP_, vlo, idesc_pv, 1u);
           PF_T(2 + x, mbar_wait(&p_full[x], gj & 1));
           tc_fence_after();
-          pv4_pair<kHi, 1>(tm + kOCol + 128 * x, tm + kSCol + 128 * x, (uint32_t)d[0], idesc_pv, 1u);
+          pv2_pair<kHi, 3>(tO_, tP_, vlo, idesc_pv, 1u);
           if (j == J - 1) commit_pair_e(&o_done[x]);
         };
         {
@@ -1407,7 +1431,7 @@ __global__ void __launch_bounds__(pp::kThreads, 1) prefill_pp_kernel(const __gri
     const uint32_t tS = tmem + kSCol + 128 * x + lane_off;
     const uint32_t tO = tmem + kOCol + 128 * x + lane_off;
     const uint32_t q_full_l = mapa_u32(smem_u32(&q_full[x]), 0), p_full_l = mapa_u32(smem_u32(&p_full[x]), 0),
-                   p_half_l = mapa_u32(smem_u32(&p_half[x]), 0);
+                   p_part_l = mapa_u32(smem_u32(&p_part[x]), 0);  // + 16 * q: quarter q's barrier
     char* qtile = qbase + x * kQTile;
     auto install_q = [&](const Geo& e) {  // this thread's Q row into the tile's SW128 K-major layout
       const int t0 = e.t0Q + (2 * x + (int)rank) * e.tpt;
@@ -1514,22 +1538,24 @@ __global__ void __launch_bounds__(pp::kThreads, 1) prefill_pp_kernel(const __gri
             lsum = __fadd2_rn(lsum, v[0]);
             tmem_st16_nowait(tS + col, pk);
           };
+          auto hand_over = [&](uint32_t bar, bool zeroed) {  // P columns stored so far -> MMA warp
+            tmem_wait_st();
+            if (zeroed) fence_async_smem();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+              if (zeroed) mbar_arrive_cluster(bar);  // orders the V-row zeroing
+              else mbar_arrive_cluster_relaxed(bar);
+            }
+          };
           exps32(ra, 0);
+          hand_over(p_part_l, x == 0 && last_partial);
           exps32(ra + 32, 16);
-          tmem_wait_st();
-          if (x == 0 && last_partial) fence_async_smem();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) {
-            if (x == 0 && last_partial) mbar_arrive_cluster(p_half_l);  // orders the V-row zeroing
-            else mbar_arrive_cluster_relaxed(p_half_l);
-          }
+          hand_over(p_part_l + 16, false);
           exps32(rb, 32);
+          hand_over(p_part_l + 32, false);
           exps32(rb + 32, 48);
-          tmem_wait_st();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_cluster_relaxed(p_full_l);
+          hand_over(p_full_l, false);
         }
       }
       tc += e.n_kt;
